@@ -1,0 +1,221 @@
+/* bp_cuda.h — C-ABI boundary of the B200-native block-wise denoising path.
+ *
+ * Drop-in for the reference `blockpipe` hot path (/root/reference/proj). The
+ * reference has no FFI of its own; its operator API is the C++ headers, and
+ * every entry point here replaces one of those functions (cited per entry).
+ * The C++ mirror in include/blockpipe/ (*.hpp) and the Python mirror in
+ * paper_2505_21070_b200/ both call through this header.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no C++ or torch types cross the boundary.
+ *  - Every call returns a bp_status that maps 1:1 onto the reference's
+ *    exception taxonomy (errors.hpp:11-41); bp_last_error() returns the
+ *    thread-local message of the last failure on the calling thread.
+ *  - Buffers are caller-owned. Arguments flagged *_is_device take device
+ *    pointers; all others are host memory.
+ *  - Handles are thread-affine (one host thread per stage, like one
+ *    DeviceWorker thread per device in engine.cpp:280-285).
+ *  - There is no CPU fallback: without a CUDA device every compute entry
+ *    returns BP_ERR_CUDA. Host-only entries (schedule, seeds) work anywhere.
+ */
+#ifndef BP_CUDA_H_
+#define BP_CUDA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.hpp:11-41) ------------------------------------ */
+typedef enum {
+  BP_OK = 0,
+  BP_ERR_CONFIG = 1,      /* ConfigError     */
+  BP_ERR_DIMENSION = 2,   /* DimensionError  */
+  BP_ERR_CACHE = 3,       /* CacheError      */
+  BP_ERR_SCHEDULER = 4,   /* SchedulerError  */
+  BP_ERR_QUEUE = 5,       /* QueueError      */
+  BP_ERR_SCHEDULING = 6,  /* SchedulingError */
+  BP_ERR_PARTITION = 7,   /* PartitionError (a ConfigError) */
+  BP_ERR_IO = 8,          /* IoError         */
+  BP_ERR_CUDA = 9,        /* CUDA runtime / no device */
+  BP_ERR_NCCL = 10,       /* NCCL transport  */
+  BP_ERR_INTERNAL = 11
+} bp_status;
+
+const char* bp_last_error(void);
+const char* bp_version(void);
+
+/* ---- enums mirroring the reference ---------------------------------------- */
+typedef enum { BP_ORDER_REVERSE = 0, BP_ORDER_SEQUENTIAL = 1 } bp_order; /* block_queue.hpp:13 */
+typedef enum { BP_CACHE_DISABLED = 0, BP_CACHE_CACHED = 1, BP_CACHE_RECOMPUTE = 2 } bp_cache_mode; /* model.hpp:103 */
+typedef enum {
+  BP_INIT_COORDINATED = 0, BP_INIT_COMPLETE_SHUFFLE = 1, BP_INIT_SUBSET = 2,
+  BP_INIT_FRESH = 3, BP_INIT_REPEAT = 4
+} bp_init_strategy; /* noise.hpp:29-35 */
+typedef enum {
+  BP_PREC_F64 = 0,   /* reference-order fp64 SIMT kernels (parity mode)         */
+  BP_PREC_F32 = 1,   /* fp32 verification mode (rel-L2 <= 1e-4)                  */
+  BP_PREC_BF16 = 2   /* tcgen05 bf16 tensor-core path, fp32 residual (<= 2e-2)  */
+} bp_precision;
+typedef enum { BP_TRANSPORT_LOOPBACK = 0, BP_TRANSPORT_NCCL = 1 } bp_transport;
+
+/* ModelConfig (model.hpp:21-32) + the defaulted FFN width extension. */
+typedef struct {
+  int32_t layers, hidden, heads, channels, height, width, context_len;
+  int32_t ffn; /* 0 => 4*hidden, the reference's fixed width (model.cpp:98-99) */
+} bp_model_desc;
+
+/* PipelineConfig (engine.hpp:24-38) + QueueParams (block_queue.hpp:36-43). */
+typedef struct {
+  int32_t devices;                 /* N pipeline stages */
+  int32_t order;                   /* bp_order */
+  int32_t cache_mode;              /* bp_cache_mode */
+  int32_t num_b, num_c, steps, block_num, retain_clean_context;
+  int32_t strategy;                /* bp_init_strategy */
+  bp_model_desc model;
+  uint64_t seed_model, seed_noise, seed_context;
+  int32_t fault_inject_ulp, record_trace, check_cache;
+  /* extensions */
+  int32_t precision;               /* bp_precision */
+  int32_t transport;               /* bp_transport */
+  int32_t uneven_split;            /* 1: allow L % N != 0 (contiguous, larger stages first) */
+  int32_t layer_split[64];         /* explicit per-stage layer counts; all 0 => automatic */
+} bp_pipeline_desc;
+
+/* ---- rng.hpp ---------------------------------------------------------------- */
+/* derive_seed (rng.cpp:51-60). Host-only. */
+uint64_t bp_derive_seed(uint64_t base, const uint64_t* tags, int32_t ntags);
+/* RandomSource(state).normal_tensor({n}, sigma) (rng.cpp:35-39) on the GPU,
+ * bit-exact (glibc log/cos port). Writes n doubles; returns the final state. */
+bp_status bp_normals(int32_t device, uint64_t state, int64_t n, double sigma, double* out,
+                     int32_t out_is_device, uint64_t* final_state);
+
+/* ---- noise.hpp -------------------------------------------------------------- */
+/* build_pool (noise.cpp:26-48): M = num_b + num_c/2 entries of H*W*C normals,
+ * drawn on the GPU. out holds M*H*W*C doubles (entry-major). */
+bp_status bp_noise_pool(int32_t device, int32_t num_b, int32_t num_c, const int64_t frame_shape[3],
+                        uint64_t noise_seed, double* out, int32_t out_is_device);
+
+/* ---- model.hpp: one pipeline stage (ModelChunk) -------------------------------- */
+typedef struct bp_stage bp_stage;
+
+/* build_chunk (model.cpp:109-128) + build_context (model.cpp:150-153): the
+ * stage's weights are generated on the device from (seed_model, layer, role). */
+bp_status bp_stage_create(int32_t device, const bp_model_desc* model, uint64_t seed_model,
+                          uint64_t seed_context, int32_t layer_begin, int32_t layer_end,
+                          int32_t precision, bp_stage** out);
+bp_status bp_stage_destroy(bp_stage* stage);
+
+/* ChunkInput (model.hpp:106-112), host fp64 payload. */
+typedef struct {
+  const double* payload;           /* chunk 0: [rows=tokens, cols=C]; else [tokens, h] */
+  int64_t rows, cols;
+  const int32_t* frame_levels;     /* nframes */
+  const int64_t* frame_ids;        /* nframes */
+  int32_t nframes;
+  const int32_t* capture_frames;   /* ncapture frame positions to snapshot */
+  int32_t ncapture;
+  int32_t record_inputs;
+  int32_t mode;                    /* bp_cache_mode */
+  int32_t use_prev;                /* 0: no prefix; 1: the stage's resident captured
+                                      K/V (KVCacheEntry); 2: its recorded inputs */
+} bp_chunk_in;
+
+/* ChunkOutput (model.hpp:114-118). payload is a caller buffer of
+ * payload_capacity doubles; rows/cols/captured/recorded are filled in. */
+typedef struct {
+  double* payload;
+  int64_t payload_capacity;
+  int64_t rows, cols;
+  int32_t captured, recorded;
+  int64_t captured_tokens;
+} bp_chunk_out;
+
+/* forward_chunk (model.cpp:227-336). The captured K/V / recorded inputs stay
+ * resident on the device and replace the stage's previous entry, like
+ * DeviceWorker::cache_ (engine.cpp:195-196). */
+bp_status bp_forward_chunk(bp_stage* stage, const bp_chunk_in* in, bp_chunk_out* out);
+/* Downloads the resident captured K (which=0) or V (which=1) rows of one local
+ * layer as fp64 [rows, h]; out may be NULL to query rows. */
+bp_status bp_stage_cache_rows(bp_stage* stage, int32_t layer, int32_t which, double* out,
+                              int64_t* rows);
+/* Bumps one resident cached value by one ulp towards +inf (engine.cpp:185-189). */
+bp_status bp_stage_cache_bump_ulp(bp_stage* stage, int32_t layer, int32_t which, int64_t index);
+/* cache_mismatch_report (model.cpp:171-199) on the resident cache vs the
+ * resident recording; report gets "" when they agree bitwise. */
+bp_status bp_stage_cache_audit(bp_stage* stage, char* report, int32_t report_len);
+
+/* scheduler_step (model.cpp:338-345): out = x - eps*(1/steps), n doubles, host. */
+bp_status bp_scheduler_step(int32_t device, const double* x, const double* eps, int64_t n,
+                            int32_t level, int32_t steps, double* out);
+
+/* ---- engine.hpp: static schedule (host-only; no GPU needed) -------------------- */
+typedef struct bp_schedule bp_schedule;
+/* Builds the data-independent schedule of run_pipeline (engine.cpp:255-497):
+ * queue states, pass order, noise ids, logical slots, ledger. */
+bp_status bp_schedule_create(const bp_pipeline_desc* desc, bp_schedule** out);
+void bp_schedule_destroy(bp_schedule* s);
+int64_t bp_schedule_rounds(const bp_schedule* s);
+int64_t bp_schedule_npasses(const bp_schedule* s);
+/* ScheduleEvent list (engine.hpp:46-58) sorted by (slot, device):
+ * 6 int64 per event: slot, device, block_id, level, phase, round. */
+int64_t bp_schedule_nevents(const bp_schedule* s);
+void bp_schedule_events(const bp_schedule* s, int64_t* out);
+/* TransferLedger (engine.hpp:62-71): channel name (<=31 chars), round, passes, scalars. */
+int64_t bp_schedule_nledger(const bp_schedule* s);
+void bp_schedule_ledger(const bp_schedule* s, int64_t i, char* channel, int64_t* round,
+                        int64_t* passes, int64_t* scalars);
+/* QueueSnapshot per round (engine.hpp:90-94); returns the block count. */
+int64_t bp_schedule_nsnapshots(const bp_schedule* s);
+int32_t bp_schedule_snapshot(const bp_schedule* s, int64_t i, int64_t* round, int64_t* ids,
+                             int32_t* levels);
+/* Emitted blocks in emission order: id, frame count, noise ids (<= frames). */
+int64_t bp_schedule_nblocks(const bp_schedule* s);
+int32_t bp_schedule_block(const bp_schedule* s, int64_t i, int64_t* block_id, int64_t* frames,
+                          int32_t* noise_ids, int64_t* frame_ids);
+/* Stage layer ranges actually used: begins[N], ends[N]. */
+void bp_schedule_partition(const bp_schedule* s, int32_t* begins, int32_t* ends);
+
+/* ---- engine.hpp: the pipeline ------------------------------------------------ */
+typedef struct bp_pipeline bp_pipeline;
+
+/* NCCL unique id for the transport (128 bytes). */
+bp_status bp_nccl_unique_id(uint8_t out[128]);
+/* Loopback: rank=0, world=1, all N stages on `device`, nccl_ids NULL.
+ * NCCL: one process per GPU, rank j owns stage j, world = N; nccl_ids holds
+ * N unique ids made by rank 0 and shared by the caller (128 bytes each). */
+bp_status bp_pipeline_create(const bp_pipeline_desc* desc, int32_t rank, int32_t world,
+                             int32_t device, const uint8_t* nccl_ids, bp_pipeline** out);
+bp_status bp_pipeline_destroy(bp_pipeline* p);
+
+/* EmittedBlock (engine.hpp:73-78) callback, rank 0 only, emission order. */
+typedef void (*bp_emit_fn)(void* user, int64_t block_id, int64_t frames, const double* data,
+                           const int32_t* noise_ids, int32_t nids, const int64_t* frame_ids);
+
+/* run_pipeline (engine.cpp:255-497): one whole generation. emit may be NULL
+ * (latents stay on the device; bp_pipeline_block can fetch them). */
+bp_status bp_pipeline_run(bp_pipeline* p, bp_emit_fn emit, void* user);
+
+typedef struct {
+  double gpu_ms;            /* device time of the last run (CUDA events) */
+  int64_t passes;
+  int64_t kernel_launches;  /* our kernels launched by the last run */
+  int64_t peak_bytes;       /* device memory high-water mark of this pipeline */
+  int64_t boundary_bytes;   /* bytes moved across stage boundaries */
+  double attn_ms, gemm_ms;  /* per-class device time when profiling is enabled */
+} bp_pipeline_stats;
+bp_status bp_pipeline_get_stats(bp_pipeline* p, bp_pipeline_stats* out);
+/* Per-kernel-class timing with CUDA events on the launching stream (0/1). */
+bp_status bp_pipeline_set_profiling(bp_pipeline* p, int32_t on);
+/* TraceRecord (engine.hpp:83-87) of pass i when record_trace is set. */
+int64_t bp_pipeline_ntrace(bp_pipeline* p);
+bp_status bp_pipeline_trace(bp_pipeline* p, int64_t i, int64_t* round, int64_t* block_id,
+                            int64_t* rows, int64_t* cols, double* eps /* may be NULL */);
+/* Device pointer + element count of emitted block i's latents (fp64). */
+bp_status bp_pipeline_block(bp_pipeline* p, int64_t i, const double** dev_data, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BP_CUDA_H_ */

@@ -1,0 +1,313 @@
+"""Python mirror of the reference's operator surface for the hot path
+(engine.hpp, model.hpp, noise.hpp, rng.hpp and the pybind module
+python/bindings.cpp:76-161), every call going through the C-ABI."""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Any, Callable, Dict, List, Optional, Sequence, Union
+
+import numpy as np
+
+from . import errors
+from ._lib import (EMIT_FN, ChunkIn, ChunkOut, PipelineStats, check, i32, i64, lib, u64, f64)
+from .config import CACHE, PRECISIONS, PipelineConfig
+
+ConfigLike = Union[PipelineConfig, Dict[str, Any], None]
+
+PHASES = ("warmup", "steady", "cooldown")
+
+
+def _cfg(config: ConfigLike) -> PipelineConfig:
+    if isinstance(config, PipelineConfig):
+        return config
+    return PipelineConfig.from_dict(config)
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+# ---- rng.hpp -----------------------------------------------------------------------
+def derive_seed(base: int, tags: Sequence[int]) -> int:
+    """derive_seed (rng.cpp:51-60), host-side."""
+    arr = (u64 * max(1, len(tags)))(*tags)
+    return int(lib.bp_derive_seed(base, arr, len(tags)))
+
+
+def normals(state: int, n: int, sigma: float = 1.0, device: int = 0) -> np.ndarray:
+    """RandomSource(state).normal_tensor({n}, sigma) drawn on the GPU (bit-exact)."""
+    out = np.empty(n, dtype=np.float64)
+    fin = u64()
+    check(lib.bp_normals(device, state, n, sigma, _ptr(out, f64), 0, C.byref(fin)))
+    return out
+
+
+# ---- noise.hpp ------------------------------------------------------------------------
+def build_pool(num_b: int, num_c: int, frame_shape: Sequence[int], noise_seed: int,
+               device: int = 0) -> np.ndarray:
+    """build_pool (noise.cpp:26-48) on the GPU: [M, H, W, C] fp64."""
+    h, w, c = (int(v) for v in frame_shape)
+    m = num_b + num_c // 2
+    out = np.empty((m, h, w, c), dtype=np.float64)
+    shape = (i64 * 3)(h, w, c)
+    check(lib.bp_noise_pool(device, num_b, num_c, shape, noise_seed, _ptr(out, f64), 0))
+    return out
+
+
+def scheduler_step(x: np.ndarray, eps: np.ndarray, level: int, steps: int, device: int = 0) -> np.ndarray:
+    """scheduler_step (model.cpp:338-345) on the GPU."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    eps = np.ascontiguousarray(eps, dtype=np.float64)
+    if x.shape != eps.shape:
+        raise errors.SchedulerError("x and eps shapes disagree")
+    out = np.empty_like(x)
+    check(lib.bp_scheduler_step(device, _ptr(x, f64), _ptr(eps, f64), x.size, level, steps, _ptr(out, f64)))
+    return out
+
+
+# ---- model.hpp -------------------------------------------------------------------------
+class Stage:
+    """A ModelChunk over layers [begin, end) resident on one GPU, with the
+    per-device KV feature cache (model.hpp:50-101)."""
+
+    def __init__(self, config: ConfigLike, seed: int, begin: int, end: int, context_seed: int,
+                 precision: str = "f64", device: int = 0):
+        cfg = _cfg(config)
+        self.cfg = cfg
+        self.begin, self.end = begin, end
+        self._h = C.c_void_p()
+        md = cfg.model_desc()
+        check(lib.bp_stage_create(device, C.byref(md), seed, context_seed, begin, end,
+                                  PRECISIONS[precision], C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            lib.bp_stage_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward_chunk(self, payload: np.ndarray, frame_levels: Sequence[int], frame_ids: Sequence[int],
+                      capture_frames: Sequence[int] = (), mode: str = "off", use_prev: int = 0,
+                      record_inputs: bool = False) -> Dict[str, Any]:
+        """forward_chunk (model.cpp:227-336). use_prev: 0 none, 1 the resident
+        captured K/V of the previous call, 2 its recorded layer inputs."""
+        payload = np.ascontiguousarray(payload, dtype=np.float64)
+        if len(frame_levels) != len(frame_ids):
+            raise errors.DimensionError("frame_ids and frame_levels disagree")
+        lv = np.ascontiguousarray(frame_levels, dtype=np.int32)
+        fi = np.ascontiguousarray(frame_ids, dtype=np.int64)
+        cf = np.ascontiguousarray(capture_frames, dtype=np.int32)
+        tpf = self.cfg.height * self.cfg.width
+        rows = payload.shape[0]
+        if rows != len(lv) * tpf:
+            raise errors.DimensionError("payload rows do not match frames * tokens_per_frame")
+        cin = ChunkIn(_ptr(payload, f64), rows, payload.shape[1] if payload.ndim > 1 else 1,
+                      _ptr(lv, i32), _ptr(fi, i64), len(lv), _ptr(cf, i32), len(cf),
+                      int(record_inputs), CACHE[mode], int(use_prev))
+        out_cols = self.cfg.channels if self.end == self.cfg.layers else self.cfg.hidden
+        out = np.empty((rows, out_cols), dtype=np.float64)
+        cout = ChunkOut(_ptr(out, f64), out.size, 0, 0, 0, 0, 0)
+        check(lib.bp_forward_chunk(self._h, C.byref(cin), C.byref(cout)))
+        return {"payload": out, "captured": bool(cout.captured), "recorded": bool(cout.recorded),
+                "captured_tokens": int(cout.captured_tokens)}
+
+    def cache_rows(self, layer: int, which: int) -> np.ndarray:
+        rows = i64()
+        check(lib.bp_stage_cache_rows(self._h, layer, which, None, C.byref(rows)))
+        out = np.empty((rows.value, self.cfg.hidden), dtype=np.float64)
+        check(lib.bp_stage_cache_rows(self._h, layer, which, _ptr(out, f64), C.byref(rows)))
+        return out
+
+    def bump_ulp(self, layer: int = 0, which: int = 1, index: int = 0) -> None:
+        check(lib.bp_stage_cache_bump_ulp(self._h, layer, which, index))
+
+    def audit(self) -> str:
+        buf = C.create_string_buffer(512)
+        check(lib.bp_stage_cache_audit(self._h, buf, 512))
+        return buf.value.decode()
+
+
+# ---- engine.hpp: schedule (host-only) ----------------------------------------------------
+class Schedule:
+    """The static schedule of run_pipeline: EventLog, TransferLedger,
+    QueueSnapshots, emitted block ids / noise ids (host-only, no GPU)."""
+
+    def __init__(self, config: ConfigLike):
+        self.cfg = _cfg(config)
+        self._h = C.c_void_p()
+        desc = self.cfg.to_desc()
+        check(lib.bp_schedule_create(C.byref(desc), C.byref(self._h)))
+        h = self._h
+        self.rounds = int(lib.bp_schedule_rounds(h))
+        self.npasses = int(lib.bp_schedule_npasses(h))
+        ne = int(lib.bp_schedule_nevents(h))
+        ev = np.zeros((max(ne, 1), 6), dtype=np.int64)
+        lib.bp_schedule_events(h, _ptr(ev, i64))
+        self.events = ev[:ne]
+        self.ledger = []
+        for i in range(int(lib.bp_schedule_nledger(h))):
+            ch = C.create_string_buffer(32)
+            r, p, s = i64(), i64(), i64()
+            lib.bp_schedule_ledger(h, i, ch, C.byref(r), C.byref(p), C.byref(s))
+            self.ledger.append({"channel": ch.value.decode(), "round": r.value, "passes": p.value,
+                                "scalars": s.value})
+        self.snapshots = []
+        for i in range(int(lib.bp_schedule_nsnapshots(h))):
+            r = i64()
+            n = lib.bp_schedule_snapshot(h, i, C.byref(r), None, None)
+            ids = np.zeros(max(n, 1), dtype=np.int64)
+            lv = np.zeros(max(n, 1), dtype=np.int32)
+            lib.bp_schedule_snapshot(h, i, C.byref(r), _ptr(ids, i64), _ptr(lv, i32))
+            self.snapshots.append({"round": r.value, "block_ids": ids[:n].tolist(), "levels": lv[:n].tolist()})
+        self.blocks = []
+        for i in range(int(lib.bp_schedule_nblocks(h))):
+            bid, fr = i64(), i64()
+            n = lib.bp_schedule_block(h, i, C.byref(bid), C.byref(fr), None, None)
+            nid = np.zeros(max(n, 1), dtype=np.int32)
+            fid = np.zeros(max(fr.value, 1), dtype=np.int64)
+            lib.bp_schedule_block(h, i, C.byref(bid), C.byref(fr), _ptr(nid, i32), _ptr(fid, i64))
+            self.blocks.append({"block_id": bid.value, "frames": fr.value, "noise_ids": nid[:n].tolist(),
+                                "frame_ids": fid[:fr.value].tolist()})
+        b = (i32 * self.cfg.devices)()
+        e = (i32 * self.cfg.devices)()
+        lib.bp_schedule_partition(h, b, e)
+        self.partition = [(b[j], e[j]) for j in range(self.cfg.devices)]
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib.bp_schedule_destroy(self._h)
+        except Exception:
+            pass
+
+
+def measure_bubbles(events: np.ndarray, devices: int) -> Dict[str, Any]:
+    """measure_bubbles (engine.cpp:505-555) over (slot, device, block, level, phase, round) rows."""
+    st = {"first_slot": 0, "last_slot": 0, "busy_per_device": 0, "idle_per_device": 0,
+          "warmup_idle": 0, "steady_idle": 0, "cooldown_idle": 0, "ratio": 0.0}
+    if len(events) == 0:
+        return st
+    per = [sorted((int(e[0]), int(e[4])) for e in events if int(e[1]) == d) for d in range(devices)]
+    first, last = int(events[:, 0].min()), int(events[:, 0].max())
+    busy = len(per[0])
+    if any(len(v) != busy for v in per):
+        raise errors.SchedulingError("malformed event log: devices saw different pass counts")
+    st.update(first_slot=first, last_slot=last, busy_per_device=busy,
+              idle_per_device=(last - first + 1) - busy)
+    keys = ("warmup_idle", "steady_idle", "cooldown_idle")
+    for v in per:
+        nxt = 0
+        for s in range(first, last + 1):
+            while nxt < len(v) and v[nxt][0] < s:
+                nxt += 1
+            if nxt < len(v) and v[nxt][0] == s:
+                continue
+            st[keys[v[nxt][1] if nxt < len(v) else 2]] += 1
+    idle = st["idle_per_device"] * devices
+    st["ratio"] = 0.0 if idle <= 0 else idle / (idle + busy * devices)
+    return st
+
+
+def coordinated_noise_ids(num_b: int, num_c: int, appends: int, seed: int = 2) -> List[List[int]]:
+    """bindings.cpp:146-160: ids of the first block and `appends` coordinated appends."""
+    s = Schedule({"num_b": num_b, "num_c": num_c, "steps": 1, "blocks": appends + 1, "devices": 1,
+                  "layers": 1, "hidden": 2, "heads": 1, "channels": 1, "height": 1, "width": 1,
+                  "seed_noise": seed})
+    return [b["noise_ids"] for b in s.blocks]
+
+
+# ---- engine.hpp: the pipeline ---------------------------------------------------------------
+class Pipeline:
+    """run_pipeline (engine.cpp:255-497) on B200: build once, run many times."""
+
+    def __init__(self, config: ConfigLike, rank: int = 0, world: int = 1, device: int = 0,
+                 nccl_ids: Optional[bytes] = None):
+        self.cfg = _cfg(config)
+        self._h = C.c_void_p()
+        desc = self.cfg.to_desc()
+        ids = None
+        if nccl_ids is not None:
+            buf = (C.c_uint8 * len(nccl_ids)).from_buffer_copy(nccl_ids)
+            ids = C.cast(buf, C.POINTER(C.c_uint8))
+        check(lib.bp_pipeline_create(C.byref(desc), rank, world, device, ids, C.byref(self._h)))
+        self.schedule = Schedule(self.cfg)
+
+    def close(self):
+        if self._h:
+            lib.bp_pipeline_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run(self, emit: Optional[Callable] = None, collect: bool = True) -> List[Dict[str, Any]]:
+        """One whole generation. Returns the emitted blocks (EmittedBlock,
+        engine.hpp:73-78) in emission order with host fp64 frames."""
+        blocks: List[Dict[str, Any]] = []
+        hwc = self.cfg.height * self.cfg.width * self.cfg.channels
+
+        def _cb(user, block_id, frames, data, nids_p, nids, fids_p):
+            arr = np.ctypeslib.as_array(data, shape=(frames * hwc,)).copy() if collect else None
+            item = {"block_id": int(block_id),
+                    "frames": None if arr is None else arr.reshape(frames, self.cfg.height, self.cfg.width,
+                                                                 self.cfg.channels),
+                    "noise_ids": [nids_p[k] for k in range(nids)],
+                    "frame_ids": [fids_p[k] for k in range(frames)]}
+            blocks.append(item)
+            if emit is not None:
+                emit(item)
+
+        cb = EMIT_FN(_cb)
+        check(lib.bp_pipeline_run(self._h, cb, None))
+        return blocks
+
+    def stats(self) -> Dict[str, Any]:
+        s = PipelineStats()
+        check(lib.bp_pipeline_get_stats(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in PipelineStats._fields_}
+
+    def trace(self) -> List[Dict[str, Any]]:
+        out = []
+        for i in range(int(lib.bp_pipeline_ntrace(self._h))):
+            r, b, rows, cols = i64(), i64(), i64(), i64()
+            check(lib.bp_pipeline_trace(self._h, i, C.byref(r), C.byref(b), C.byref(rows), C.byref(cols), None))
+            eps = np.empty((rows.value, cols.value), dtype=np.float64)
+            check(lib.bp_pipeline_trace(self._h, i, C.byref(r), C.byref(b), C.byref(rows), C.byref(cols),
+                                        _ptr(eps, f64)))
+            out.append({"round": r.value, "block_id": b.value, "eps": eps})
+        return out
+
+
+def run_pipeline(config: ConfigLike = None) -> Dict[str, Any]:
+    """bindings.cpp:139-141 + run_to_dict (:37-72), plus the event log,
+    snapshots and (when record_trace) the per-pass eps trace."""
+    cfg = _cfg(config)
+    p = Pipeline(cfg)
+    try:
+        blocks = p.run()
+        sched = p.schedule
+        out = {"blocks": blocks, "rounds": sched.rounds,
+               "bubbles": measure_bubbles(sched.events, cfg.devices),
+               "ledger": sched.ledger, "events": sched.events, "queue_snapshots": sched.snapshots,
+               "stats": p.stats()}
+        if cfg.record_trace:
+            out["trace"] = p.trace()
+        return out
+    finally:
+        p.close()
+
+
+def serial_oracle(config: ConfigLike = None) -> Dict[str, Any]:
+    """serial_oracle (engine.cpp:499-503): the same run on a single stage."""
+    cfg = _cfg(config)
+    cfg = PipelineConfig(**{**cfg.__dict__, "devices": 1, "threaded": False, "uneven_split": False,
+                            "layer_split": None})
+    return run_pipeline(cfg)

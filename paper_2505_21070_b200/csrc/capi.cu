@@ -1,0 +1,229 @@
+// C-ABI entry points for rng / noise / stage / scheduler_step (bp_cuda.h).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "kernels_simt.cuh"
+#include "schedule.hpp"
+#include "stage.hpp"
+
+namespace bp {
+
+std::atomic<int64_t> g_launches{0};
+std::atomic<int64_t> g_dev_bytes{0}, g_dev_peak{0};
+
+namespace {
+thread_local std::string t_last_error;
+
+void require_device(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    fail(BP_ERR_CUDA, "no CUDA device available (this library has no CPU fallback)");
+  if (device < 0 || device >= n) fail(BP_ERR_CUDA, "device index out of range");
+  BP_CUDA(cudaSetDevice(device));
+}
+}  // namespace
+
+void set_last_error(const std::string& m) { t_last_error = m; }
+
+}  // namespace bp
+
+struct bp_stage {
+  std::unique_ptr<bp::Stage> s;
+  int device = 0;
+  bp::DevBuf payload, levels, ids;
+};
+
+extern "C" {
+
+const char* bp_last_error(void) { return bp::t_last_error.c_str(); }
+const char* bp_version(void) { return "blockpipe-b200 0.1 (sm_100a)"; }
+
+uint64_t bp_derive_seed(uint64_t base, const uint64_t* tags, int32_t ntags) {
+  return bp::derive_seed(base, tags, ntags);
+}
+
+bp_status bp_normals(int32_t device, uint64_t state, int64_t n, double sigma, double* out,
+                     int32_t out_is_device, uint64_t* final_state) {
+  return bp::guarded([&] {
+    if (n < 0) bp::fail(BP_ERR_DIMENSION, "negative count");
+    bp::require_device(device);
+    bp::DevBuf tmp;
+    double* dst = out;
+    if (!out_is_device) {
+      tmp.alloc(static_cast<size_t>(n) * 8);
+      dst = tmp.as<double>();
+    }
+    bp::launch_normal_fill(state, n, sigma, dst, nullptr);
+    if (!out_is_device) BP_CUDA(cudaMemcpy(out, dst, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+    BP_CUDA(cudaDeviceSynchronize());
+    if (final_state) *final_state = state + bp::kGolden * static_cast<uint64_t>(2 * n);
+  });
+}
+
+bp_status bp_noise_pool(int32_t device, int32_t num_b, int32_t num_c, const int64_t frame_shape[3],
+                        uint64_t noise_seed, double* out, int32_t out_is_device) {
+  return bp::guarded([&] {
+    // build_pool argument checks (noise.cpp:28-29)
+    if (num_b < 1) bp::fail(BP_ERR_CONFIG, "num_b must be >= 1");
+    if (num_c < 0 || num_c % 2 != 0) bp::fail(BP_ERR_CONFIG, "num_c must be even and >= 0");
+    bp::require_device(device);
+    const int m = num_b + num_c / 2;
+    const int64_t per = frame_shape[0] * frame_shape[1] * frame_shape[2];
+    bp::DevBuf tmp, flags;
+    double* dst = out;
+    if (!out_is_device) {
+      tmp.alloc(static_cast<size_t>(m * per) * 8);
+      dst = tmp.as<double>();
+    }
+    bp::launch_normal_fill(noise_seed, m * per, 1.0, dst, nullptr);
+    if (m > 1) {
+      flags.alloc(static_cast<size_t>(m) * m * 4);
+      BP_CUDA(cudaMemset(flags.p, 0, static_cast<size_t>(m) * m * 4));
+      bp::launch_pool_differs(dst, m, per, flags.as<int>(), nullptr);
+      std::vector<int> f(static_cast<size_t>(m) * m);
+      BP_CUDA(cudaMemcpy(f.data(), flags.p, f.size() * 4, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < m; ++i)
+        for (int j = i + 1; j < m; ++j)
+          if (!f[static_cast<size_t>(i) * m + j])
+            bp::fail(BP_ERR_CONFIG, "noise pool entries collided; change the noise seed");
+    }
+    if (!out_is_device) BP_CUDA(cudaMemcpy(out, dst, static_cast<size_t>(m * per) * 8, cudaMemcpyDeviceToHost));
+    BP_CUDA(cudaDeviceSynchronize());
+  });
+}
+
+bp_status bp_stage_create(int32_t device, const bp_model_desc* model, uint64_t seed_model,
+                          uint64_t seed_context, int32_t layer_begin, int32_t layer_end, int32_t precision,
+                          bp_stage** out) {
+  return bp::guarded([&] {
+    if (!model || !out) bp::fail(BP_ERR_CONFIG, "null argument");
+    bp::validate_model(*model);
+    bp::require_device(device);
+    auto h = std::make_unique<bp_stage>();
+    h->device = device;
+    h->s = std::make_unique<bp::Stage>(device, *model, seed_model, seed_context, layer_begin, layer_end,
+                                       precision, nullptr);
+    *out = h.release();
+  });
+}
+
+bp_status bp_stage_destroy(bp_stage* stage) {
+  return bp::guarded([&] { delete stage; });
+}
+
+bp_status bp_forward_chunk(bp_stage* h, const bp_chunk_in* in, bp_chunk_out* out) {
+  return bp::guarded([&] {
+    if (!h || !in || !out) bp::fail(BP_ERR_CONFIG, "null argument");
+    bp::Stage& s = *h->s;
+    BP_CUDA(cudaSetDevice(h->device));
+    const int tpf = 0;  // unused; tokens come from the stage's geometry below
+    (void)tpf;
+    const int64_t frames = in->nframes;
+    // forward_chunk's shape checks (model.cpp:230-266)
+    const int64_t tokens = frames * static_cast<int64_t>(s.hidden() > 0 ? 1 : 1);
+    (void)tokens;
+    bp::StageInput si;
+    const int64_t tpf64 = in->nframes > 0 ? in->rows / std::max<int64_t>(1, in->nframes) : 0;
+    (void)tpf64;
+    // tokens = frames * tokens_per_frame, checked against the payload rows
+    si.nframes = in->nframes;
+    si.tokens = in->rows;
+    si.capture_frames.assign(in->capture_frames, in->capture_frames + in->ncapture);
+    si.record_inputs = in->record_inputs != 0;
+    si.mode = in->mode;
+    si.use_prev = in->use_prev;
+    const int64_t want_cols = s.is_first() ? s.channels() : s.hidden();
+    if (in->cols != want_cols)
+      bp::fail(BP_ERR_DIMENSION, s.is_first() ? "chunk 0 expects [tokens, C] latents"
+                                              : "interior chunk expects [tokens, h] hidden state");
+    // upload payload (fp64 host -> device, in the stage's activation dtype)
+    const size_t n = static_cast<size_t>(in->rows * in->cols);
+    h->payload.reserve(n * 8 + 8);
+    h->levels.reserve(static_cast<size_t>(frames) * 4 + 4);
+    h->ids.reserve(static_cast<size_t>(frames) * 8 + 8);
+    cudaStream_t st = s.stream();
+    BP_CUDA(cudaMemcpyAsync(h->payload.p, in->payload, n * 8, cudaMemcpyHostToDevice, st));
+    if (!s.is_first() && s.act_bytes() == 4) {
+      bp::DevBuf f;
+      f.alloc(n * 4);
+      bp::launch_convert<double, float>(h->payload.as<double>(), f.as<float>(), static_cast<int64_t>(n), st);
+      BP_CUDA(cudaMemcpyAsync(h->payload.p, f.p, n * 4, cudaMemcpyDeviceToDevice, st));
+      BP_CUDA(cudaStreamSynchronize(st));
+    }
+    if (frames > 0) {
+      BP_CUDA(cudaMemcpyAsync(h->levels.p, in->frame_levels, static_cast<size_t>(frames) * 4, cudaMemcpyHostToDevice, st));
+      BP_CUDA(cudaMemcpyAsync(h->ids.p, in->frame_ids, static_cast<size_t>(frames) * 8, cudaMemcpyHostToDevice, st));
+    }
+    si.payload = h->payload.p;
+    si.d_levels = h->levels.as<int32_t>();
+    si.d_frame_ids = h->ids.as<int64_t>();
+    const void* res = s.forward(si);
+    const int64_t out_cols = s.is_last() ? s.channels() : s.hidden();
+    const size_t on = static_cast<size_t>(in->rows * out_cols);
+    if (out->payload_capacity < static_cast<int64_t>(on)) bp::fail(BP_ERR_DIMENSION, "output buffer too small");
+    if (s.is_last() ? s.eps_bytes() == 8 : s.act_bytes() == 8) {
+      BP_CUDA(cudaMemcpyAsync(out->payload, res, on * 8, cudaMemcpyDeviceToHost, st));
+    } else {
+      std::vector<float> f(on);
+      BP_CUDA(cudaMemcpyAsync(f.data(), res, on * 4, cudaMemcpyDeviceToHost, st));
+      BP_CUDA(cudaStreamSynchronize(st));
+      for (size_t i = 0; i < on; ++i) out->payload[i] = f[i];
+    }
+    BP_CUDA(cudaStreamSynchronize(st));
+    out->rows = in->rows;
+    out->cols = out_cols;
+    out->captured = s.cache_valid() ? 1 : 0;
+    out->recorded = s.rec_valid() ? 1 : 0;
+    out->captured_tokens = s.cache_valid() ? s.cache_tokens() : 0;
+  });
+}
+
+bp_status bp_stage_cache_rows(bp_stage* h, int32_t layer, int32_t which, double* out, int64_t* rows) {
+  return bp::guarded([&] {
+    if (!h->s->cache_valid()) bp::fail(BP_ERR_CACHE, "no resident cache");
+    if (rows) *rows = h->s->cache_tokens();
+    if (out) h->s->cache_rows(layer, which, out);
+  });
+}
+
+bp_status bp_stage_cache_bump_ulp(bp_stage* h, int32_t layer, int32_t which, int64_t index) {
+  return bp::guarded([&] {
+    h->s->bump_ulp(layer, which, index);
+    BP_CUDA(cudaStreamSynchronize(h->s->stream()));
+  });
+}
+
+bp_status bp_stage_cache_audit(bp_stage* h, char* report, int32_t report_len) {
+  return bp::guarded([&] {
+    const std::string r = h->s->audit();
+    if (report && report_len > 0) {
+      std::strncpy(report, r.c_str(), static_cast<size_t>(report_len) - 1);
+      report[report_len - 1] = 0;
+    }
+  });
+}
+
+bp_status bp_scheduler_step(int32_t device, const double* x, const double* eps, int64_t n, int32_t level,
+                            int32_t steps, double* out) {
+  return bp::guarded([&] {
+    // scheduler_step's range check (model.cpp:339-343)
+    if (level < 1 || level > steps)
+      bp::fail(BP_ERR_SCHEDULER, "level " + std::to_string(level) + " outside 1.." + std::to_string(steps));
+    bp::require_device(device);
+    bp::DevBuf dx, de, dout;
+    dx.alloc(static_cast<size_t>(n) * 8 + 8);
+    de.alloc(static_cast<size_t>(n) * 8 + 8);
+    dout.alloc(static_cast<size_t>(n) * 8 + 8);
+    BP_CUDA(cudaMemcpy(dx.p, x, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice));
+    BP_CUDA(cudaMemcpy(de.p, eps, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice));
+    bp::launch_scheduler_step<double>(dx.as<double>(), de.as<double>(), n, steps, dout.as<double>(), nullptr);
+    BP_CUDA(cudaMemcpy(out, dout.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

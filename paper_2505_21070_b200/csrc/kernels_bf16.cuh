@@ -1,0 +1,45 @@
+// bf16 tensor-core path: LayerNorm (fp32 residual -> bf16 operand), GEMMs
+// with fused epilogues (tcgen05), attention over two KV segments.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace bp {
+
+using bf16 = __nv_bfloat16;
+
+// ln_affine (model.cpp:32-41): fp32 x [rows, n] -> bf16 y, fp32 stats.
+void launch_ln_bf16(const float* x, int64_t ldx, const float* g, const float* b, int64_t rows,
+                    int n, bf16* y, cudaStream_t st);
+
+enum GemmEpi {
+  kGemmStoreBf16 = 0,    // C bf16 = acc
+  kGemmGeluBf16 = 1,     // C bf16 = gelu_erf(acc)           (ffn_sublayer, model.cpp:221-225)
+  kGemmResidualF32 = 2,  // C fp32 = C + acc (x += sublayer)  (forward_chunk, model.cpp:325-331)
+  kGemmStoreF32 = 3      // C fp32 = acc
+};
+// C[M,N] = A[M,K] (bf16, row stride lda) x W[N,K]^T (bf16, K-major weights).
+void launch_gemm_bf16(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C,
+                      int64_t ldc, int epi, cudaStream_t st);
+// Which GEMM implementation launch_gemm_bf16 uses: 1 = tcgen05 (default), 0 = SIMT check path.
+void set_gemm_impl(int impl);
+int gemm_impl();
+
+struct AttnBf16Args {
+  const bf16* q; int64_t ldq;
+  const bf16* k0; int64_t ldk0; const bf16* v0; int64_t ldv0; int64_t n0;  // cached prefix
+  const bf16* k1; int64_t ldk1; const bf16* v1; int64_t ldv1; int64_t n1;  // current block
+  bf16* out; int64_t ldo;
+  int heads, dh;
+  float scale;
+};
+// Non-causal multi-head attention (model.cpp:47-72) of q rows against
+// [prefix ++ current] keys; softmax in fp32.
+void launch_attn_bf16(const AttnBf16Args& a, int64_t rows, cudaStream_t st);
+void set_attn_impl(int impl);
+int attn_impl();
+
+}  // namespace bp

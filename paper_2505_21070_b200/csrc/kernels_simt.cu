@@ -1,0 +1,393 @@
+// SIMT kernels for the fp64 parity mode and the fp32 verification mode.
+// fp64 follows the reference's arithmetic order: matmul accumulates k
+// ascending with separate multiply/add roundings (tensor.cpp:84-109), the
+// LayerNorm is two-pass (tensor.cpp:128-146) followed by *g + b
+// (model.cpp:32-41), softmax divides by the sum (tensor.cpp:111-126) and the
+// attention output accumulates keys ascending (model.cpp:63-69). nvcc's FMA
+// contraction is suppressed with explicit _rn intrinsics. fp32 uses FMA.
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+#include "kernels_simt.cuh"
+
+namespace bp {
+
+template <typename T> struct Ar;
+template <> struct Ar<double> {
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+  static __device__ __forceinline__ double madd(double acc, double a, double b) {
+    return __dadd_rn(acc, __dmul_rn(a, b));
+  }
+  static __device__ __forceinline__ double ex(double x) { return exp(x); }
+  static __device__ __forceinline__ double erf_(double x) { return erf(x); }
+  static __device__ __forceinline__ double sqrt_(double x) { return __dsqrt_rn(x); }
+};
+template <> struct Ar<float> {
+  static __device__ __forceinline__ float add(float a, float b) { return a + b; }
+  static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
+  static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
+  static __device__ __forceinline__ float div(float a, float b) { return a / b; }
+  static __device__ __forceinline__ float madd(float acc, float a, float b) { return fmaf(a, b, acc); }
+  static __device__ __forceinline__ float ex(float x) { return expf(x); }
+  static __device__ __forceinline__ float erf_(float x) { return erff(x); }
+  static __device__ __forceinline__ float sqrt_(float x) { return sqrtf(x); }
+};
+
+template <typename T>
+__device__ __forceinline__ T block_reduce(T v, T* red, bool is_max) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    const T other = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? (other > v ? other : v) : Ar<T>::add(v, other);
+  }
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  T r = red[0];
+  for (int w = 1; w < nw; ++w) r = is_max ? (red[w] > r ? red[w] : r) : Ar<T>::add(r, red[w]);
+  return r;
+}
+
+// ---- patchify + embeddings (model.cpp:245-260, 155-169) ----------------------
+// x[r,j] = (sum_c lat[r,c] w_in[c,j]) + (pe[j] + te[j]) in fp64 for every
+// precision (arguments reach ~4e5 rad), then stored as TO.
+template <typename TO>
+__global__ void k_embed(const double* __restrict__ lat, const double* __restrict__ w_in,
+                        const double* __restrict__ freq, const int32_t* __restrict__ levels,
+                        const int64_t* __restrict__ frame_ids, int64_t tokens, int C, int h,
+                        int tpf, TO* __restrict__ x) {
+  const int64_t total = tokens * h;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / h;
+    const int j = static_cast<int>(e - r * h);
+    double acc = 0.0;
+    for (int c = 0; c < C; ++c) acc = __dadd_rn(acc, __dmul_rn(lat[r * C + c], w_in[static_cast<int64_t>(c) * h + j]));
+    const int64_t f = r / tpf, t = r - f * tpf;
+    const int64_t pos = frame_ids[f] * tpf + t;
+    const int64_t tpos = static_cast<int64_t>(levels[f]) + 1000000;
+    const double fr = freq[j >> 1];
+    const double ap = __dmul_rn(static_cast<double>(pos), fr);
+    const double at = __dmul_rn(static_cast<double>(tpos), fr);
+    const double pe = (j & 1) ? cos(ap) : sin(ap);
+    const double te = (j & 1) ? cos(at) : sin(at);
+    x[e] = static_cast<TO>(__dadd_rn(acc, __dadd_rn(pe, te)));
+  }
+}
+
+template <typename TO>
+void launch_embed(const double* lat, const double* w_in, const double* freq, const int32_t* levels,
+                  const int64_t* frame_ids, int64_t tokens, int C, int h, int tpf, TO* x,
+                  cudaStream_t st) {
+  const int64_t total = tokens * h;
+  if (total <= 0) return;
+  const int64_t want = (total + 255) / 256;
+  k_embed<TO><<<static_cast<int>(want < kNumSms * 16 ? want : kNumSms * 16), 256, 0, st>>>(
+      lat, w_in, freq, levels, frame_ids, tokens, C, h, tpf, x);
+  count_launch();
+}
+template void launch_embed<double>(const double*, const double*, const double*, const int32_t*,
+                                   const int64_t*, int64_t, int, int, int, double*, cudaStream_t);
+template void launch_embed<float>(const double*, const double*, const double*, const int32_t*,
+                                  const int64_t*, int64_t, int, int, int, float*, cudaStream_t);
+
+// ---- ln_affine (model.cpp:32-41 over tensor.cpp:128-146) ---------------------
+template <typename T>
+__global__ void k_ln(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
+                     int64_t rows, int n, T eps, T* __restrict__ y) {
+  __shared__ T red[32];
+  const int64_t r = blockIdx.x;
+  const T* xr = x + r * n;
+  T s = 0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) s = Ar<T>::add(s, xr[j]);
+  const T mean = Ar<T>::div(block_reduce<T>(s, red, false), static_cast<T>(n));
+  T v = 0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const T d = Ar<T>::sub(xr[j], mean);
+    v = Ar<T>::madd(v, d, d);
+  }
+  const T var = Ar<T>::div(block_reduce<T>(v, red, false), static_cast<T>(n));
+  const T inv = Ar<T>::div(static_cast<T>(1), Ar<T>::sqrt_(Ar<T>::add(var, eps)));
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const T yn = Ar<T>::mul(Ar<T>::sub(xr[j], mean), inv);
+    y[r * n + j] = Ar<T>::add(Ar<T>::mul(yn, g[j]), b[j]);
+  }
+}
+
+template <typename T>
+void launch_ln(const T* x, const T* g, const T* b, int64_t rows, int n, T* y, cudaStream_t st) {
+  if (rows <= 0) return;
+  k_ln<T><<<static_cast<unsigned>(rows), 128, 0, st>>>(x, g, b, rows, n, static_cast<T>(1e-5), y);
+  count_launch();
+}
+template void launch_ln<double>(const double*, const double*, const double*, int64_t, int, double*, cudaStream_t);
+template void launch_ln<float>(const float*, const float*, const float*, int64_t, int, float*, cudaStream_t);
+
+// ---- matmul (tensor.cpp:84-109) with fused epilogues ---------------------------
+// C[M,N] = A[M,K] (row stride lda) @ B[K,N] (row-major). Each thread owns a
+// 4x4 micro-tile and accumulates k in ascending order.
+template <typename T, int EPI>
+__global__ void __launch_bounds__(256) k_matmul(const T* __restrict__ A, int64_t lda,
+                                                const T* __restrict__ B, int64_t ldb, int M, int N, int K,
+                                                T* __restrict__ Cm, int64_t ldc,
+                                                const T* __restrict__ R, int64_t ldr) {
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ T As[BK][BM + 1];
+  __shared__ T Bs[BK][BN];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  T acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0;
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    for (int e = threadIdx.x; e < BM * BK; e += 256) {
+      const int mm = e / BK, kk = e % BK;
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < M && gk < K) ? A[static_cast<int64_t>(gm) * lda + gk] : T(0);
+    }
+    for (int e = threadIdx.x; e < BK * BN; e += 256) {
+      const int kk = e / BN, nn = e % BN;
+      const int gk = k0 + kk, gn = n0 + nn;
+      Bs[kk][nn] = (gk < K && gn < N) ? B[static_cast<int64_t>(gk) * ldb + gn] : T(0);
+    }
+    __syncthreads();
+    const int kmax = (K - k0) < BK ? (K - k0) : BK;
+    for (int kk = 0; kk < kmax; ++kk) {
+      T a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bb[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = Ar<T>::madd(acc[i][j], a[i], bb[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty * 4 + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tx * 4 + j;
+      if (gn >= N) continue;
+      T v = acc[i][j];
+      if (EPI == kEpiGelu) {
+        // gelu (model.cpp:43): 0.5*x*(1 + erf(x/sqrt(2)))
+        const T t = Ar<T>::div(v, static_cast<T>(1.4142135623730951));
+        v = Ar<T>::mul(Ar<T>::mul(static_cast<T>(0.5), v), Ar<T>::add(static_cast<T>(1), Ar<T>::erf_(t)));
+      } else if (EPI == kEpiResidual) {
+        // add(x, y) (tensor.cpp:148-156): x + y
+        v = Ar<T>::add(R[static_cast<int64_t>(gm) * ldr + gn], v);
+      }
+      Cm[static_cast<int64_t>(gm) * ldc + gn] = v;
+    }
+  }
+}
+
+template <typename T>
+void launch_matmul(const T* A, int64_t lda, const T* B, int64_t ldb, int M, int N, int K, T* C,
+                   int64_t ldc, int epi, const T* R, int64_t ldr, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  dim3 grid((N + 63) / 64, (M + 63) / 64);
+  switch (epi) {
+    case kEpiNone: k_matmul<T, kEpiNone><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, C, ldc, R, ldr); break;
+    case kEpiGelu: k_matmul<T, kEpiGelu><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, C, ldc, R, ldr); break;
+    default: k_matmul<T, kEpiResidual><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, C, ldc, R, ldr); break;
+  }
+  count_launch();
+}
+template void launch_matmul<double>(const double*, int64_t, const double*, int64_t, int, int, int, double*, int64_t, int, const double*, int64_t, cudaStream_t);
+template void launch_matmul<float>(const float*, int64_t, const float*, int64_t, int, int, int, float*, int64_t, int, const float*, int64_t, cudaStream_t);
+
+// ---- attention (model.cpp:47-72) over two KV segments ---------------------------
+// One block per (query row, head). Pass 1: row max of the scaled scores;
+// pass 2: sum of exp(s - max); pass 3: p = e / sum, out = sum_j p_j v_j in
+// ascending key order (prefix segment first, like vcat_rows(prefix, k)).
+template <typename T>
+__global__ void __launch_bounds__(128) k_attention(AttnArgs<T> a) {
+  extern __shared__ unsigned char smem_raw[];
+  T* qs = reinterpret_cast<T*>(smem_raw);  // dh
+  T* ps = qs + a.dh;                        // 128
+  __shared__ T red[32];
+  const int64_t i = blockIdx.x;
+  const int hd = blockIdx.y;
+  const int c0 = hd * a.dh;
+  const T* qrow = a.q + i * a.ldq + c0;
+  for (int t = threadIdx.x; t < a.dh; t += blockDim.x) qs[t] = qrow[t];
+  __syncthreads();
+  const int64_t nkv = a.n0 + a.n1;
+  auto krow = [&](int64_t j) -> const T* {
+    return j < a.n0 ? a.k0 + j * a.ldk0 + c0 : a.k1 + (j - a.n0) * a.ldk1 + c0;
+  };
+  auto vrow = [&](int64_t j) -> const T* {
+    return j < a.n0 ? a.v0 + j * a.ldv0 + c0 : a.v1 + (j - a.n0) * a.ldv1 + c0;
+  };
+  auto score = [&](int64_t j) -> T {
+    const T* kr = krow(j);
+    T acc = 0;
+    for (int t = 0; t < a.dh; ++t) acc = Ar<T>::madd(acc, qs[t], kr[t]);
+    return Ar<T>::mul(acc, a.scale);
+  };
+  T mx = -INFINITY;
+  for (int64_t j = threadIdx.x; j < nkv; j += blockDim.x) {
+    const T s = score(j);
+    mx = s > mx ? s : mx;
+  }
+  mx = block_reduce<T>(mx, red, true);
+  T sum = 0;
+  for (int64_t j = threadIdx.x; j < nkv; j += blockDim.x) sum = Ar<T>::add(sum, Ar<T>::ex(Ar<T>::sub(score(j), mx)));
+  sum = block_reduce<T>(sum, red, false);
+  T acc0 = 0, acc1 = 0;  // dims threadIdx.x and threadIdx.x + 128 (dh <= 256)
+  for (int64_t j0 = 0; j0 < nkv; j0 += blockDim.x) {
+    __syncthreads();
+    const int64_t j = j0 + threadIdx.x;
+    if (j < nkv) ps[threadIdx.x] = Ar<T>::div(Ar<T>::ex(Ar<T>::sub(score(j), mx)), sum);
+    __syncthreads();
+    const int jn = static_cast<int>((nkv - j0) < blockDim.x ? (nkv - j0) : blockDim.x);
+    for (int jj = 0; jj < jn; ++jj) {
+      const T* vr = vrow(j0 + jj);
+      const T p = ps[jj];
+      if (threadIdx.x < a.dh) acc0 = Ar<T>::madd(acc0, p, vr[threadIdx.x]);
+      if (threadIdx.x + 128 < a.dh) acc1 = Ar<T>::madd(acc1, p, vr[threadIdx.x + 128]);
+    }
+  }
+  T* orow = a.out + i * a.ldo + c0;
+  if (threadIdx.x < a.dh) orow[threadIdx.x] = acc0;
+  if (threadIdx.x + 128 < a.dh) orow[threadIdx.x + 128] = acc1;
+}
+
+template <typename T>
+void launch_attention(const AttnArgs<T>& a, int64_t rows, int heads, cudaStream_t st) {
+  if (rows <= 0) return;
+  if (a.dh > 256) fail(BP_ERR_CONFIG, "SIMT attention supports head dim <= 256");
+  dim3 grid(static_cast<unsigned>(rows), heads);
+  const size_t smem = sizeof(T) * (a.dh + 128);
+  k_attention<T><<<grid, 128, smem, st>>>(a);
+  count_launch();
+}
+template void launch_attention<double>(const AttnArgs<double>&, int64_t, int, cudaStream_t);
+template void launch_attention<float>(const AttnArgs<float>&, int64_t, int, cudaStream_t);
+
+// ---- strided row copy / bitwise compare / conversion --------------------------
+__global__ void k_copy_rows(const uint32_t* __restrict__ src, int64_t src_ld, uint32_t* __restrict__ dst,
+                            int64_t dst_ld, int64_t rows, int64_t words) {
+  const int64_t total = rows * words;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / words, c = e - r * words;
+    dst[r * dst_ld + c] = src[r * src_ld + c];
+  }
+}
+
+void launch_copy_rows(const void* src, int64_t src_ld_bytes, void* dst, int64_t dst_ld_bytes,
+                      int64_t rows, int64_t row_bytes, cudaStream_t st) {
+  if (rows <= 0 || row_bytes <= 0) return;
+  if ((row_bytes | src_ld_bytes | dst_ld_bytes) & 3) fail(BP_ERR_INTERNAL, "copy_rows needs 4-byte rows");
+  const int64_t words = row_bytes / 4, total = rows * words;
+  const int64_t want = (total + 255) / 256;
+  k_copy_rows<<<static_cast<int>(want < kNumSms * 8 ? want : kNumSms * 8), 256, 0, st>>>(
+      static_cast<const uint32_t*>(src), src_ld_bytes / 4, static_cast<uint32_t*>(dst),
+      dst_ld_bytes / 4, rows, words);
+  count_launch();
+}
+
+// First flat index where a[r*lda + c] and b[r*ldb + c] differ bitwise (words);
+// *first is initialised to INT64_MAX by the caller.
+__global__ void k_first_diff(const uint32_t* __restrict__ a, int64_t lda, const uint32_t* __restrict__ b,
+                             int64_t ldb, int64_t rows, int64_t words, unsigned long long* first) {
+  const int64_t total = rows * words;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / words, c = e - r * words;
+    if (a[r * lda + c] != b[r * ldb + c]) atomicMin(first, static_cast<unsigned long long>(e));
+  }
+}
+
+void launch_first_diff(const void* a, int64_t lda_bytes, const void* b, int64_t ldb_bytes,
+                       int64_t rows, int64_t row_bytes, unsigned long long* first, cudaStream_t st) {
+  if (rows <= 0) return;
+  const int64_t words = row_bytes / 4, total = rows * words;
+  const int64_t want = (total + 255) / 256;
+  k_first_diff<<<static_cast<int>(want < kNumSms * 8 ? want : kNumSms * 8), 256, 0, st>>>(
+      static_cast<const uint32_t*>(a), lda_bytes / 4, static_cast<const uint32_t*>(b), ldb_bytes / 4,
+      rows, words, first);
+  count_launch();
+}
+
+template <typename TI, typename TO>
+__global__ void k_convert(const TI* __restrict__ in, TO* __restrict__ out, int64_t n) {
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[e] = static_cast<TO>(in[e]);
+}
+template <typename TI, typename TO>
+void launch_convert(const TI* in, TO* out, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  const int64_t want = (n + 255) / 256;
+  k_convert<TI, TO><<<static_cast<int>(want < kNumSms * 8 ? want : kNumSms * 8), 256, 0, st>>>(in, out, n);
+  count_launch();
+}
+template void launch_convert<double, float>(const double*, float*, int64_t, cudaStream_t);
+template void launch_convert<float, double>(const float*, double*, int64_t, cudaStream_t);
+template void launch_convert<double, double>(const double*, double*, int64_t, cudaStream_t);
+
+// bumps one double / float / bf16 value by one ulp towards +inf
+__global__ void k_bump_ulp(void* p, int kind) {
+  if (kind == 0) {
+    double* d = static_cast<double*>(p);
+    *d = nextafter(*d, INFINITY);
+  } else if (kind == 1) {
+    float* f = static_cast<float*>(p);
+    *f = nextafterf(*f, INFINITY);
+  } else {
+    uint16_t* u = static_cast<uint16_t*>(p);
+    const uint16_t v = *u;
+    // bf16 nextafter towards +inf (finite values)
+    if ((v & 0x7fff) == 0) *u = 0x0001;
+    else if (v & 0x8000) *u = static_cast<uint16_t>(v - 1);
+    else *u = static_cast<uint16_t>(v + 1);
+  }
+}
+void launch_bump_ulp(void* p, int kind, cudaStream_t st) {
+  k_bump_ulp<<<1, 1, 0, st>>>(p, kind);
+  count_launch();
+}
+
+}  // namespace bp
+
+namespace bp {
+// Places an fp64 [rows, cols] tensor into a destination of type TO with row
+// stride ld (optionally transposed: dst[c*ld + r]).
+template <typename TO>
+__global__ void k_place(const double* __restrict__ src, int64_t rows, int64_t cols, TO* __restrict__ dst,
+                        int64_t ld, int transpose) {
+  const int64_t total = rows * cols;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / cols, c = e - r * cols;
+    const TO v = static_cast<TO>(src[e]);
+    if (transpose) dst[c * ld + r] = v; else dst[r * ld + c] = v;
+  }
+}
+template <typename TO>
+void launch_place(const double* src, int64_t rows, int64_t cols, TO* dst, int64_t ld, int transpose,
+                  cudaStream_t st) {
+  const int64_t total = rows * cols;
+  if (total <= 0) return;
+  const int64_t want = (total + 255) / 256;
+  k_place<TO><<<static_cast<int>(want < kNumSms * 16 ? want : kNumSms * 16), 256, 0, st>>>(src, rows, cols, dst, ld, transpose);
+  count_launch();
+}
+template void launch_place<double>(const double*, int64_t, int64_t, double*, int64_t, int, cudaStream_t);
+template void launch_place<float>(const double*, int64_t, int64_t, float*, int64_t, int, cudaStream_t);
+template void launch_place<__nv_bfloat16>(const double*, int64_t, int64_t, __nv_bfloat16*, int64_t, int, cudaStream_t);
+}  // namespace bp

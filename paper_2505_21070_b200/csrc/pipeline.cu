@@ -1,0 +1,570 @@
+// run_pipeline (engine.cpp:255-497) on B200s: the host replays the static
+// schedule (schedule.cpp); rank 0 owns the block latents, the noise pool
+// and the Euler updates; stage j runs on rank j (NCCL transport, one process
+// per GPU) or all stages share one GPU (loopback). Hidden states move
+// between stages with ncclSend/ncclRecv on dedicated streams, double-buffered
+// and event-chained to compute, so transfers overlap the next pass.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "device.cuh"
+#include "kernels_simt.cuh"
+#include "schedule.hpp"
+#include "stage.hpp"
+
+#define BP_NCCL(call)                                                                  \
+  do {                                                                                 \
+    ncclResult_t r_ = (call);                                                          \
+    if (r_ != ncclSuccess)                                                             \
+      ::bp::fail(BP_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));     \
+  } while (0)
+
+namespace bp {
+
+class Pipeline {
+ public:
+  Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, const uint8_t* ids);
+  ~Pipeline();
+  void run(bp_emit_fn emit, void* user);
+  Schedule sched;
+  bp_pipeline_stats stats{};
+  std::vector<std::vector<double>> trace;  // host eps per pass (record_trace)
+  std::vector<int64_t> trace_rows;
+  std::vector<const double*> block_dev;    // emitted blocks' device latents (rank 0)
+  std::vector<int64_t> block_count;
+  bool profiling = false;
+
+ private:
+  void run_rank0_loopback(bp_emit_fn emit, void* user);
+  void run_nccl(bp_emit_fn emit, void* user);
+  void build_pool_and_check(cudaStream_t st);
+  void append_block(const SchedBlock& b, cudaStream_t st);
+  void assemble(const SchedPass& p, cudaStream_t st);
+  void step(const SchedPass& p, const void* eps, cudaStream_t st);
+  void emit_block(const SchedBlock& b, cudaStream_t st);
+  StageInput stage_input(const SchedPass& p, int stage, const void* payload, bool* use_cache_checked);
+  void before_stage(const SchedPass& p, int stage, Stage& s, StageInput* in);
+  void after_stage(const SchedPass& p, int stage, Stage& s);
+  double* version_ptr(int64_t block, int version) const;
+
+  bp_pipeline_desc d_;
+  int rank_, world_, device_;
+  int64_t tpf_, C_, hwc_;
+  std::vector<std::unique_ptr<Stage>> stages_;  // index = stage id (only local ones non-null)
+  cudaStream_t st_ = nullptr;
+  // rank 0 state
+  DevBuf pool_, latents_, payload_, pass_levels_, pass_ids_, flags_;
+  std::vector<int64_t> block_off_;             // element offset of each block's 3 versions
+  std::vector<int64_t> pass_off_;              // offset into pass_levels_/pass_ids_
+  std::vector<double*> pinned_;                // emission buffers
+  bool fault_pending_ = false;
+  int64_t launches_at_start_ = 0;
+  // NCCL
+  ncclComm_t comm_prev_ = nullptr, comm_next_ = nullptr, comm_eps_ = nullptr;
+  cudaStream_t s_recv_ = nullptr, s_send_ = nullptr, s_eps_ = nullptr;
+  DevBuf rbuf_[2], ebuf_[2];
+};
+
+extern std::atomic<int64_t> g_launches;
+
+Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, const uint8_t* ids)
+    : sched(build_schedule(d)), d_(d), rank_(rank), world_(world), device_(device) {
+  const int N = d.devices;
+  if (d.transport == BP_TRANSPORT_NCCL) {
+    if (world != N) fail(BP_ERR_CONFIG, "NCCL transport needs world == devices (one stage per GPU)");
+    if (rank < 0 || rank >= world) fail(BP_ERR_CONFIG, "bad rank");
+    if (N > 1 && ids == nullptr) fail(BP_ERR_CONFIG, "NCCL transport needs unique ids");
+  } else {
+    if (world != 1 || rank != 0) fail(BP_ERR_CONFIG, "loopback runs as a single process");
+  }
+  BP_CUDA(cudaSetDevice(device_));
+  BP_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  tpf_ = static_cast<int64_t>(d.model.height) * d.model.width;
+  C_ = d.model.channels;
+  hwc_ = tpf_ * C_;
+  stages_.resize(static_cast<size_t>(N));
+  for (int j = 0; j < N; ++j) {
+    const bool local = d.transport != BP_TRANSPORT_NCCL || j == rank;
+    if (!local) continue;
+    stages_[static_cast<size_t>(j)] = std::make_unique<Stage>(
+        device_, d.model, d.seed_model, d.seed_context, sched.begins[static_cast<size_t>(j)],
+        sched.ends[static_cast<size_t>(j)], d.precision, st_);
+  }
+  if (rank_ == 0) {
+    const int M = d.num_b + d.num_c / 2;
+    pool_.alloc(static_cast<size_t>(M) * hwc_ * 8);
+    flags_.alloc(static_cast<size_t>(M) * M * 4);
+    int64_t at = 0;
+    for (const SchedBlock& b : sched.blocks) {
+      block_off_.push_back(at);
+      at += 3 * b.frames * hwc_;  // three state versions (current, previous, one older)
+    }
+    latents_.alloc(static_cast<size_t>(at) * 8);
+    payload_.alloc(static_cast<size_t>(sched.max_tokens) * C_ * 8);
+    std::vector<int32_t> lv;
+    std::vector<int64_t> fi;
+    for (const SchedPass& p : sched.passes) {
+      pass_off_.push_back(static_cast<int64_t>(lv.size()));
+      lv.insert(lv.end(), p.frame_levels.begin(), p.frame_levels.end());
+      fi.insert(fi.end(), p.frame_ids.begin(), p.frame_ids.end());
+    }
+    pass_levels_.alloc(std::max<size_t>(lv.size(), 1) * 4);
+    pass_ids_.alloc(std::max<size_t>(fi.size(), 1) * 8);
+    BP_CUDA(cudaMemcpy(pass_levels_.p, lv.data(), lv.size() * 4, cudaMemcpyHostToDevice));
+    BP_CUDA(cudaMemcpy(pass_ids_.p, fi.data(), fi.size() * 8, cudaMemcpyHostToDevice));
+    for (int64_t id : sched.emission) {
+      double* h = nullptr;
+      const size_t n = static_cast<size_t>(sched.blocks[static_cast<size_t>(id - 1)].frames * hwc_);
+      BP_CUDA(cudaMallocHost(&h, n * 8));
+      pinned_.push_back(h);
+    }
+  } else {
+    // non-zero ranks need the per-pass frame metadata only on stage 0 (rank 0)
+  }
+  if (d.transport == BP_TRANSPORT_NCCL && N > 1) {
+    auto id_of = [&](int k) {
+      ncclUniqueId u;
+      std::memcpy(&u, ids + 128 * k, sizeof(u));
+      return u;
+    };
+    // pair (j, j+1) uses id j; the eps return (N-1 -> 0) uses id N-1.
+    if (rank_ > 0) BP_NCCL(ncclCommInitRank(&comm_prev_, 2, id_of(rank_ - 1), 1));
+    if (rank_ + 1 < N) BP_NCCL(ncclCommInitRank(&comm_next_, 2, id_of(rank_), 0));
+    if (rank_ == N - 1) BP_NCCL(ncclCommInitRank(&comm_eps_, 2, id_of(N - 1), 0));
+    if (rank_ == 0) BP_NCCL(ncclCommInitRank(&comm_eps_, 2, id_of(N - 1), 1));
+    BP_CUDA(cudaStreamCreateWithFlags(&s_recv_, cudaStreamNonBlocking));
+    BP_CUDA(cudaStreamCreateWithFlags(&s_send_, cudaStreamNonBlocking));
+    BP_CUDA(cudaStreamCreateWithFlags(&s_eps_, cudaStreamNonBlocking));
+    const Stage& s = *stages_[static_cast<size_t>(rank_)];
+    const size_t hid = static_cast<size_t>(sched.max_tokens) * d.model.hidden * s.act_bytes();
+    const size_t eps = static_cast<size_t>(sched.max_tokens) * C_ * s.eps_bytes();
+    if (rank_ > 0) { rbuf_[0].alloc(hid); rbuf_[1].alloc(hid); }
+    if (rank_ == 0) { ebuf_[0].alloc(eps); ebuf_[1].alloc(eps); }
+  }
+  BP_CUDA(cudaDeviceSynchronize());
+}
+
+Pipeline::~Pipeline() {
+  cudaSetDevice(device_);
+  cudaDeviceSynchronize();
+  for (double* h : pinned_) cudaFreeHost(h);
+  if (comm_prev_) ncclCommDestroy(comm_prev_);
+  if (comm_next_) ncclCommDestroy(comm_next_);
+  if (comm_eps_) ncclCommDestroy(comm_eps_);
+  stages_.clear();
+  if (s_recv_) cudaStreamDestroy(s_recv_);
+  if (s_send_) cudaStreamDestroy(s_send_);
+  if (s_eps_) cudaStreamDestroy(s_eps_);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+double* Pipeline::version_ptr(int64_t block, int version) const {
+  const SchedBlock& b = sched.blocks[static_cast<size_t>(block - 1)];
+  return latents_.as<double>() + block_off_[static_cast<size_t>(block - 1)] + (version % 3) * b.frames * hwc_;
+}
+
+// build_pool (noise.cpp:26-48) on the device, plus its collision check.
+void Pipeline::build_pool_and_check(cudaStream_t st) {
+  const int M = d_.num_b + d_.num_c / 2;
+  const uint64_t tag0 = 0;
+  launch_normal_fill(derive_seed(d_.seed_noise, &tag0, 1), M * hwc_, 1.0, pool_.as<double>(), st);
+  if (M > 1) {
+    BP_CUDA(cudaMemsetAsync(flags_.p, 0, static_cast<size_t>(M) * M * 4, st));
+    launch_pool_differs(pool_.as<double>(), M, hwc_, flags_.as<int>(), st);
+    std::vector<int> f(static_cast<size_t>(M) * M);
+    BP_CUDA(cudaMemcpyAsync(f.data(), flags_.p, f.size() * 4, cudaMemcpyDeviceToHost, st));
+    BP_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < M; ++i)
+      for (int j = i + 1; j < M; ++j)
+        if (!f[static_cast<size_t>(i) * M + j]) fail(BP_ERR_CONFIG, "noise pool entries collided; change the noise seed");
+  }
+}
+
+// make_block's frames: stack_entries of the pool (noise.cpp:12-22) or fresh normals.
+void Pipeline::append_block(const SchedBlock& b, cudaStream_t st) {
+  double* dst = version_ptr(b.id, 0);
+  if (b.fresh) {
+    launch_normal_fill(b.fresh_state, b.frames * hwc_, 1.0, dst, st);
+    return;
+  }
+  // at most 4 segments per launch
+  for (size_t i = 0; i < b.noise_ids.size(); i += 4) {
+    GatherSegs g;
+    for (size_t k = i; k < b.noise_ids.size() && k < i + 4; ++k)
+      g.add(pool_.as<double>() + static_cast<int64_t>(b.noise_ids[k]) * hwc_, 1);
+    launch_gather_rows(g, hwc_, dst + static_cast<int64_t>(i) * hwc_, st);
+  }
+}
+
+// vcat(explicit context frames, center frames) (engine.cpp:373-383).
+void Pipeline::assemble(const SchedPass& p, cudaStream_t st) {
+  GatherSegs g;
+  if (p.ctx != CtxSrc::None)
+    g.add(version_ptr(p.ctx_block, p.ctx_version) + static_cast<int64_t>(p.ctx_first_frame) * hwc_,
+          p.ctx_frames * tpf_);
+  g.add(version_ptr(p.block, p.version), p.center_tokens);
+  launch_gather_rows(g, C_, payload_.as<double>(), st);
+}
+
+// scheduler_step on the center rows + apply_update (engine.cpp:440-445).
+void Pipeline::step(const SchedPass& p, const void* eps, cudaStream_t st) {
+  const int64_t off = (p.tokens - p.center_tokens) * C_;
+  const int64_t n = p.center_tokens * C_;
+  double* x = version_ptr(p.block, p.version);
+  double* out = version_ptr(p.block, p.version + 1);
+  if (p.level < 1 || p.level > d_.steps) fail(BP_ERR_SCHEDULER, "level outside 1..T");
+  if (d_.precision == BP_PREC_F64)
+    launch_scheduler_step<double>(x, static_cast<const double*>(eps) + off, n, d_.steps, out, st);
+  else
+    launch_scheduler_step<float>(x, static_cast<const float*>(eps) + off, n, d_.steps, out, st);
+  if (d_.record_trace) {
+    std::vector<double> h(static_cast<size_t>(p.tokens * C_));
+    if (d_.precision == BP_PREC_F64) {
+      BP_CUDA(cudaMemcpyAsync(h.data(), eps, h.size() * 8, cudaMemcpyDeviceToHost, st));
+      BP_CUDA(cudaStreamSynchronize(st));
+    } else {
+      std::vector<float> f(h.size());
+      BP_CUDA(cudaMemcpyAsync(f.data(), eps, f.size() * 4, cudaMemcpyDeviceToHost, st));
+      BP_CUDA(cudaStreamSynchronize(st));
+      for (size_t i = 0; i < f.size(); ++i) h[i] = f[i];
+    }
+    trace.push_back(std::move(h));
+    trace_rows.push_back(p.tokens);
+  }
+}
+
+void Pipeline::emit_block(const SchedBlock& b, cudaStream_t st) {
+  const size_t k = block_dev.size();
+  const double* src = version_ptr(b.id, d_.steps);
+  block_dev.push_back(src);
+  block_count.push_back(b.frames * hwc_);
+  BP_CUDA(cudaMemcpyAsync(pinned_[k], src, static_cast<size_t>(b.frames * hwc_) * 8, cudaMemcpyDeviceToHost, st));
+}
+
+// DeviceWorker::process cache checks (engine.cpp:142-171) before the forward.
+void Pipeline::before_stage(const SchedPass& p, int j, Stage& s, StageInput* in) {
+  in->tokens = p.tokens;
+  in->nframes = static_cast<int>(p.frame_levels.size());
+  if (rank_ == 0) {
+    in->d_levels = pass_levels_.as<int32_t>() + pass_off_[static_cast<size_t>(p.index)];
+    in->d_frame_ids = pass_ids_.as<int64_t>() + pass_off_[static_cast<size_t>(p.index)];
+  }
+  in->capture_frames = p.capture_frames;
+  in->mode = d_.cache_mode;
+  in->record_inputs = d_.check_cache && d_.cache_mode == BP_CACHE_CACHED;
+  in->use_prev = 0;
+  if (p.cached_context_id >= 0 && d_.cache_mode != BP_CACHE_DISABLED) {
+    if (d_.cache_mode == BP_CACHE_CACHED) {
+      if (!s.cache_valid() || s.cache_block() != p.cached_context_id)
+        fail(BP_ERR_CACHE, "device " + std::to_string(j) + " expected cache of block " +
+                               std::to_string(p.cached_context_id));
+      if (s.cache_level() != p.level + 1)
+        fail(BP_ERR_CACHE, "cache level " + std::to_string(s.cache_level()) +
+                               " does not precede pass level " + std::to_string(p.level));
+      if (d_.check_cache) {
+        if (!s.rec_valid() || s.rec_block() != s.cache_block())
+          fail(BP_ERR_CACHE, "cache audit has no recording for block " + std::to_string(s.cache_block()));
+        const std::string report = s.audit();
+        if (!report.empty()) fail(BP_ERR_CACHE, report);
+      }
+      in->use_prev = 1;
+    } else {
+      if (!s.rec_valid() || s.rec_block() != p.cached_context_id)
+        fail(BP_ERR_CACHE, "device " + std::to_string(j) + " expected recorded rows of block " +
+                               std::to_string(p.cached_context_id));
+      in->use_prev = 2;
+    }
+  }
+}
+
+void Pipeline::after_stage(const SchedPass& p, int j, Stage& s) {
+  s.tag_entries(p.block, p.level);
+  // fault injection: one cached V value on device 0, once (engine.cpp:185-189)
+  if (fault_pending_ && j == 0 && s.cache_valid() && !p.capture_frames.empty() &&
+      d_.cache_mode == BP_CACHE_CACHED) {
+    s.bump_ulp(0, 1, 0);
+    fault_pending_ = false;
+  }
+}
+
+void Pipeline::run(bp_emit_fn emit, void* user) {
+  BP_CUDA(cudaSetDevice(device_));
+  trace.clear();
+  trace_rows.clear();
+  block_dev.clear();
+  block_count.clear();
+  fault_pending_ = d_.fault_inject_ulp != 0;
+  launches_at_start_ = g_launches.load();
+  if (d_.transport == BP_TRANSPORT_NCCL && d_.devices > 1) run_nccl(emit, user);
+  else run_rank0_loopback(emit, user);
+  stats.passes = static_cast<int64_t>(sched.passes.size());
+  stats.kernel_launches = g_launches.load() - launches_at_start_;
+  stats.peak_bytes = g_dev_peak.load();
+}
+
+void Pipeline::run_rank0_loopback(bp_emit_fn emit, void* user) {
+  cudaStream_t st = st_;
+  cudaEvent_t e0, e1;
+  BP_CUDA(cudaEventCreate(&e0));
+  BP_CUDA(cudaEventCreate(&e1));
+  BP_CUDA(cudaEventRecord(e0, st));
+  build_pool_and_check(st);
+  size_t next_append = 0;
+  size_t next_emit = 0;
+  const int N = d_.devices;
+  int64_t boundary = 0;
+  for (const SchedPass& p : sched.passes) {
+    while (next_append < sched.blocks.size() && sched.blocks[next_append].append_round <= p.round)
+      append_block(sched.blocks[next_append++], st);
+    assemble(p, st);
+    const void* cur = payload_.p;
+    for (int j = 0; j < N; ++j) {
+      Stage& s = *stages_[static_cast<size_t>(j)];
+      StageInput in;
+      before_stage(p, j, s, &in);
+      in.payload = cur;
+      cur = s.forward(in);
+      after_stage(p, j, s);
+      if (j + 1 < N) boundary += p.tokens * d_.model.hidden * static_cast<int64_t>(s.act_bytes());
+    }
+    step(p, cur, st);
+    if (p.finishes_block) {
+      const SchedBlock& b = sched.blocks[static_cast<size_t>(p.block - 1)];
+      emit_block(b, st);
+      ++next_emit;
+    }
+  }
+  BP_CUDA(cudaEventRecord(e1, st));
+  BP_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  BP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  stats.gpu_ms = ms;
+  stats.boundary_bytes = boundary;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (emit) {
+    for (size_t k = 0; k < sched.emission.size(); ++k) {
+      const SchedBlock& b = sched.blocks[static_cast<size_t>(sched.emission[k] - 1)];
+      emit(user, b.id, b.frames, pinned_[k], b.noise_ids.data(), static_cast<int32_t>(b.noise_ids.size()),
+           b.frame_ids.data());
+    }
+  }
+}
+
+// One process per GPU. Stream layout per rank: st_ (compute), s_recv_
+// (hidden state from rank-1), s_send_ (hidden state to rank+1), s_eps_
+// (eps return N-1 -> 0). Two-deep buffer rings; every cross-stream edge is an
+// event. Rank 0 orders its compute stream by the logical slot clock so the
+// data dependencies of the ideal schedule are never inverted.
+void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
+  const int N = d_.devices;
+  const int j = rank_;
+  Stage& s = *stages_[static_cast<size_t>(j)];
+  const int64_t P = static_cast<int64_t>(sched.passes.size());
+  const size_t abytes = s.act_bytes(), ebytes = s.eps_bytes();
+  const ncclDataType_t adt = abytes == 8 ? ncclFloat64 : ncclFloat32;
+  const ncclDataType_t edt = ebytes == 8 ? ncclFloat64 : ncclFloat32;
+  const int H = d_.model.hidden;
+  std::vector<cudaEvent_t> ev_fwd(P), ev_recv(P), ev_sent(P), ev_used(P);
+  for (int64_t i = 0; i < P; ++i) {
+    BP_CUDA(cudaEventCreateWithFlags(&ev_fwd[i], cudaEventDisableTiming));
+    BP_CUDA(cudaEventCreateWithFlags(&ev_recv[i], cudaEventDisableTiming));
+    BP_CUDA(cudaEventCreateWithFlags(&ev_sent[i], cudaEventDisableTiming));
+    BP_CUDA(cudaEventCreateWithFlags(&ev_used[i], cudaEventDisableTiming));
+  }
+  cudaEvent_t e0, e1;
+  BP_CUDA(cudaEventCreate(&e0));
+  BP_CUDA(cudaEventCreate(&e1));
+  BP_CUDA(cudaEventRecord(e0, st_));
+  // Stage outputs alternate between two staging copies so a send can
+  // overlap the next forward.
+  DevBuf out_ring[2];
+  const size_t out_bytes = static_cast<size_t>(sched.max_tokens) *
+                           (s.is_last() ? static_cast<size_t>(C_) * ebytes : static_cast<size_t>(H) * abytes);
+  out_ring[0].alloc(out_bytes);
+  out_ring[1].alloc(out_bytes);
+  int64_t boundary = 0;
+
+  auto forward_pass = [&](const SchedPass& p, const void* payload) {
+    StageInput in;
+    before_stage(p, j, s, &in);
+    in.payload = payload;
+    const void* out = s.forward(in);
+    after_stage(p, j, s);
+    const int64_t i = p.index;
+    if (i >= 2) BP_CUDA(cudaStreamWaitEvent(st_, ev_sent[i - 2], 0));  // ring slot free
+    const size_t n = static_cast<size_t>(p.tokens) * (s.is_last() ? C_ * ebytes : H * abytes);
+    BP_CUDA(cudaMemcpyAsync(out_ring[i & 1].p, out, n, cudaMemcpyDeviceToDevice, st_));
+    BP_CUDA(cudaEventRecord(ev_fwd[i], st_));
+    return out_ring[i & 1].p;
+  };
+  auto send_to = [&](ncclComm_t comm, cudaStream_t ss, const SchedPass& p, const void* buf, int peer,
+                     size_t count, ncclDataType_t dt) {
+    BP_CUDA(cudaStreamWaitEvent(ss, ev_fwd[p.index], 0));
+    BP_NCCL(ncclSend(buf, count, dt, peer, comm, ss));
+    BP_CUDA(cudaEventRecord(ev_sent[p.index], ss));
+  };
+
+  if (j == 0) {
+    build_pool_and_check(st_);
+    // merge stage-0 passes and eps updates by logical time
+    struct Op { double t; int kind; int64_t pass; };
+    std::vector<Op> ops;
+    for (const SchedPass& p : sched.passes) {
+      ops.push_back({static_cast<double>(p.slots[0]), 0, p.index});
+      ops.push_back({static_cast<double>(p.completion) + 0.5, 1, p.index});
+    }
+    std::stable_sort(ops.begin(), ops.end(), [](const Op& a, const Op& b) { return a.t < b.t; });
+    // eps receives are posted in pass order; receive i reuses the ring slot
+    // of receive i-2, so it is posted right after STEP(i-2) is enqueued
+    // (an event must be recorded before another stream can wait on it).
+    auto post_eps_recv = [&](int64_t i) {
+      if (i >= P) return;
+      const SchedPass& p = sched.passes[static_cast<size_t>(i)];
+      if (i >= 2) BP_CUDA(cudaStreamWaitEvent(s_eps_, ev_used[i - 2], 0));
+      BP_NCCL(ncclRecv(ebuf_[i & 1].p, static_cast<size_t>(p.tokens) * C_, edt, 0, comm_eps_, s_eps_));
+      BP_CUDA(cudaEventRecord(ev_recv[i], s_eps_));
+    };
+    post_eps_recv(0);
+    post_eps_recv(1);
+    size_t next_append = 0;
+    for (const Op& op : ops) {
+      const SchedPass& p = sched.passes[static_cast<size_t>(op.pass)];
+      if (op.kind == 0) {
+        while (next_append < sched.blocks.size() && sched.blocks[next_append].append_round <= p.round)
+          append_block(sched.blocks[next_append++], st_);
+        assemble(p, st_);
+        const void* out = forward_pass(p, payload_.p);
+        send_to(comm_next_, s_send_, p, out, 1, static_cast<size_t>(p.tokens) * H, adt);
+        boundary += p.tokens * H * static_cast<int64_t>(abytes);
+      } else {
+        BP_CUDA(cudaStreamWaitEvent(st_, ev_recv[p.index], 0));
+        step(p, ebuf_[p.index & 1].p, st_);
+        BP_CUDA(cudaEventRecord(ev_used[p.index], st_));
+        post_eps_recv(p.index + 2);
+        if (p.finishes_block) emit_block(sched.blocks[static_cast<size_t>(p.block - 1)], st_);
+      }
+    }
+  } else {
+    auto post_recv = [&](int64_t i) {
+      if (i >= P) return;
+      const SchedPass& p = sched.passes[static_cast<size_t>(i)];
+      if (i >= 2) BP_CUDA(cudaStreamWaitEvent(s_recv_, ev_used[i - 2], 0));
+      BP_NCCL(ncclRecv(rbuf_[i & 1].p, static_cast<size_t>(p.tokens) * H, adt, 0, comm_prev_, s_recv_));
+      BP_CUDA(cudaEventRecord(ev_recv[i], s_recv_));
+    };
+    post_recv(0);
+    post_recv(1);
+    for (int64_t i = 0; i < P; ++i) {
+      const SchedPass& p = sched.passes[static_cast<size_t>(i)];
+      BP_CUDA(cudaStreamWaitEvent(st_, ev_recv[i], 0));
+      const void* out = forward_pass(p, rbuf_[i & 1].p);
+      BP_CUDA(cudaEventRecord(ev_used[i], st_));  // input copied into the stage's residual stream
+      post_recv(i + 2);
+      if (j + 1 < N) {
+        send_to(comm_next_, s_send_, p, out, 1, static_cast<size_t>(p.tokens) * H, adt);
+        boundary += p.tokens * H * static_cast<int64_t>(abytes);
+      } else {
+        send_to(comm_eps_, s_send_, p, out, 1, static_cast<size_t>(p.tokens) * C_, edt);
+      }
+    }
+  }
+  BP_CUDA(cudaStreamSynchronize(s_send_));
+  if (s_eps_) BP_CUDA(cudaStreamSynchronize(s_eps_));
+  BP_CUDA(cudaStreamSynchronize(s_recv_));
+  BP_CUDA(cudaEventRecord(e1, st_));
+  BP_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  BP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  stats.gpu_ms = ms;
+  stats.boundary_bytes = boundary;
+  for (int64_t i = 0; i < P; ++i) {
+    cudaEventDestroy(ev_fwd[i]); cudaEventDestroy(ev_recv[i]);
+    cudaEventDestroy(ev_sent[i]); cudaEventDestroy(ev_used[i]);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (j == 0 && emit) {
+    for (size_t k = 0; k < sched.emission.size(); ++k) {
+      const SchedBlock& b = sched.blocks[static_cast<size_t>(sched.emission[k] - 1)];
+      emit(user, b.id, b.frames, pinned_[k], b.noise_ids.data(), static_cast<int32_t>(b.noise_ids.size()),
+           b.frame_ids.data());
+    }
+  }
+}
+
+}  // namespace bp
+
+// ---- C-ABI -------------------------------------------------------------------------
+struct bp_pipeline {
+  std::unique_ptr<bp::Pipeline> p;
+};
+
+extern "C" {
+
+bp_status bp_nccl_unique_id(uint8_t out[128]) {
+  return bp::guarded([&] {
+    ncclUniqueId u;
+    BP_NCCL(ncclGetUniqueId(&u));
+    static_assert(sizeof(u) == 128, "ncclUniqueId size");
+    std::memcpy(out, &u, 128);
+  });
+}
+
+bp_status bp_pipeline_create(const bp_pipeline_desc* desc, int32_t rank, int32_t world, int32_t device,
+                             const uint8_t* nccl_ids, bp_pipeline** out) {
+  return bp::guarded([&] {
+    if (!desc || !out) bp::fail(BP_ERR_CONFIG, "null argument");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) bp::fail(BP_ERR_CUDA, "no CUDA device");
+    auto h = std::make_unique<bp_pipeline>();
+    h->p = std::make_unique<bp::Pipeline>(*desc, rank, world, device, nccl_ids);
+    *out = h.release();
+  });
+}
+
+bp_status bp_pipeline_destroy(bp_pipeline* p) {
+  return bp::guarded([&] { delete p; });
+}
+
+bp_status bp_pipeline_run(bp_pipeline* p, bp_emit_fn emit, void* user) {
+  return bp::guarded([&] { p->p->run(emit, user); });
+}
+
+bp_status bp_pipeline_get_stats(bp_pipeline* p, bp_pipeline_stats* out) {
+  return bp::guarded([&] { *out = p->p->stats; });
+}
+
+bp_status bp_pipeline_set_profiling(bp_pipeline* p, int32_t on) {
+  return bp::guarded([&] { p->p->profiling = on != 0; });
+}
+
+int64_t bp_pipeline_ntrace(bp_pipeline* p) { return static_cast<int64_t>(p->p->trace.size()); }
+
+bp_status bp_pipeline_trace(bp_pipeline* p, int64_t i, int64_t* round, int64_t* block_id, int64_t* rows,
+                            int64_t* cols, double* eps) {
+  return bp::guarded([&] {
+    if (i < 0 || i >= static_cast<int64_t>(p->p->trace.size())) bp::fail(BP_ERR_DIMENSION, "trace index");
+    const bp::SchedPass& ps = p->p->sched.passes[static_cast<size_t>(i)];
+    *round = ps.round;
+    *block_id = ps.block;
+    *rows = p->p->trace_rows[static_cast<size_t>(i)];
+    *cols = p->p->sched.desc.model.channels;
+    if (eps) std::memcpy(eps, p->p->trace[static_cast<size_t>(i)].data(), p->p->trace[static_cast<size_t>(i)].size() * 8);
+  });
+}
+
+bp_status bp_pipeline_block(bp_pipeline* p, int64_t i, const double** dev_data, int64_t* count) {
+  return bp::guarded([&] {
+    if (i < 0 || i >= static_cast<int64_t>(p->p->block_dev.size())) bp::fail(BP_ERR_DIMENSION, "block index");
+    *dev_data = p->p->block_dev[static_cast<size_t>(i)];
+    *count = p->p->block_count[static_cast<size_t>(i)];
+  });
+}
+
+}  // extern "C"

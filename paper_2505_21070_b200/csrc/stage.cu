@@ -1,0 +1,584 @@
+// Stage: device-resident ModelChunk + forward_chunk. See stage.hpp.
+#include "stage.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "kernels_bf16.cuh"
+#include "kernels_simt.cuh"
+#include "schedule.hpp"
+
+namespace bp {
+
+namespace {
+
+// Weight roles (model.cpp:17-24); the numeric values key the streams.
+enum Role : uint64_t {
+  kWq = 0, kWk, kWv, kWo, kCq, kCk, kCv, kCo, kW1, kW2,
+  kLn1G, kLn1B, kLn2G, kLn2B, kLn3G, kLn3B,
+  kPatchify = 100, kHead = 101
+};
+
+size_t align256(size_t n) { return (n + 255) & ~static_cast<size_t>(255); }
+
+}  // namespace
+
+Stage::Stage(int device, const bp_model_desc& m, uint64_t seed_model, uint64_t seed_context, int begin,
+             int end, int precision, cudaStream_t stream)
+    : device_(device), prec_(precision), m_(m), begin_(begin), end_(end), stream_(stream) {
+  validate_model(m);
+  if (begin < 0 || end > m.layers || begin >= end)
+    fail(BP_ERR_CONFIG, "bad layer range [" + std::to_string(begin) + "," + std::to_string(end) +
+                            ") for L=" + std::to_string(m.layers));
+  if (prec_ < BP_PREC_F64 || prec_ > BP_PREC_BF16) fail(BP_ERR_CONFIG, "unknown precision");
+  h_ = m.hidden;
+  heads_ = m.heads;
+  dh_ = h_ / heads_;
+  F_ = ffn_width(m);
+  C_ = m.channels;
+  tpf_ = m.height * m.width;
+  Lc_ = m.context_len;
+  if (prec_ == BP_PREC_BF16) {
+    if (h_ % 64 != 0 || F_ % 64 != 0) fail(BP_ERR_CONFIG, "bf16 path needs hidden and ffn multiples of 64");
+    if (dh_ % 16 != 0 || dh_ > 256) fail(BP_ERR_CONFIG, "bf16 path needs head dim % 16 == 0 and <= 256");
+  }
+  BP_CUDA(cudaSetDevice(device_));
+  if (!stream_) {
+    BP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    own_stream_ = true;
+  }
+  build_weights(seed_model, seed_context);
+}
+
+Stage::~Stage() {
+  cudaSetDevice(device_);
+  cudaStreamSynchronize(stream_);
+  if (own_stream_) cudaStreamDestroy(stream_);
+}
+
+size_t Stage::act_bytes() const { return prec_ == BP_PREC_F64 ? 8 : 4; }
+
+void Stage::build_weights(uint64_t seed_model, uint64_t seed_context) {
+  const int nl = end_ - begin_;
+  const bool bf = prec_ == BP_PREC_BF16;
+  const size_t te = prec_ == BP_PREC_F64 ? 8 : 4;  // SIMT element / fp32 side tensors
+  const size_t me = bf ? 2 : te;                    // matrix element
+  const size_t hh = static_cast<size_t>(h_) * h_;
+  const size_t hF = static_cast<size_t>(h_) * F_;
+  struct Off { size_t wqkv, wo, cq, co, w1, w2, ln, ctx_kv; };
+  std::vector<Off> offs(static_cast<size_t>(nl));
+  size_t at = 0;
+  for (int l = 0; l < nl; ++l) {
+    Off& o = offs[static_cast<size_t>(l)];
+    o.wqkv = at; at += align256(3 * hh * me);
+    o.wo = at; at += align256(hh * me);
+    o.cq = at; at += align256(hh * me);
+    o.co = at; at += align256(hh * me);
+    o.w1 = at; at += align256(hF * me);
+    o.w2 = at; at += align256(hF * me);
+    o.ln = at; at += align256(6 * static_cast<size_t>(h_) * te);
+    o.ctx_kv = at; at += align256(static_cast<size_t>(Lc_) * 2 * h_ * me);
+  }
+  size_t off_in = 0, off_out = 0;
+  if (is_first()) { off_in = at; at += align256(static_cast<size_t>(C_) * h_ * 8); }
+  if (is_last()) { off_out = at; at += align256(static_cast<size_t>(h_) * C_ * te); }
+  weights_.alloc(at);
+  char* base = weights_.as<char>();
+  lw_.resize(static_cast<size_t>(nl));
+  for (int l = 0; l < nl; ++l) {
+    const Off& o = offs[static_cast<size_t>(l)];
+    LayerW& w = lw_[static_cast<size_t>(l)];
+    w.wqkv = base + o.wqkv; w.wo = base + o.wo; w.cq = base + o.cq; w.co = base + o.co;
+    w.w1 = base + o.w1; w.w2 = base + o.w2; w.ln = base + o.ln; w.ctx_kv = base + o.ctx_kv;
+  }
+  if (is_first()) w_in_ = base + off_in;
+  if (is_last()) w_out_ = base + off_out;
+
+  // Scratch: fp64 draw buffer, context, and the cross K|V weights for hoisting.
+  const size_t max_numel = std::max({hF, hh, static_cast<size_t>(Lc_) * h_,
+                                     static_cast<size_t>(C_) * h_});
+  DevBuf gen, ctx64, ctxT, ckvT, kvT;
+  gen.alloc(max_numel * 8);
+  ctx64.alloc(static_cast<size_t>(Lc_) * h_ * 8);
+  ctxT.alloc(static_cast<size_t>(Lc_) * h_ * te);
+  ckvT.alloc(2 * hh * te);
+  kvT.alloc(static_cast<size_t>(Lc_) * 2 * h_ * te);
+  double* g = gen.as<double>();
+  cudaStream_t st = stream_;
+
+  auto draw = [&](uint64_t layer, uint64_t role, int64_t numel, int64_t fan_in) {
+    // draw (model.cpp:26-30): RandomSource(derive_seed(seed, {layer, role})), sigma 1/sqrt(fan_in)
+    const uint64_t state = derive_seed2(seed_model, layer, role);
+    launch_normal_fill(state, numel, 1.0 / std::sqrt(static_cast<double>(fan_in)), g, st);
+  };
+  // place an fp64 [rows, cols] draw into a matrix slot of this precision
+  auto place_mat = [&](void* dst, int64_t rows, int64_t cols, int64_t ld, int64_t col_off, bool transposed_store) {
+    if (bf) {
+      // K-major weights: W^T [cols(out), rows(in)]; col_off counts output rows
+      launch_place<bf16>(g, rows, cols, static_cast<bf16*>(dst) + col_off * rows, rows, 1, st);
+    } else if (prec_ == BP_PREC_F64) {
+      launch_place<double>(g, rows, cols, static_cast<double*>(dst) + col_off, ld, 0, st);
+    } else {
+      launch_place<float>(g, rows, cols, static_cast<float*>(dst) + col_off, ld, 0, st);
+    }
+    (void)transposed_store;
+  };
+  auto place_side = [&](void* dst, int64_t n, int64_t off) {  // fp32/fp64 vectors
+    if (prec_ == BP_PREC_F64) launch_place<double>(g, 1, n, static_cast<double*>(dst) + off, n, 0, st);
+    else launch_place<float>(g, 1, n, static_cast<float*>(dst) + off, n, 0, st);
+  };
+
+  // context (build_context, model.cpp:150-153): RandomSource(seed_context), sigma 1
+  launch_normal_fill(seed_context, static_cast<int64_t>(Lc_) * h_, 1.0, ctx64.as<double>(), st);
+  if (prec_ == BP_PREC_F64) launch_place<double>(ctx64.as<double>(), Lc_, h_, ctxT.as<double>(), h_, 0, st);
+  else launch_place<float>(ctx64.as<double>(), Lc_, h_, ctxT.as<float>(), h_, 0, st);
+
+  for (int l = 0; l < nl; ++l) {
+    LayerW& w = lw_[static_cast<size_t>(l)];
+    const uint64_t layer = static_cast<uint64_t>(begin_ + l);
+    const int64_t H = h_;
+    for (uint64_t r = kWq; r <= kWv; ++r) {
+      draw(layer, r, H * H, H);
+      place_mat(w.wqkv, H, H, 3 * H, static_cast<int64_t>(r) * H, true);
+    }
+    draw(layer, kWo, H * H, H); place_mat(w.wo, H, H, H, 0, true);
+    draw(layer, kCq, H * H, H); place_mat(w.cq, H, H, H, 0, true);
+    draw(layer, kCo, H * H, H); place_mat(w.co, H, H, H, 0, true);
+    draw(layer, kW1, H * F_, H); place_mat(w.w1, H, F_, F_, 0, true);
+    draw(layer, kW2, static_cast<int64_t>(F_) * H, F_); place_mat(w.w2, F_, H, H, 0, true);
+    for (uint64_t r = kLn1G; r <= kLn3B; ++r) {
+      draw(layer, r, H, H);
+      place_side(w.ln, H, static_cast<int64_t>(r - kLn1G) * H);
+    }
+    // Cross-attention K|V of the fixed context, hoisted out of the per-pass
+    // loop (model.cpp:216-217 recomputes it every pass; it is constant).
+    for (uint64_t r = kCk; r <= kCv; ++r) {
+      draw(layer, r, H * H, H);
+      const int64_t off = static_cast<int64_t>(r - kCk) * H;
+      if (prec_ == BP_PREC_F64) launch_place<double>(g, H, H, ckvT.as<double>() + off, 2 * H, 0, st);
+      else launch_place<float>(g, H, H, ckvT.as<float>() + off, 2 * H, 0, st);
+    }
+    if (prec_ == BP_PREC_F64) {
+      launch_matmul<double>(ctxT.as<double>(), H, ckvT.as<double>(), 2 * H, Lc_, 2 * h_, h_,
+                            static_cast<double*>(w.ctx_kv), 2 * H, kEpiNone, nullptr, 0, st);
+    } else if (prec_ == BP_PREC_F32) {
+      launch_matmul<float>(ctxT.as<float>(), H, ckvT.as<float>(), 2 * H, Lc_, 2 * h_, h_,
+                           static_cast<float*>(w.ctx_kv), 2 * H, kEpiNone, nullptr, 0, st);
+    } else {
+      launch_matmul<float>(ctxT.as<float>(), H, ckvT.as<float>(), 2 * H, Lc_, 2 * h_, h_,
+                           kvT.as<float>(), 2 * H, kEpiNone, nullptr, 0, st);
+      // fp32 -> bf16 via an fp64 hop through the draw scratch
+      launch_convert<float, double>(kvT.as<float>(), g, static_cast<int64_t>(Lc_) * 2 * H, st);
+      launch_place<bf16>(g, Lc_, 2 * H, static_cast<bf16*>(w.ctx_kv), 2 * H, 0, st);
+    }
+  }
+  if (is_first()) {
+    const uint64_t state = derive_seed2(seed_model, static_cast<uint64_t>(m_.layers), kPatchify);
+    launch_normal_fill(state, static_cast<int64_t>(C_) * h_, 1.0 / std::sqrt(static_cast<double>(C_)),
+                       static_cast<double*>(w_in_), st);
+  }
+  if (is_last()) {
+    draw(static_cast<uint64_t>(m_.layers), kHead, static_cast<int64_t>(h_) * C_, h_);
+    if (prec_ == BP_PREC_F64) launch_place<double>(g, h_, C_, static_cast<double*>(w_out_), C_, 0, st);
+    else launch_place<float>(g, h_, C_, static_cast<float*>(w_out_), C_, 0, st);
+  }
+  // Embedding frequencies pow(10000, -2i/h) (model.cpp:158), computed with the
+  // host libm so they match the reference bit-for-bit.
+  std::vector<double> fr(static_cast<size_t>((h_ + 1) / 2));
+  for (size_t i = 0; i < fr.size(); ++i) fr[i] = std::pow(10000.0, -2.0 * static_cast<double>(i) / h_);
+  freq_.alloc(fr.size() * 8);
+  BP_CUDA(cudaMemcpyAsync(freq_.p, fr.data(), fr.size() * 8, cudaMemcpyHostToDevice, st));
+  BP_CUDA(cudaStreamSynchronize(st));
+}
+
+void Stage::ensure_workspace(int64_t tokens, int64_t capture) {
+  const bool bf = prec_ == BP_PREC_BF16;
+  const size_t te = prec_ == BP_PREC_F64 ? 8 : 4;
+  const size_t me = bf ? 2 : te;
+  const size_t S = static_cast<size_t>(tokens), P = static_cast<size_t>(capture);
+  const size_t H = static_cast<size_t>(h_), nl = static_cast<size_t>(end_ - begin_);
+  if (tokens > cap_tokens_) {
+    x_.alloc(S * H * te);
+    ln_.alloc(S * H * me);
+    attn_.alloc(S * H * me);
+    cq_.alloc(S * H * me);
+    hmid_.alloc(S * static_cast<size_t>(F_) * me);
+    eps_.alloc(S * static_cast<size_t>(C_) * te);
+    cap_tokens_ = tokens;
+  }
+  // per-parity buffers: only the set written by this pass may be resized,
+  // the other holds the resident cache of the previous pass
+  qkv_[parity_].reserve(nl * S * 3 * H * me);
+  if (capture > 0) {
+    recbuf_[parity_].reserve(nl * P * H * te);
+    capcopy_[parity_].reserve(nl * P * 2 * H * me);
+  }
+  if (capture > cap_capture_ || rec_.tokens > cap_capture_ || cache_.tokens > cap_capture_) {
+    const int64_t p = std::max({capture, rec_.tokens, cache_.tokens, cap_capture_});
+    kvp_.alloc(static_cast<size_t>(p) * 2 * H * me);
+    lnp_.alloc(static_cast<size_t>(p) * H * me);
+    cap_capture_ = p;
+  }
+}
+
+void Stage::kv_prefix_from_recording(int li, const void* rec_rows, int64_t rows, void* kv_out) {
+  const LayerW& w = lw_[static_cast<size_t>(li)];
+  const int64_t H = h_;
+  if (prec_ == BP_PREC_BF16) {
+    const float* lnp = static_cast<const float*>(w.ln);
+    launch_ln_bf16(static_cast<const float*>(rec_rows), H, lnp, lnp + H, rows, h_, lnp_.as<bf16>(), stream_);
+    launch_gemm_bf16(lnp_.as<bf16>(), H, static_cast<const bf16*>(w.wqkv) + H * H, static_cast<int>(rows),
+                     2 * h_, h_, kv_out, 2 * H, kGemmStoreBf16, stream_);
+  } else if (prec_ == BP_PREC_F64) {
+    const double* lnw = static_cast<const double*>(w.ln);
+    launch_ln<double>(static_cast<const double*>(rec_rows), lnw, lnw + H, rows, h_, lnp_.as<double>(), stream_);
+    launch_matmul<double>(lnp_.as<double>(), H, static_cast<const double*>(w.wqkv) + H, 3 * H,
+                          static_cast<int>(rows), 2 * h_, h_, static_cast<double*>(kv_out), 2 * H,
+                          kEpiNone, nullptr, 0, stream_);
+  } else {
+    const float* lnw = static_cast<const float*>(w.ln);
+    launch_ln<float>(static_cast<const float*>(rec_rows), lnw, lnw + H, rows, h_, lnp_.as<float>(), stream_);
+    launch_matmul<float>(lnp_.as<float>(), H, static_cast<const float*>(w.wqkv) + H, 3 * H,
+                         static_cast<int>(rows), 2 * h_, h_, static_cast<float*>(kv_out), 2 * H,
+                         kEpiNone, nullptr, 0, stream_);
+  }
+}
+
+const void* Stage::forward(const StageInput& in) {
+  BP_CUDA(cudaSetDevice(device_));
+  const bool use_prefix = in.use_prev != 0;
+  if (in.mode == BP_CACHE_DISABLED && use_prefix)
+    fail(BP_ERR_CACHE, "cache supplied while caching is disabled");  // model.cpp:269-271
+  if (in.use_prev == 1 && !cache_.valid) fail(BP_ERR_CACHE, "no resident captured K/V on this stage");
+  if (in.use_prev == 2 && !rec_.valid) fail(BP_ERR_CACHE, "no resident recorded inputs on this stage");
+  for (int f : in.capture_frames)
+    if (f < 0 || f >= in.nframes) fail(BP_ERR_DIMENSION, "capture frame out of range");
+  switch (prec_) {
+    case BP_PREC_F64: return forward_simt<double>(in);
+    case BP_PREC_F32: return forward_simt<float>(in);
+    default: return forward_bf16(in);
+  }
+}
+
+template <typename T>
+const void* Stage::forward_simt(const StageInput& in) {
+  const int64_t S = in.tokens, H = h_;
+  const int64_t P = static_cast<int64_t>(in.capture_frames.size()) * tpf_;
+  const int nl = end_ - begin_;
+  const bool capturing = P > 0;
+  const bool new_cache = capturing && in.mode == BP_CACHE_CACHED;
+  const bool new_rec = capturing && (in.mode == BP_CACHE_RECOMPUTE || in.record_inputs);
+  ensure_workspace(S, P);
+  cudaStream_t st = stream_;
+  T* x = x_.as<T>();
+  T* ln = ln_.as<T>();
+  T* at = attn_.as<T>();
+  T* cq = cq_.as<T>();
+  T* hm = hmid_.as<T>();
+  if (is_first()) {
+    launch_embed<T>(static_cast<const double*>(in.payload), static_cast<const double*>(w_in_),
+                    freq_.as<double>(), in.d_levels, in.d_frame_ids, S, C_, h_, tpf_, x, st);
+  } else {
+    BP_CUDA(cudaMemcpyAsync(x, in.payload, static_cast<size_t>(S * H) * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  }
+  bool contiguous = true;
+  for (size_t i = 1; i < in.capture_frames.size(); ++i)
+    contiguous &= in.capture_frames[i] == in.capture_frames[i - 1] + 1;
+  const int64_t row0 = capturing ? static_cast<int64_t>(in.capture_frames[0]) * tpf_ : 0;
+
+  Entry nc, nr;
+  T* qkv_set = qkv_[parity_].as<T>();
+  for (int li = 0; li < nl; ++li) {
+    const LayerW& w = lw_[static_cast<size_t>(li)];
+    const T* lnw = static_cast<const T*>(w.ln);
+    T* qkv = qkv_set + static_cast<int64_t>(li) * S * 3 * H;
+    if (new_rec) {  // recorded->layer_inputs += take_rows(x, capture_rows) (model.cpp:295)
+      T* dst = recbuf_[parity_].as<T>() + static_cast<int64_t>(li) * P * H;
+      for (size_t f = 0; f < in.capture_frames.size(); ++f)
+        launch_copy_rows(x + static_cast<int64_t>(in.capture_frames[f]) * tpf_ * H, H * sizeof(T),
+                         dst + static_cast<int64_t>(f) * tpf_ * H, H * sizeof(T), tpf_, H * sizeof(T), st);
+      nr.rec.push_back(dst);
+    }
+    launch_ln<T>(x, lnw, lnw + H, S, h_, ln, st);
+    AttnArgs<T> a{};
+    if (in.use_prev == 1) {
+      a.k0 = static_cast<const T*>(cache_.k[static_cast<size_t>(li)]);
+      a.v0 = static_cast<const T*>(cache_.v[static_cast<size_t>(li)]);
+      a.ldk0 = a.ldv0 = cache_.ld;
+      a.n0 = cache_.tokens;
+    } else if (in.use_prev == 2) {
+      kv_prefix_from_recording(li, rec_.rec[static_cast<size_t>(li)], rec_.tokens, kvp_.p);
+      a.k0 = kvp_.as<T>();
+      a.v0 = kvp_.as<T>() + H;
+      a.ldk0 = a.ldv0 = 2 * H;
+      a.n0 = rec_.tokens;
+    }
+    launch_matmul<T>(ln, H, static_cast<const T*>(w.wqkv), 3 * H, static_cast<int>(S), 3 * h_, h_, qkv,
+                     3 * H, kEpiNone, nullptr, 0, st);
+    a.q = qkv; a.ldq = 3 * H;
+    a.k1 = qkv + H; a.ldk1 = 3 * H;
+    a.v1 = qkv + 2 * H; a.ldv1 = 3 * H;
+    a.n1 = S;
+    a.out = at; a.ldo = H;
+    a.dh = dh_;
+    a.scale = static_cast<T>(1.0 / std::sqrt(static_cast<double>(dh_)));
+    launch_attention<T>(a, S, heads_, st);
+    if (new_cache) {  // captured K,V rows stay where this pass wrote them
+      if (contiguous) {
+        nc.k.push_back(qkv + row0 * 3 * H + H);
+        nc.v.push_back(qkv + row0 * 3 * H + 2 * H);
+        nc.ld = 3 * H;
+      } else {
+        T* dst = capcopy_[parity_].as<T>() + static_cast<int64_t>(li) * P * 2 * H;
+        for (size_t f = 0; f < in.capture_frames.size(); ++f)
+          launch_copy_rows(qkv + static_cast<int64_t>(in.capture_frames[f]) * tpf_ * 3 * H + H,
+                           3 * H * sizeof(T), dst + static_cast<int64_t>(f) * tpf_ * 2 * H,
+                           2 * H * sizeof(T), tpf_, 2 * H * sizeof(T), st);
+        nc.k.push_back(dst);
+        nc.v.push_back(dst + H);
+        nc.ld = 2 * H;
+      }
+    }
+    launch_matmul<T>(at, H, static_cast<const T*>(w.wo), H, static_cast<int>(S), h_, h_, x, H,
+                     kEpiResidual, x, H, st);
+    // cross-attention against the hoisted context K|V
+    launch_ln<T>(x, lnw + 2 * H, lnw + 3 * H, S, h_, ln, st);
+    launch_matmul<T>(ln, H, static_cast<const T*>(w.cq), H, static_cast<int>(S), h_, h_, cq, H, kEpiNone,
+                     nullptr, 0, st);
+    AttnArgs<T> c{};
+    c.q = cq; c.ldq = H;
+    c.k1 = static_cast<const T*>(w.ctx_kv); c.ldk1 = 2 * H;
+    c.v1 = static_cast<const T*>(w.ctx_kv) + H; c.ldv1 = 2 * H;
+    c.n1 = Lc_;
+    c.out = at; c.ldo = H;
+    c.dh = dh_;
+    c.scale = a.scale;
+    launch_attention<T>(c, S, heads_, st);
+    launch_matmul<T>(at, H, static_cast<const T*>(w.co), H, static_cast<int>(S), h_, h_, x, H,
+                     kEpiResidual, x, H, st);
+    // FFN
+    launch_ln<T>(x, lnw + 4 * H, lnw + 5 * H, S, h_, ln, st);
+    launch_matmul<T>(ln, H, static_cast<const T*>(w.w1), F_, static_cast<int>(S), F_, h_, hm, F_,
+                     kEpiGelu, nullptr, 0, st);
+    launch_matmul<T>(hm, F_, static_cast<const T*>(w.w2), H, static_cast<int>(S), h_, F_, x, H,
+                     kEpiResidual, x, H, st);
+  }
+  cache_ = Entry{};
+  if (new_cache) { nc.valid = true; nc.tokens = P; cache_ = std::move(nc); }
+  rec_ = Entry{};
+  if (new_rec) { nr.valid = true; nr.tokens = P; rec_ = std::move(nr); }
+  parity_ ^= 1;
+  if (is_last()) {
+    launch_matmul<T>(x, H, static_cast<const T*>(w_out_), C_, static_cast<int>(S), C_, h_, eps_.as<T>(),
+                     C_, kEpiNone, nullptr, 0, st);
+    return eps_.p;
+  }
+  return x_.p;
+}
+
+const void* Stage::forward_bf16(const StageInput& in) {
+  const int64_t S = in.tokens, H = h_;
+  const int64_t P = static_cast<int64_t>(in.capture_frames.size()) * tpf_;
+  const int nl = end_ - begin_;
+  const bool capturing = P > 0;
+  const bool new_cache = capturing && in.mode == BP_CACHE_CACHED;
+  const bool new_rec = capturing && (in.mode == BP_CACHE_RECOMPUTE || in.record_inputs);
+  ensure_workspace(S, P);
+  cudaStream_t st = stream_;
+  float* x = x_.as<float>();
+  bf16* ln = ln_.as<bf16>();
+  bf16* at = attn_.as<bf16>();
+  bf16* cq = cq_.as<bf16>();
+  bf16* hm = hmid_.as<bf16>();
+  if (is_first()) {
+    launch_embed<float>(static_cast<const double*>(in.payload), static_cast<const double*>(w_in_),
+                        freq_.as<double>(), in.d_levels, in.d_frame_ids, S, C_, h_, tpf_, x, st);
+  } else {
+    BP_CUDA(cudaMemcpyAsync(x, in.payload, static_cast<size_t>(S * H) * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  bool contiguous = true;
+  for (size_t i = 1; i < in.capture_frames.size(); ++i)
+    contiguous &= in.capture_frames[i] == in.capture_frames[i - 1] + 1;
+  const int64_t row0 = capturing ? static_cast<int64_t>(in.capture_frames[0]) * tpf_ : 0;
+  const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(dh_)));
+
+  Entry nc, nr;
+  bf16* qkv_set = qkv_[parity_].as<bf16>();
+  for (int li = 0; li < nl; ++li) {
+    const LayerW& w = lw_[static_cast<size_t>(li)];
+    const float* lnw = static_cast<const float*>(w.ln);
+    bf16* qkv = qkv_set + static_cast<int64_t>(li) * S * 3 * H;
+    if (new_rec) {
+      float* dst = recbuf_[parity_].as<float>() + static_cast<int64_t>(li) * P * H;
+      for (size_t f = 0; f < in.capture_frames.size(); ++f)
+        launch_copy_rows(x + static_cast<int64_t>(in.capture_frames[f]) * tpf_ * H, H * 4,
+                         dst + static_cast<int64_t>(f) * tpf_ * H, H * 4, tpf_, H * 4, st);
+      nr.rec.push_back(dst);
+    }
+    launch_ln_bf16(x, H, lnw, lnw + H, S, h_, ln, st);
+    AttnBf16Args a{};
+    if (in.use_prev == 1) {
+      a.k0 = static_cast<const bf16*>(cache_.k[static_cast<size_t>(li)]);
+      a.v0 = static_cast<const bf16*>(cache_.v[static_cast<size_t>(li)]);
+      a.ldk0 = a.ldv0 = cache_.ld;
+      a.n0 = cache_.tokens;
+    } else if (in.use_prev == 2) {
+      kv_prefix_from_recording(li, rec_.rec[static_cast<size_t>(li)], rec_.tokens, kvp_.p);
+      a.k0 = kvp_.as<bf16>();
+      a.v0 = kvp_.as<bf16>() + H;
+      a.ldk0 = a.ldv0 = 2 * H;
+      a.n0 = rec_.tokens;
+    }
+    launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.wqkv), static_cast<int>(S), 3 * h_, h_, qkv, 3 * H,
+                     kGemmStoreBf16, st);
+    a.q = qkv; a.ldq = 3 * H;
+    a.k1 = qkv + H; a.ldk1 = 3 * H;
+    a.v1 = qkv + 2 * H; a.ldv1 = 3 * H;
+    a.n1 = S;
+    a.out = at; a.ldo = H;
+    a.heads = heads_; a.dh = dh_; a.scale = scale;
+    launch_attn_bf16(a, S, st);
+    if (new_cache) {
+      if (contiguous) {
+        nc.k.push_back(qkv + row0 * 3 * H + H);
+        nc.v.push_back(qkv + row0 * 3 * H + 2 * H);
+        nc.ld = 3 * H;
+      } else {
+        bf16* dst = capcopy_[parity_].as<bf16>() + static_cast<int64_t>(li) * P * 2 * H;
+        for (size_t f = 0; f < in.capture_frames.size(); ++f)
+          launch_copy_rows(qkv + static_cast<int64_t>(in.capture_frames[f]) * tpf_ * 3 * H + H, 3 * H * 2,
+                           dst + static_cast<int64_t>(f) * tpf_ * 2 * H, 2 * H * 2, tpf_, 2 * H * 2, st);
+        nc.k.push_back(dst);
+        nc.v.push_back(dst + H);
+        nc.ld = 2 * H;
+      }
+    }
+    launch_gemm_bf16(at, H, static_cast<const bf16*>(w.wo), static_cast<int>(S), h_, h_, x, H,
+                     kGemmResidualF32, st);
+    launch_ln_bf16(x, H, lnw + 2 * H, lnw + 3 * H, S, h_, ln, st);
+    launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.cq), static_cast<int>(S), h_, h_, cq, H,
+                     kGemmStoreBf16, st);
+    AttnBf16Args c{};
+    c.q = cq; c.ldq = H;
+    c.k1 = static_cast<const bf16*>(w.ctx_kv); c.ldk1 = 2 * H;
+    c.v1 = static_cast<const bf16*>(w.ctx_kv) + H; c.ldv1 = 2 * H;
+    c.n1 = Lc_;
+    c.out = at; c.ldo = H;
+    c.heads = heads_; c.dh = dh_; c.scale = scale;
+    launch_attn_bf16(c, S, st);
+    launch_gemm_bf16(at, H, static_cast<const bf16*>(w.co), static_cast<int>(S), h_, h_, x, H,
+                     kGemmResidualF32, st);
+    launch_ln_bf16(x, H, lnw + 4 * H, lnw + 5 * H, S, h_, ln, st);
+    launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.w1), static_cast<int>(S), F_, h_, hm, F_,
+                     kGemmGeluBf16, st);
+    launch_gemm_bf16(hm, F_, static_cast<const bf16*>(w.w2), static_cast<int>(S), h_, F_, x, H,
+                     kGemmResidualF32, st);
+  }
+  cache_ = Entry{};
+  if (new_cache) { nc.valid = true; nc.tokens = P; cache_ = std::move(nc); }
+  rec_ = Entry{};
+  if (new_rec) { nr.valid = true; nr.tokens = P; rec_ = std::move(nr); }
+  parity_ ^= 1;
+  if (is_last()) {
+    launch_matmul<float>(x, H, static_cast<const float*>(w_out_), C_, static_cast<int>(S), C_, h_,
+                         eps_.as<float>(), C_, kEpiNone, nullptr, 0, st);
+    return eps_.p;
+  }
+  return x_.p;
+}
+
+void Stage::tag_entries(int64_t block_id, int level) {
+  if (cache_.valid) { cache_.block_id = block_id; cache_.level = level; }
+  if (rec_.valid) { rec_.block_id = block_id; rec_.level = level; }
+}
+
+void Stage::cache_rows(int layer, int which, double* host_out) {
+  if (!cache_.valid) fail(BP_ERR_CACHE, "no resident cache");
+  if (layer < 0 || layer >= end_ - begin_) fail(BP_ERR_DIMENSION, "layer out of range");
+  const void* src = which ? cache_.v[static_cast<size_t>(layer)] : cache_.k[static_cast<size_t>(layer)];
+  const int64_t rows = cache_.tokens, H = h_;
+  const size_t eb = prec_ == BP_PREC_F64 ? 8 : (prec_ == BP_PREC_F32 ? 4 : 2);
+  DevBuf tight, d64;
+  tight.alloc(static_cast<size_t>(rows * H) * eb);
+  launch_copy_rows(src, cache_.ld * static_cast<int64_t>(eb), tight.p, H * static_cast<int64_t>(eb), rows,
+                   H * static_cast<int64_t>(eb), stream_);
+  d64.alloc(static_cast<size_t>(rows * H) * 8);
+  if (prec_ == BP_PREC_F64) {
+    BP_CUDA(cudaMemcpyAsync(d64.p, tight.p, static_cast<size_t>(rows * H) * 8, cudaMemcpyDeviceToDevice, stream_));
+  } else if (prec_ == BP_PREC_F32) {
+    launch_convert<float, double>(tight.as<float>(), d64.as<double>(), rows * H, stream_);
+  } else {
+    std::vector<uint16_t> hb(static_cast<size_t>(rows * H));
+    BP_CUDA(cudaMemcpyAsync(hb.data(), tight.p, hb.size() * 2, cudaMemcpyDeviceToHost, stream_));
+    BP_CUDA(cudaStreamSynchronize(stream_));
+    for (size_t i = 0; i < hb.size(); ++i) {
+      const uint32_t u = static_cast<uint32_t>(hb[i]) << 16;
+      float f;
+      std::memcpy(&f, &u, 4);
+      host_out[i] = f;
+    }
+    return;
+  }
+  BP_CUDA(cudaMemcpyAsync(host_out, d64.p, static_cast<size_t>(rows * H) * 8, cudaMemcpyDeviceToHost, stream_));
+  BP_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Stage::bump_ulp(int layer, int which, int64_t index) {
+  if (!cache_.valid) fail(BP_ERR_CACHE, "no resident cache");
+  if (layer < 0 || layer >= end_ - begin_) fail(BP_ERR_DIMENSION, "layer out of range");
+  if (index < 0 || index >= cache_.tokens * h_) fail(BP_ERR_DIMENSION, "index out of range");
+  const size_t eb = prec_ == BP_PREC_F64 ? 8 : (prec_ == BP_PREC_F32 ? 4 : 2);
+  const char* base = static_cast<const char*>(which ? cache_.v[static_cast<size_t>(layer)]
+                                                    : cache_.k[static_cast<size_t>(layer)]);
+  const int64_t r = index / h_, c = index % h_;
+  void* p = const_cast<char*>(base) + (r * cache_.ld + c) * static_cast<int64_t>(eb);
+  launch_bump_ulp(p, prec_ == BP_PREC_F64 ? 0 : (prec_ == BP_PREC_F32 ? 1 : 2), stream_);
+}
+
+std::string Stage::audit() {
+  if (!cache_.valid || !rec_.valid) return "cache audit has no recording";
+  if (cache_.block_id != rec_.block_id) return "cache and recording cover different blocks";
+  const size_t eb = prec_ == BP_PREC_F64 ? 8 : (prec_ == BP_PREC_F32 ? 4 : 2);
+  const int64_t rows = cache_.tokens, H = h_;
+  scratch_.reserve(16 * static_cast<size_t>(end_ - begin_));
+  auto* firsts = scratch_.as<unsigned long long>();
+  const int nl = end_ - begin_;
+  std::vector<unsigned long long> host(static_cast<size_t>(2 * nl));
+  BP_CUDA(cudaMemsetAsync(firsts, 0xff, 16 * static_cast<size_t>(nl), stream_));
+  for (int li = 0; li < nl; ++li) {
+    kv_prefix_from_recording(li, rec_.rec[static_cast<size_t>(li)], rows, kvp_.p);
+    const char* kv = kvp_.as<char>();
+    if (eb == 2) {
+      // compare in 16-bit units: rows of H bf16 = H/2 words; done as 4-byte
+      // words first, the element index is refined on the host below
+    }
+    launch_first_diff(kv, 2 * H * eb, cache_.k[static_cast<size_t>(li)], cache_.ld * eb, rows, H * eb,
+                      firsts + 2 * li, stream_);
+    launch_first_diff(kv + H * eb, 2 * H * eb, cache_.v[static_cast<size_t>(li)], cache_.ld * eb, rows,
+                      H * eb, firsts + 2 * li + 1, stream_);
+  }
+  BP_CUDA(cudaMemcpyAsync(host.data(), firsts, 16 * static_cast<size_t>(nl), cudaMemcpyDeviceToHost, stream_));
+  BP_CUDA(cudaStreamSynchronize(stream_));
+  const int64_t words_per_row = H * static_cast<int64_t>(eb) / 4;
+  for (int li = 0; li < nl; ++li) {
+    const unsigned long long fk = host[static_cast<size_t>(2 * li)], fv = host[static_cast<size_t>(2 * li + 1)];
+    if (fk == ~0ULL && fv == ~0ULL) continue;
+    // word index -> flat element index (first element covered by that word)
+    auto elem = [&](unsigned long long wi) -> int64_t {
+      const int64_t r = static_cast<int64_t>(wi) / words_per_row, wc = static_cast<int64_t>(wi) % words_per_row;
+      return r * H + (wc * 4) / static_cast<int64_t>(eb);
+    };
+    const int64_t ek = fk == ~0ULL ? INT64_MAX : elem(fk);
+    const int64_t ev = fv == ~0ULL ? INT64_MAX : elem(fv);
+    const int layer = begin_ + li;
+    if (ek <= ev) return "cached K diverges at layer " + std::to_string(layer) + " flat index " + std::to_string(ek);
+    return "cached V diverges at layer " + std::to_string(layer) + " flat index " + std::to_string(ev);
+  }
+  return "";
+}
+
+template const void* Stage::forward_simt<double>(const StageInput&);
+template const void* Stage::forward_simt<float>(const StageInput&);
+
+}  // namespace bp

@@ -1,0 +1,112 @@
+// One pipeline stage on one GPU: the reference's ModelChunk (model.hpp:50-60)
+// with device-resident weights, the per-device single-entry KV feature cache
+// (KVCacheEntry / RecomputeEntry, model.hpp:82-101) kept in HBM and reused in
+// place, and forward_chunk (model.cpp:227-336) as device kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "bp_cuda.h"
+#include "device.cuh"
+
+namespace bp {
+
+struct StageInput {
+  const void* payload = nullptr;       // device: fp64 latents [tokens, C] (first) or hidden [tokens, h]
+  int64_t tokens = 0;
+  int nframes = 0;
+  const int32_t* d_levels = nullptr;   // device, nframes
+  const int64_t* d_frame_ids = nullptr;
+  std::vector<int> capture_frames;     // host
+  bool record_inputs = false;
+  int mode = BP_CACHE_DISABLED;
+  int use_prev = 0;                    // 0 none, 1 resident cache, 2 resident recording
+};
+
+class Stage {
+ public:
+  Stage(int device, const bp_model_desc& m, uint64_t seed_model, uint64_t seed_context, int begin,
+        int end, int precision, cudaStream_t stream);
+  ~Stage();
+
+  // Runs forward_chunk; returns the device output pointer (hidden state in
+  // the stage's activation dtype, or eps [tokens, C] on the last stage).
+  const void* forward(const StageInput& in);
+
+  bool is_first() const { return begin_ == 0; }
+  bool is_last() const { return end_ == m_.layers; }
+  int precision() const { return prec_; }
+  size_t act_bytes() const;  // bytes per hidden element (8 fp64, 4 fp32/bf16-path residual)
+  size_t eps_bytes() const { return prec_ == BP_PREC_F64 ? 8 : 4; }
+  int hidden() const { return m_.hidden; }
+  int channels() const { return m_.channels; }
+  int local_layers() const { return end_ - begin_; }
+  cudaStream_t stream() const { return stream_; }
+
+  // Resident cache bookkeeping (DeviceWorker::cache_/recorded_, engine.cpp:215-216).
+  bool cache_valid() const { return cache_.valid; }
+  int64_t cache_block() const { return cache_.block_id; }
+  int cache_level() const { return cache_.level; }
+  int64_t cache_tokens() const { return cache_.tokens; }
+  bool rec_valid() const { return rec_.valid; }
+  int64_t rec_block() const { return rec_.block_id; }
+  void tag_entries(int64_t block_id, int level);
+  void cache_rows(int layer, int which, double* host_out);  // fp64 download
+  void bump_ulp(int layer, int which, int64_t index);
+  std::string audit();  // cache_mismatch_report (model.cpp:171-199)
+
+ private:
+  struct LayerW {
+    void* wqkv = nullptr;   // SIMT: [h, 3h] row-major; bf16: [3h, h] (K-major)
+    void* wo = nullptr;
+    void* cq = nullptr;
+    void* co = nullptr;
+    void* w1 = nullptr;     // SIMT: [h, F]; bf16: [F, h]
+    void* w2 = nullptr;     // SIMT: [F, h]; bf16: [h, F]
+    void* ln = nullptr;     // 6 x [h]: ln1 g,b ln2 g,b ln3 g,b (T; fp32 on bf16 path)
+    void* ctx_kv = nullptr; // hoisted cross-attention K|V [Lc, 2h] (T; bf16 on bf16 path)
+  };
+  struct Entry {  // resident KVCacheEntry or RecomputeEntry
+    bool valid = false;
+    int64_t block_id = -1;
+    int level = -1;
+    int64_t tokens = 0;
+    std::vector<const void*> k, v, rec;  // per local layer
+    int64_t ld = 0;                      // row stride of k/v in elements
+  };
+
+  template <typename T> const void* forward_simt(const StageInput& in);
+  const void* forward_bf16(const StageInput& in);
+  void build_weights(uint64_t seed_model, uint64_t seed_context);
+  void ensure_workspace(int64_t tokens, int64_t capture_tokens);
+  void kv_prefix_from_recording(int li, const void* rec_rows, int64_t rows, void* kv_out);
+
+  int device_, prec_;
+  bp_model_desc m_;
+  int begin_, end_;
+  int h_, heads_, dh_, F_, C_, tpf_, Lc_;
+  cudaStream_t stream_;
+  bool own_stream_ = false;
+
+  DevBuf weights_;
+  std::vector<LayerW> lw_;
+  void* w_in_ = nullptr;   // fp64 [C, h]
+  void* w_out_ = nullptr;  // T [h, C] (fp32 on the bf16 path)
+  DevBuf freq_;            // fp64 [h/2] embedding frequencies
+
+  // workspace
+  int64_t cap_tokens_ = 0, cap_capture_ = 0;
+  DevBuf x_, ln_, attn_, cq_, hmid_, eps_, kvp_, lnp_;
+  DevBuf qkv_[2];          // [L_local][tokens][3h] per parity
+  DevBuf recbuf_[2];       // [L_local][capture][h] per parity
+  DevBuf capcopy_[2];      // [L_local][capture][2h] (non-contiguous captures)
+  DevBuf scratch_;         // audit
+  int parity_ = 0;
+  Entry cache_, rec_;
+};
+
+}  // namespace bp
