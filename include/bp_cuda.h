@@ -193,8 +193,9 @@ bp_status bp_pipeline_destroy(bp_pipeline* p);
 typedef void (*bp_emit_fn)(void* user, int64_t block_id, int64_t frames, const double* data,
                            const int32_t* noise_ids, int32_t nids, const int64_t* frame_ids);
 
-/* run_pipeline (engine.cpp:255-497): one whole generation. emit may be NULL
- * (latents stay on the device; bp_pipeline_block can fetch them). */
+/* run_pipeline (engine.cpp:255-497): one whole generation. emit may be NULL:
+ * the emitted latents then stay on the device (no device->host copies;
+ * bp_pipeline_block returns their device pointers). */
 bp_status bp_pipeline_run(bp_pipeline* p, bp_emit_fn emit, void* user);
 
 typedef struct {
@@ -204,6 +205,8 @@ typedef struct {
   int64_t peak_bytes;       /* device memory high-water mark of this pipeline */
   int64_t boundary_bytes;   /* bytes moved across stage boundaries */
   double attn_ms, gemm_ms;  /* per-class device time when profiling is enabled */
+  double cross_ms;          /* cross-attention device time (profiling)             */
+  int64_t attn_launches, gemm_launches, cross_launches;
 } bp_pipeline_stats;
 bp_status bp_pipeline_get_stats(bp_pipeline* p, bp_pipeline_stats* out);
 /* Per-kernel-class timing with CUDA events on the launching stream (0/1). */

@@ -269,6 +269,11 @@ class Pipeline:
         check(lib.bp_pipeline_run(self._h, cb, None))
         return blocks
 
+    def run_device(self) -> None:
+        """One whole generation with the emitted latents left in HBM (no
+        device->host copies); bp_pipeline_block exposes their device pointers."""
+        check(lib.bp_pipeline_run(self._h, C.cast(None, EMIT_FN), None))
+
     def stats(self) -> Dict[str, Any]:
         s = PipelineStats()
         check(lib.bp_pipeline_get_stats(self._h, C.byref(s)))

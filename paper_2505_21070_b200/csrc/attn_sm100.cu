@@ -1,6 +1,332 @@
-// tcgen05 attention (placeholder until implemented).
+// tcgen05 flash attention over two KV segments (K6/K7): every query tile of
+// 128 rows of one head attends to [cached prefix (previous pass on this GPU,
+// resident in HBM) ++ current block] without concatenating them in memory
+// (model.cpp:201-211, 302-318: vcat_rows(prefix, k) then attention()).
+//
+//   warp 0      TMA producer: Q once, then K/V tiles of 128 keys into a 2-stage ring
+//   warp 1      MMA issuer: S_j = Q K_j^T (TMEM, double-buffered), O += P_{j-1} V_{j-1}
+//   warps 2..5  softmax: one thread per query row reads S from TMEM, online
+//               softmax in the log2 domain, P (bf16) -> swizzled smem; lazy
+//               rescaling of O in TMEM only when the row max grows by > 2^8;
+//               epilogue O / l -> bf16 -> global
+// Keys past a segment's end (a tile that straddles it) are masked; TMA
+// zero-fills the rows.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <unordered_map>
+
 #include "device.cuh"
 #include "kernels_bf16.cuh"
+#include "tc_common.cuh"
+
 namespace bp {
-void launch_attn_tc(const AttnBf16Args&, int64_t, cudaStream_t) { fail(BP_ERR_INTERNAL, "tcgen05 attention not built"); }
+
+void launch_attn_simt(const AttnBf16Args& a, int64_t rows, cudaStream_t st);
+
+namespace {
+
+constexpr int kDh = 128, BQ = 128, BKV = 128;
+constexpr uint32_t HALF = 128 * 64 * 2;      // [128 rows][64 bf16] swizzled box
+constexpr uint32_t TILE = 2 * HALF;          // 32 KB
+constexpr uint32_t SMEM_Q = 0;
+constexpr uint32_t SMEM_K = SMEM_Q + TILE;           // 2 stages
+constexpr uint32_t SMEM_V = SMEM_K + 2 * TILE;       // 2 stages
+constexpr uint32_t SMEM_P = SMEM_V + 2 * TILE;
+constexpr uint32_t SMEM_BAR = SMEM_P + TILE;
+constexpr uint32_t SMEM_BYTES = SMEM_BAR + 256 + 1024;
+constexpr int kThreads = 192;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: P values up to 2^8 before O is rescaled
+
+struct AttnMaps {
+  CUtensorMap q, k0, v0, k1, v1;
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_attn_tc(const __grid_constant__ AttnMaps maps, int64_t rows, int64_t n0, int64_t n1, float scale_log2,
+              bf16* __restrict__ out, int64_t ldo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;    // [2]
+  uint64_t* kv_empty = bars + 3;   // [2]
+  uint64_t* s_full = bars + 5;     // [2]
+  uint64_t* s_free = bars + 7;     // [2]
+  uint64_t* p_full = bars + 9;
+  uint64_t* pv_done = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qtile = blockIdx.x, head = blockIdx.y;
+  const int t0 = static_cast<int>((n0 + BKV - 1) / BKV);
+  const int t1 = static_cast<int>((n1 + BKV - 1) / BKV);
+  const int T = t0 + t1;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&maps.q);
+    tc::tma_prefetch(&maps.k1);
+    tc::tma_prefetch(&maps.v1);
+    tc::mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&kv_full[s], 1);
+      tc::mbar_init(&kv_empty[s], 1);
+      tc::mbar_init(&s_full[s], 1);
+      tc::mbar_init(&s_free[s], 128);
+    }
+    tc::mbar_init(p_full, 128);
+    tc::mbar_init(pv_done, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_o = tmem + 256;
+
+  if (warp == 0) {
+    // ---- TMA producer -----------------------------------------------------------------
+    if (lane == 0) {
+      tc::mbar_arrive_expect_tx(q_full, TILE);
+      tc::tma_load_2d(smem + SMEM_Q, &maps.q, q_full, head * kDh, qtile * BQ);
+      tc::tma_load_2d(smem + SMEM_Q + HALF, &maps.q, q_full, head * kDh + 64, qtile * BQ);
+    }
+    for (int j = 0; j < T; ++j) {
+      const int s = j & 1;
+      tc::mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+      if (lane == 0) {
+        const bool seg0 = j < t0;
+        const CUtensorMap* mk = seg0 ? &maps.k0 : &maps.k1;
+        const CUtensorMap* mv = seg0 ? &maps.v0 : &maps.v1;
+        const int row0 = (seg0 ? j : j - t0) * BKV;
+        tc::mbar_arrive_expect_tx(&kv_full[s], 2 * TILE);
+        uint8_t* kd = smem + SMEM_K + s * TILE;
+        uint8_t* vd = smem + SMEM_V + s * TILE;
+        tc::tma_load_2d(kd, mk, &kv_full[s], head * kDh, row0);
+        tc::tma_load_2d(kd + HALF, mk, &kv_full[s], head * kDh + 64, row0);
+        tc::tma_load_2d(vd, mv, &kv_full[s], head * kDh, row0);
+        tc::tma_load_2d(vd + HALF, mv, &kv_full[s], head * kDh + 64, row0);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer -------------------------------------------------------------------
+    constexpr uint32_t idesc_s = tc::idesc_bf16(BQ, BKV, 0, 0);   // Q (K-major) x K^T (K-major)
+    constexpr uint32_t idesc_o = tc::idesc_bf16(BQ, kDh, 0, 1);   // P (K-major) x V (MN-major)
+    const uint32_t q_addr = tc::smem_u32(smem + SMEM_Q);
+    const uint32_t p_addr = tc::smem_u32(smem + SMEM_P);
+    tc::mbar_wait(q_full, 0);
+    auto issue_pv = [&](int jj) {
+      tc::mbar_wait(p_full, jj & 1);
+      tc::fence_after_sync();
+      if (lane == 0) {
+        const uint32_t v_addr = tc::smem_u32(smem + SMEM_V + (jj & 1) * TILE);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint64_t ad = tc::desc_sw128(p_addr + (kk >> 2) * HALF + (kk & 3) * 32, 1024, 16);
+          // V tile [keys][d]: MN-major (d contiguous); 16 keys = two 8-row groups
+          const uint64_t bd = tc::desc_sw128(v_addr + kk * 2048, 1024, HALF);
+          tc::mma_bf16(tmem_o, ad, bd, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit(pv_done);
+        tc::mma_commit(&kv_empty[jj & 1]);
+      }
+      __syncwarp();
+    };
+    for (int j = 0; j < T; ++j) {
+      const int s = j & 1;
+      tc::mbar_wait(&kv_full[s], (j >> 1) & 1);
+      tc::mbar_wait(&s_free[s], ((j >> 1) & 1) ^ 1);
+      tc::fence_after_sync();
+      if (lane == 0) {
+        const uint32_t k_addr = tc::smem_u32(smem + SMEM_K + s * TILE);
+        const uint32_t d = tmem + static_cast<uint32_t>(s * BKV);
+#pragma unroll
+        for (int kk = 0; kk < kDh / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
+          tc::mma_bf16(d, tc::desc_sw128(q_addr + off, 1024, 16), tc::desc_sw128(k_addr + off, 1024, 16),
+                       idesc_s, kk > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(&s_full[s]);
+      }
+      __syncwarp();
+      if (j >= 1) issue_pv(j - 1);
+    }
+    if (T >= 1) issue_pv(T - 1);
+  } else {
+    // ---- softmax + epilogue: thread <-> query row ------------------------------------------
+    const int qq = warp & 3;
+    const int r = qq * 32 + lane;  // row within the tile (= TMEM lane)
+    const uint32_t lane_off = static_cast<uint32_t>(qq * 32) << 16;
+    uint8_t* p_smem = smem + SMEM_P;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < T; ++j) {
+      const int s = j & 1;
+      const bool seg0 = j < t0;
+      const int64_t seg_n = seg0 ? n0 : n1;
+      const int row0 = (seg0 ? j : j - t0) * BKV;
+      const int valid = static_cast<int>(seg_n - row0 < BKV ? seg_n - row0 : BKV);
+      tc::mbar_wait(&s_full[s], (j >> 1) & 1);
+      tc::fence_after_sync();
+      uint32_t sr[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        tc::tmem_ld32(tmem + lane_off + static_cast<uint32_t>(s * BKV + c * 32),
+                      *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+      tc::tmem_ld_wait();
+      tc::fence_before_sync();
+      tc::mbar_arrive(&s_free[s]);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        const float v = c < valid ? __uint_as_float(sr[c]) * scale_log2 : -INFINITY;
+        sr[c] = __float_as_uint(v);
+        mx = fmaxf(mx, v);
+      }
+      const bool need = mx > m_used + kRescaleThreshold;
+      const float m_new = need ? mx : m_used;
+      const float corr = need ? ex2(m_used - m_new) : 1.f;  // 0 on the first tile
+      uint32_t pk[64];
+      float ls = 0.f;
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        const float p0 = ex2(__uint_as_float(sr[2 * c]) - m_new);
+        const float p1 = ex2(__uint_as_float(sr[2 * c + 1]) - m_new);
+        ls += p0 + p1;
+        pk[c] = pack_bf16(p0, p1);
+      }
+      l = l * corr + ls;
+      m_used = m_new;
+      // P buffer and O are free once PV_{j-1} completed
+      if (j >= 1) {
+        tc::mbar_wait(pv_done, (j - 1) & 1);
+        tc::fence_after_sync();
+        if (__any_sync(0xffffffffu, need)) {
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            const uint32_t ta = tmem_o + lane_off + static_cast<uint32_t>(c * 32);
+            tc::tmem_ld32(ta, o);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+            tc::tmem_st32(ta, o);
+          }
+          tc::tmem_st_wait();
+        }
+      }
+      // P row -> smem, K-major SW128: 16-byte chunk c of row r at (c ^ (r & 7))
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const int half = c >> 3, ch = c & 7;
+        uint4* dst = reinterpret_cast<uint4*>(p_smem + half * HALF + r * 128 + ((ch ^ (r & 7)) << 4));
+        *dst = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc::fence_before_sync();
+      tc::mbar_arrive(p_full);
+    }
+    // epilogue: O / l
+    if (T >= 1) {
+      tc::mbar_wait(pv_done, (T - 1) & 1);
+      tc::fence_after_sync();
+    }
+    const int64_t row = static_cast<int64_t>(qtile) * BQ + r;
+    const float inv_l = 1.f / l;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      tc::tmem_ld32(tmem_o + lane_off + static_cast<uint32_t>(c * 32), o);
+      tc::tmem_ld_wait();
+      if (row < rows) {
+        uint4* dst = reinterpret_cast<uint4*>(out + row * ldo + head * kDh + c * 32);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          dst[v] = make_uint4(pack_bf16(__uint_as_float(o[8 * v]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l),
+                              pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l),
+                              pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l),
+                              pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l));
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<512>(tmem);
+  }
+}
+
+std::mutex g_mu;
+struct Key {
+  const void* p; int64_t rows, cols, ld;
+  bool operator==(const Key& o) const { return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld; }
+};
+struct KeyHash {
+  size_t operator()(const Key& k) const {
+    return (reinterpret_cast<size_t>(k.p) * 1000003u) ^ (static_cast<size_t>(k.rows) * 7919u) ^
+           (static_cast<size_t>(k.cols) << 20) ^ static_cast<size_t>(k.ld);
+  }
+};
+std::unordered_map<Key, CUtensorMap, KeyHash> g_maps;
+
+CUtensorMap map_for(const bf16* p, int64_t rows, int64_t cols, int64_t ld) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  const Key k{p, rows, cols, ld};
+  auto it = g_maps.find(k);
+  if (it != g_maps.end()) return it->second;
+  if (g_maps.size() > 4096) g_maps.clear();
+  CUtensorMap m;
+  make_tmap_2d_bf16(&m, p, static_cast<uint64_t>(rows < 1 ? 1 : rows), static_cast<uint64_t>(cols),
+                    static_cast<uint64_t>(ld), 128, 64);
+  g_maps.emplace(k, m);
+  return m;
+}
+
+}  // namespace
+
+void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st) {
+  const int64_t H = static_cast<int64_t>(a.heads) * a.dh;
+  const bool aligned = ((a.ldq | a.ldk1 | a.ldv1 | a.ldo) * 2) % 16 == 0 &&
+                       (a.n0 == 0 || ((a.ldk0 | a.ldv0) * 2) % 16 == 0);
+  if (a.dh != kDh || !aligned || a.n0 + a.n1 == 0) {  // other head dims: SIMT kernel
+    launch_attn_simt(a, rows, st);
+    return;
+  }
+  static bool configured = false;
+  if (!configured) {
+    BP_CUDA(cudaFuncSetAttribute(k_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    configured = true;
+  }
+  AttnMaps maps;
+  maps.q = map_for(a.q, rows, H, a.ldq);
+  maps.k1 = map_for(a.k1, a.n1, H, a.ldk1);
+  maps.v1 = map_for(a.v1, a.n1, H, a.ldv1);
+  if (a.n0 > 0) {
+    maps.k0 = map_for(a.k0, a.n0, H, a.ldk0);
+    maps.v0 = map_for(a.v0, a.n0, H, a.ldv0);
+  } else {
+    maps.k0 = maps.k1;
+    maps.v0 = maps.v1;
+  }
+  dim3 grid(static_cast<unsigned>((rows + BQ - 1) / BQ), static_cast<unsigned>(a.heads));
+  k_attn_tc<<<grid, kThreads, SMEM_BYTES, st>>>(maps, rows, a.n0, a.n1, a.scale * 1.4426950408889634f, a.out, a.ldo);
+  count_launch();
+}
+
 }  // namespace bp

@@ -1,8 +1,268 @@
-// tcgen05 GEMM (placeholder until implemented).
+// tcgen05 GEMM for the DiT projections (K5a-K5f): C[M,N] = A[M,K] . W[N,K]^T
+// with bf16 operands, fp32 accumulation in TMEM and fused epilogues (bf16
+// store, erf-GELU, fp32 residual add). Persistent kernel, one CTA per SM:
+//   warp 0      TMA producer (one elected lane) into a 4-stage smem ring
+//   warp 1      MMA issuer (one elected lane), 128x256x16 UMMA, TMEM alloc
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> global
+// Two 256-column TMEM accumulators let the epilogue of tile i overlap the
+// MMAs of tile i+1. K is consumed in a fixed ascending order and there is no
+// split-K, so every output row is computed identically wherever it sits in
+// M (the cached == recompute invariant).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
 #include "device.cuh"
 #include "kernels_bf16.cuh"
+#include "tc_common.cuh"
+
 namespace bp {
-void launch_gemm_tc(const bf16*, int64_t, const bf16*, int, int, int, void*, int64_t, int, cudaStream_t) {
-  fail(BP_ERR_INTERNAL, "tcgen05 GEMM not built");
+
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr uint32_t A_BYTES = BM * BK * 2;
+constexpr uint32_t B_BYTES = BN * BK * 2;
+constexpr uint32_t SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ float gelu_erf_f(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M, int N,
+              int K, void* __restrict__ Cv, int64_t ldc) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int m_tiles = (M + BM - 1) / BM;
+  const int total = n_tiles * m_tiles;
+  const int num_k = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&map_a);
+    tc::tma_prefetch(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 128);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- TMA producer -----------------------------------------------------------
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int m_blk = tile / n_tiles, n_blk = tile - m_blk * n_tiles;
+      for (int kb = 0; kb < num_k; ++kb) {
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) {
+          tc::mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
+          tc::tma_load_2d(sa + stage * A_BYTES, &map_a, &full[stage], kb * BK, m_blk * BM);
+          tc::tma_load_2d(sb + stage * B_BYTES, &map_b, &full[stage], kb * BK, n_blk * BN);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer ---------------------------------------------------------------
+    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc::fence_after_sync();
+      const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+      for (int kb = 0; kb < num_k; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
+        tc::fence_after_sync();
+        if (lane == 0) {
+          const uint32_t a0 = tc::smem_u32(sa + stage * A_BYTES);
+          const uint32_t b0 = tc::smem_u32(sb + stage * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = tc::desc_sw128(a0 + kk * 32, 1024, 16);
+            const uint64_t bd = tc::desc_sw128(b0 + kk * 32, 1024, 16);
+            tc::mma_bf16(d, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+          }
+          tc::mma_commit(&empty[stage]);  // smem slot free once these MMAs finish
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) tc::mma_commit(&tfull[acc]);  // accumulator ready
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else {
+    // ---- epilogue (warps 2..5 -> TMEM lane quarters 2,3,0,1) -----------------------------
+    const int q = warp & 3;
+    const int r_in = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int m_blk = tile / n_tiles, n_blk = tile - m_blk * n_tiles;
+      tc::mbar_wait(&tfull[acc], acc_phase);
+      tc::fence_after_sync();
+      const int row = m_blk * BM + r_in;
+      const bool row_ok = row < M;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tc::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c), r);
+        tc::tmem_ld_wait();
+        const int col = n_blk * BN + c;
+        if (!row_ok || col >= N) continue;
+        if (EPI == kGemmStoreBf16 || EPI == kGemmGeluBf16) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+            if (EPI == kGemmGeluBf16) { x0 = gelu_erf_f(x0); x1 = gelu_erf_f(x1); }
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
+            pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<bf16*>(Cv) + static_cast<int64_t>(row) * ldc + col);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+        } else {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(Cv) + static_cast<int64_t>(row) * ldc + col);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            float4 o = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                   __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+            if (EPI == kGemmResidualF32) {
+              const float4 old = dst[v];
+              o.x = old.x + o.x; o.y = old.y + o.y; o.z = old.z + o.z; o.w = old.w + o.w;
+            }
+            dst[v] = o;
+          }
+        }
+      }
+      tc::fence_before_sync();
+      tc::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<512>(tmem_base);
+  }
 }
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::mutex g_map_mu;
+
+struct MapKey {
+  const void* p; uint64_t rows, cols, ld; uint32_t br, bc;
+  bool operator==(const MapKey& o) const {
+    return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld && br == o.br && bc == o.bc;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = reinterpret_cast<size_t>(k.p);
+    h = h * 1000003u ^ k.rows;
+    h = h * 1000003u ^ k.cols;
+    h = h * 1000003u ^ k.ld;
+    h = h * 1000003u ^ (static_cast<size_t>(k.br) << 16 | k.bc);
+    return h;
+  }
+};
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+template <int EPI>
+void launch_epi(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, void* C, int64_t ldc,
+                cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    BP_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    configured = true;
+  }
+  const int total = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = total < kNumSms ? total : kNumSms;
+  k_gemm_tc<EPI><<<grid, kThreads, SMEM_BYTES, st>>>(ma, mb, M, N, K, C, ldc);
+}
+
+}  // namespace
+
+void make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                       uint32_t box_rows, uint32_t box_cols) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q{};
+    void* fn = nullptr;
+    BP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) fail(BP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(BP_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+static const CUtensorMap& cached_map(const void* p, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t br,
+                                     uint32_t bc) {
+  std::lock_guard<std::mutex> lock(g_map_mu);
+  const MapKey k{p, rows, cols, ld, br, bc};
+  auto it = g_maps.find(k);
+  if (it != g_maps.end()) return it->second;
+  if (g_maps.size() > 4096) g_maps.clear();
+  CUtensorMap m;
+  make_tmap_2d_bf16(&m, p, rows, cols, ld, br, bc);
+  return g_maps.emplace(k, m).first->second;
+}
+
+void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C, int64_t ldc, int epi,
+                    cudaStream_t st) {
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15)
+    fail(BP_ERR_INTERNAL, "GEMM operands must be 16-byte aligned");
+  if ((lda * 2) % 16 || (K * 2) % 16 || N % 32 || ldc % 8)
+    fail(BP_ERR_INTERNAL, "GEMM strides must be 16-byte multiples and N % 32 == 0");
+  const CUtensorMap ma = cached_map(A, static_cast<uint64_t>(M), static_cast<uint64_t>(K), static_cast<uint64_t>(lda), BM, BK);
+  const CUtensorMap mb = cached_map(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(K), BN, BK);
+  switch (epi) {
+    case kGemmStoreBf16: launch_epi<kGemmStoreBf16>(ma, mb, M, N, K, C, ldc, st); break;
+    case kGemmGeluBf16: launch_epi<kGemmGeluBf16>(ma, mb, M, N, K, C, ldc, st); break;
+    case kGemmResidualF32: launch_epi<kGemmResidualF32>(ma, mb, M, N, K, C, ldc, st); break;
+    default: launch_epi<kGemmStoreF32>(ma, mb, M, N, K, C, ldc, st); break;
+  }
+  count_launch();
+}
+
 }  // namespace bp

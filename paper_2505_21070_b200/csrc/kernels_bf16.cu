@@ -182,8 +182,8 @@ void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int
 void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st);
 
 namespace {
-int g_gemm_impl = 0;  // 0 = SIMT check path, 1 = tcgen05
-int g_attn_impl = 0;
+int g_gemm_impl = 1;  // 0 = SIMT check path, 1 = tcgen05
+int g_attn_impl = 1;
 }  // namespace
 
 void set_gemm_impl(int impl) { g_gemm_impl = impl; }

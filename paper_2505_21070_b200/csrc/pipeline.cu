@@ -46,7 +46,7 @@ class Pipeline {
   void append_block(const SchedBlock& b, cudaStream_t st);
   void assemble(const SchedPass& p, cudaStream_t st);
   void step(const SchedPass& p, const void* eps, cudaStream_t st);
-  void emit_block(const SchedBlock& b, cudaStream_t st);
+  void emit_block(const SchedBlock& b, cudaStream_t st, bool to_host);
   StageInput stage_input(const SchedPass& p, int stage, const void* payload, bool* use_cache_checked);
   void before_stage(const SchedPass& p, int stage, Stage& s, StageInput* in);
   void after_stage(const SchedPass& p, int stage, Stage& s);
@@ -238,12 +238,13 @@ void Pipeline::step(const SchedPass& p, const void* eps, cudaStream_t st) {
   }
 }
 
-void Pipeline::emit_block(const SchedBlock& b, cudaStream_t st) {
+void Pipeline::emit_block(const SchedBlock& b, cudaStream_t st, bool to_host) {
   const size_t k = block_dev.size();
   const double* src = version_ptr(b.id, d_.steps);
   block_dev.push_back(src);
   block_count.push_back(b.frames * hwc_);
-  BP_CUDA(cudaMemcpyAsync(pinned_[k], src, static_cast<size_t>(b.frames * hwc_) * 8, cudaMemcpyDeviceToHost, st));
+  if (to_host)
+    BP_CUDA(cudaMemcpyAsync(pinned_[k], src, static_cast<size_t>(b.frames * hwc_) * 8, cudaMemcpyDeviceToHost, st));
 }
 
 // DeviceWorker::process cache checks (engine.cpp:142-171) before the forward.
@@ -300,8 +301,20 @@ void Pipeline::run(bp_emit_fn emit, void* user) {
   block_count.clear();
   fault_pending_ = d_.fault_inject_ulp != 0;
   launches_at_start_ = g_launches.load();
+  for (auto& s : stages_)
+    if (s) s->set_profiling(profiling);
   if (d_.transport == BP_TRANSPORT_NCCL && d_.devices > 1) run_nccl(emit, user);
   else run_rank0_loopback(emit, user);
+  stats.attn_ms = stats.gemm_ms = stats.cross_ms = 0.0;
+  stats.attn_launches = stats.gemm_launches = stats.cross_launches = 0;
+  for (auto& s : stages_) {
+    if (!s) continue;
+    double ms[3];
+    int64_t n[3];
+    s->prof_collect(ms, n);
+    stats.attn_ms += ms[0]; stats.cross_ms += ms[1]; stats.gemm_ms += ms[2];
+    stats.attn_launches += n[0]; stats.cross_launches += n[1]; stats.gemm_launches += n[2];
+  }
   stats.passes = static_cast<int64_t>(sched.passes.size());
   stats.kernel_launches = g_launches.load() - launches_at_start_;
   stats.peak_bytes = g_dev_peak.load();
@@ -335,7 +348,7 @@ void Pipeline::run_rank0_loopback(bp_emit_fn emit, void* user) {
     step(p, cur, st);
     if (p.finishes_block) {
       const SchedBlock& b = sched.blocks[static_cast<size_t>(p.block - 1)];
-      emit_block(b, st);
+      emit_block(b, st, emit != nullptr);
       ++next_emit;
     }
   }
@@ -447,7 +460,7 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
         step(p, ebuf_[p.index & 1].p, st_);
         BP_CUDA(cudaEventRecord(ev_used[p.index], st_));
         post_eps_recv(p.index + 2);
-        if (p.finishes_block) emit_block(sched.blocks[static_cast<size_t>(p.block - 1)], st_);
+        if (p.finishes_block) emit_block(sched.blocks[static_cast<size_t>(p.block - 1)], st_, emit != nullptr);
       }
     }
   } else {

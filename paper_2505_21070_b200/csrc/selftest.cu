@@ -1,0 +1,147 @@
+// Kernel-level self-test and micro-benchmark hooks (include/bp_cuda_test.h).
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "bp_cuda_test.h"
+#include "device.cuh"
+#include "kernels_bf16.cuh"
+
+namespace bp {
+__global__ void k_fill_rand_bf16(bf16* p, int64_t n, uint64_t seed, float scale) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t z = seed + static_cast<uint64_t>(i) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    const float u = static_cast<float>(z >> 40) * (1.0f / 16777216.0f) - 0.5f;
+    p[i] = __float2bfloat16_rn(u * scale);
+  }
+}
+}  // namespace bp
+
+extern "C" {
+
+bp_status bp_set_kernel_impl(int32_t gemm_impl, int32_t attn_impl) {
+  return bp::guarded([&] {
+    bp::set_gemm_impl(gemm_impl);
+    bp::set_attn_impl(attn_impl);
+  });
+}
+
+bp_status bp_selftest_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int32_t epi, const uint16_t* A,
+                           int64_t lda, const uint16_t* W, void* C, int64_t ldc) {
+  return bp::guarded([&] {
+    BP_CUDA(cudaSetDevice(device));
+    const size_t cb = (epi == bp::kGemmStoreBf16 || epi == bp::kGemmGeluBf16) ? 2 : 4;
+    bp::DevBuf da, dw, dc;
+    da.alloc(static_cast<size_t>(M) * lda * 2);
+    dw.alloc(static_cast<size_t>(N) * K * 2);
+    dc.alloc(static_cast<size_t>(M) * ldc * cb);
+    BP_CUDA(cudaMemcpy(da.p, A, static_cast<size_t>(M) * lda * 2, cudaMemcpyHostToDevice));
+    BP_CUDA(cudaMemcpy(dw.p, W, static_cast<size_t>(N) * K * 2, cudaMemcpyHostToDevice));
+    BP_CUDA(cudaMemcpy(dc.p, C, static_cast<size_t>(M) * ldc * cb, cudaMemcpyHostToDevice));
+    bp::launch_gemm_bf16(da.as<bp::bf16>(), lda, dw.as<bp::bf16>(), M, N, K, dc.p, ldc, epi, nullptr);
+    BP_CUDA(cudaDeviceSynchronize());
+    BP_CUDA(cudaMemcpy(C, dc.p, static_cast<size_t>(M) * ldc * cb, cudaMemcpyDeviceToHost));
+  });
+}
+
+bp_status bp_selftest_attn(int32_t device, int64_t rows, int32_t heads, int32_t dh, const uint16_t* q,
+                           const uint16_t* k0, const uint16_t* v0, int64_t n0, const uint16_t* k1,
+                           const uint16_t* v1, int64_t n1, float scale, uint16_t* out) {
+  return bp::guarded([&] {
+    BP_CUDA(cudaSetDevice(device));
+    const int64_t H = static_cast<int64_t>(heads) * dh;
+    bp::DevBuf dq, dk0, dv0, dk1, dv1, dout;
+    auto up = [&](bp::DevBuf& b, const uint16_t* h, int64_t n) {
+      b.alloc(static_cast<size_t>(n) * H * 2 + 16);
+      if (n > 0) BP_CUDA(cudaMemcpy(b.p, h, static_cast<size_t>(n) * H * 2, cudaMemcpyHostToDevice));
+    };
+    up(dq, q, rows);
+    up(dk0, k0, n0);
+    up(dv0, v0, n0);
+    up(dk1, k1, n1);
+    up(dv1, v1, n1);
+    dout.alloc(static_cast<size_t>(rows) * H * 2);
+    bp::AttnBf16Args a{};
+    a.q = dq.as<bp::bf16>(); a.ldq = H;
+    a.k0 = dk0.as<bp::bf16>(); a.ldk0 = H; a.v0 = dv0.as<bp::bf16>(); a.ldv0 = H; a.n0 = n0;
+    a.k1 = dk1.as<bp::bf16>(); a.ldk1 = H; a.v1 = dv1.as<bp::bf16>(); a.ldv1 = H; a.n1 = n1;
+    a.out = dout.as<bp::bf16>(); a.ldo = H;
+    a.heads = heads; a.dh = dh; a.scale = scale;
+    bp::launch_attn_bf16(a, rows, nullptr);
+    BP_CUDA(cudaDeviceSynchronize());
+    BP_CUDA(cudaMemcpy(out, dout.p, static_cast<size_t>(rows) * H * 2, cudaMemcpyDeviceToHost));
+  });
+}
+
+bp_status bp_bench_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int32_t epi, int32_t iters, double* ms) {
+  return bp::guarded([&] {
+    BP_CUDA(cudaSetDevice(device));
+    const size_t cb = (epi == bp::kGemmStoreBf16 || epi == bp::kGemmGeluBf16) ? 2 : 4;
+    bp::DevBuf da, dw, dc;
+    da.alloc(static_cast<size_t>(M) * K * 2);
+    dw.alloc(static_cast<size_t>(N) * K * 2);
+    dc.alloc(static_cast<size_t>(M) * N * cb);
+    bp::k_fill_rand_bf16<<<1024, 256>>>(da.as<bp::bf16>(), static_cast<int64_t>(M) * K, 1, 1.0f);
+    bp::k_fill_rand_bf16<<<1024, 256>>>(dw.as<bp::bf16>(), static_cast<int64_t>(N) * K, 2, 0.05f);
+    BP_CUDA(cudaMemset(dc.p, 0, static_cast<size_t>(M) * N * cb));
+    cudaStream_t st;
+    BP_CUDA(cudaStreamCreate(&st));
+    for (int i = 0; i < 3; ++i) bp::launch_gemm_bf16(da.as<bp::bf16>(), K, dw.as<bp::bf16>(), M, N, K, dc.p, N, epi, st);
+    cudaEvent_t e0, e1;
+    BP_CUDA(cudaEventCreate(&e0));
+    BP_CUDA(cudaEventCreate(&e1));
+    BP_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; ++i) bp::launch_gemm_bf16(da.as<bp::bf16>(), K, dw.as<bp::bf16>(), M, N, K, dc.p, N, epi, st);
+    BP_CUDA(cudaEventRecord(e1, st));
+    BP_CUDA(cudaEventSynchronize(e1));
+    float t = 0;
+    BP_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *ms = t / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+  });
+}
+
+bp_status bp_bench_attn(int32_t device, int64_t rows, int32_t heads, int32_t dh, int64_t n0, int64_t n1,
+                        int32_t iters, double* ms) {
+  return bp::guarded([&] {
+    BP_CUDA(cudaSetDevice(device));
+    const int64_t H = static_cast<int64_t>(heads) * dh;
+    // q/k/v interleaved like the QKV GEMM output [rows, 3H]; prefix [n0, 2H]
+    bp::DevBuf qkv, pre, out;
+    qkv.alloc(static_cast<size_t>(std::max(rows, n1)) * 3 * H * 2);
+    pre.alloc(static_cast<size_t>(n0 + 1) * 2 * H * 2);
+    out.alloc(static_cast<size_t>(rows) * H * 2);
+    bp::k_fill_rand_bf16<<<1024, 256>>>(qkv.as<bp::bf16>(), std::max(rows, n1) * 3 * H, 3, 2.0f);
+    bp::k_fill_rand_bf16<<<1024, 256>>>(pre.as<bp::bf16>(), (n0 + 1) * 2 * H, 4, 2.0f);
+    bp::AttnBf16Args a{};
+    a.q = qkv.as<bp::bf16>(); a.ldq = 3 * H;
+    a.k0 = pre.as<bp::bf16>(); a.ldk0 = 2 * H; a.v0 = pre.as<bp::bf16>() + H; a.ldv0 = 2 * H; a.n0 = n0;
+    a.k1 = qkv.as<bp::bf16>() + H; a.ldk1 = 3 * H; a.v1 = qkv.as<bp::bf16>() + 2 * H; a.ldv1 = 3 * H; a.n1 = n1;
+    a.out = out.as<bp::bf16>(); a.ldo = H;
+    a.heads = heads; a.dh = dh; a.scale = 1.0f / sqrtf(static_cast<float>(dh));
+    cudaStream_t st;
+    BP_CUDA(cudaStreamCreate(&st));
+    for (int i = 0; i < 2; ++i) bp::launch_attn_bf16(a, rows, st);
+    cudaEvent_t e0, e1;
+    BP_CUDA(cudaEventCreate(&e0));
+    BP_CUDA(cudaEventCreate(&e1));
+    BP_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; ++i) bp::launch_attn_bf16(a, rows, st);
+    BP_CUDA(cudaEventRecord(e1, st));
+    BP_CUDA(cudaEventSynchronize(e1));
+    float t = 0;
+    BP_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *ms = t / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+  });
+}
+
+}  // extern "C"

@@ -54,6 +54,7 @@ Stage::Stage(int device, const bp_model_desc& m, uint64_t seed_model, uint64_t s
 Stage::~Stage() {
   cudaSetDevice(device_);
   cudaStreamSynchronize(stream_);
+  for (cudaEvent_t e : prof_pool_) cudaEventDestroy(e);
   if (own_stream_) cudaStreamDestroy(stream_);
 }
 
@@ -430,15 +431,19 @@ const void* Stage::forward_bf16(const StageInput& in) {
       a.ldk0 = a.ldv0 = 2 * H;
       a.n0 = rec_.tokens;
     }
+    prof_mark(2, true);
     launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.wqkv), static_cast<int>(S), 3 * h_, h_, qkv, 3 * H,
                      kGemmStoreBf16, st);
+    prof_mark(2, false);
     a.q = qkv; a.ldq = 3 * H;
     a.k1 = qkv + H; a.ldk1 = 3 * H;
     a.v1 = qkv + 2 * H; a.ldv1 = 3 * H;
     a.n1 = S;
     a.out = at; a.ldo = H;
     a.heads = heads_; a.dh = dh_; a.scale = scale;
+    prof_mark(0, true);
     launch_attn_bf16(a, S, st);
+    prof_mark(0, false);
     if (new_cache) {
       if (contiguous) {
         nc.k.push_back(qkv + row0 * 3 * H + H);
@@ -454,11 +459,15 @@ const void* Stage::forward_bf16(const StageInput& in) {
         nc.ld = 2 * H;
       }
     }
+    prof_mark(2, true);
     launch_gemm_bf16(at, H, static_cast<const bf16*>(w.wo), static_cast<int>(S), h_, h_, x, H,
                      kGemmResidualF32, st);
+    prof_mark(2, false);
     launch_ln_bf16(x, H, lnw + 2 * H, lnw + 3 * H, S, h_, ln, st);
+    prof_mark(2, true);
     launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.cq), static_cast<int>(S), h_, h_, cq, H,
                      kGemmStoreBf16, st);
+    prof_mark(2, false);
     AttnBf16Args c{};
     c.q = cq; c.ldq = H;
     c.k1 = static_cast<const bf16*>(w.ctx_kv); c.ldk1 = 2 * H;
@@ -466,14 +475,20 @@ const void* Stage::forward_bf16(const StageInput& in) {
     c.n1 = Lc_;
     c.out = at; c.ldo = H;
     c.heads = heads_; c.dh = dh_; c.scale = scale;
+    prof_mark(1, true);
     launch_attn_bf16(c, S, st);
+    prof_mark(1, false);
+    prof_mark(2, true);
     launch_gemm_bf16(at, H, static_cast<const bf16*>(w.co), static_cast<int>(S), h_, h_, x, H,
                      kGemmResidualF32, st);
+    prof_mark(2, false);
     launch_ln_bf16(x, H, lnw + 4 * H, lnw + 5 * H, S, h_, ln, st);
+    prof_mark(2, true);
     launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.w1), static_cast<int>(S), F_, h_, hm, F_,
                      kGemmGeluBf16, st);
     launch_gemm_bf16(hm, F_, static_cast<const bf16*>(w.w2), static_cast<int>(S), h_, F_, x, H,
                      kGemmResidualF32, st);
+    prof_mark(2, false);
   }
   cache_ = Entry{};
   if (new_cache) { nc.valid = true; nc.tokens = P; cache_ = std::move(nc); }
@@ -576,6 +591,35 @@ std::string Stage::audit() {
     return "cached V diverges at layer " + std::to_string(layer) + " flat index " + std::to_string(ev);
   }
   return "";
+}
+
+void Stage::prof_mark(int cls, bool begin) {
+  if (!prof_on_) return;
+  if (prof_used_ == prof_pool_.size()) {
+    cudaEvent_t e;
+    BP_CUDA(cudaEventCreate(&e));
+    prof_pool_.push_back(e);
+  }
+  cudaEvent_t e = prof_pool_[prof_used_++];
+  BP_CUDA(cudaEventRecord(e, stream_));
+  if (begin) {
+    prof_open_ = e;
+  } else {
+    prof_marks_.push_back({cls, {prof_open_, e}});
+  }
+}
+
+void Stage::prof_collect(double ms[3], int64_t launches[3]) {
+  for (int i = 0; i < 3; ++i) { ms[i] = 0.0; launches[i] = 0; }
+  if (!prof_marks_.empty()) BP_CUDA(cudaEventSynchronize(prof_marks_.back().second.second));
+  for (const auto& m : prof_marks_) {
+    float t = 0.f;
+    BP_CUDA(cudaEventElapsedTime(&t, m.second.first, m.second.second));
+    ms[m.first] += t;
+    launches[m.first] += 1;
+  }
+  prof_marks_.clear();
+  prof_used_ = 0;
 }
 
 template const void* Stage::forward_simt<double>(const StageInput&);

@@ -59,7 +59,19 @@ class Stage {
   void bump_ulp(int layer, int which, int64_t index);
   std::string audit();  // cache_mismatch_report (model.cpp:171-199)
 
+  // Per-kernel-class device timing with CUDA events on this stage's stream:
+  // class 0 self-attention, 1 cross-attention, 2 GEMMs.
+  void set_profiling(bool on) { prof_on_ = on; }
+  void prof_collect(double ms[3], int64_t launches[3]);
+
  private:
+  void prof_mark(int cls, bool begin);
+  bool prof_on_ = false;
+  std::vector<cudaEvent_t> prof_pool_;
+  size_t prof_used_ = 0;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_marks_;
+  cudaEvent_t prof_open_ = nullptr;
+
   struct LayerW {
     void* wqkv = nullptr;   // SIMT: [h, 3h] row-major; bf16: [3h, h] (K-major)
     void* wo = nullptr;
