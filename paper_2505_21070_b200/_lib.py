@@ -19,6 +19,23 @@ if not os.path.exists(LIB_PATH):
         f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
         "(nvcc, sm_100a). The blockpipe-b200 path has no CPU fallback.")
 
+def _prefer_bundled_nccl() -> None:
+    """NCCL is dlopen'ed lazily by the library; point it at torch's bundled
+    libnccl (if installed) so one process never mixes two NCCL builds."""
+    if "BP_NCCL_LIB" in os.environ:
+        return
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        if spec and spec.submodule_search_locations:
+            cand = os.path.join(list(spec.submodule_search_locations)[0], "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["BP_NCCL_LIB"] = cand
+    except Exception:
+        pass
+
+
+_prefer_bundled_nccl()
 lib = C.CDLL(LIB_PATH)
 
 i32, i64, u64, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double

@@ -5,7 +5,7 @@
 // between stages with ncclSend/ncclRecv on dedicated streams, double-buffered
 // and event-chained to compute, so transfers overlap the next pass.
 #include <cuda_runtime.h>
-#include <nccl.h>
+#include "nccl_dl.hpp"
 
 #include <algorithm>
 #include <cstring>
@@ -21,7 +21,7 @@
   do {                                                                                 \
     ncclResult_t r_ = (call);                                                          \
     if (r_ != ncclSuccess)                                                             \
-      ::bp::fail(BP_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));     \
+      ::bp::fail(BP_ERR_NCCL, std::string(#call) + ": " + bp::nccl().GetErrorString(r_));     \
   } while (0)
 
 namespace bp {
@@ -133,10 +133,10 @@ Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, c
       return u;
     };
     // pair (j, j+1) uses id j; the eps return (N-1 -> 0) uses id N-1.
-    if (rank_ > 0) BP_NCCL(ncclCommInitRank(&comm_prev_, 2, id_of(rank_ - 1), 1));
-    if (rank_ + 1 < N) BP_NCCL(ncclCommInitRank(&comm_next_, 2, id_of(rank_), 0));
-    if (rank_ == N - 1) BP_NCCL(ncclCommInitRank(&comm_eps_, 2, id_of(N - 1), 0));
-    if (rank_ == 0) BP_NCCL(ncclCommInitRank(&comm_eps_, 2, id_of(N - 1), 1));
+    if (rank_ > 0) BP_NCCL(bp::nccl().CommInitRank(&comm_prev_, 2, id_of(rank_ - 1), 1));
+    if (rank_ + 1 < N) BP_NCCL(bp::nccl().CommInitRank(&comm_next_, 2, id_of(rank_), 0));
+    if (rank_ == N - 1) BP_NCCL(bp::nccl().CommInitRank(&comm_eps_, 2, id_of(N - 1), 0));
+    if (rank_ == 0) BP_NCCL(bp::nccl().CommInitRank(&comm_eps_, 2, id_of(N - 1), 1));
     BP_CUDA(cudaStreamCreateWithFlags(&s_recv_, cudaStreamNonBlocking));
     BP_CUDA(cudaStreamCreateWithFlags(&s_send_, cudaStreamNonBlocking));
     BP_CUDA(cudaStreamCreateWithFlags(&s_eps_, cudaStreamNonBlocking));
@@ -153,9 +153,9 @@ Pipeline::~Pipeline() {
   cudaSetDevice(device_);
   cudaDeviceSynchronize();
   for (double* h : pinned_) cudaFreeHost(h);
-  if (comm_prev_) ncclCommDestroy(comm_prev_);
-  if (comm_next_) ncclCommDestroy(comm_next_);
-  if (comm_eps_) ncclCommDestroy(comm_eps_);
+  if (comm_prev_) bp::nccl().CommDestroy(comm_prev_);
+  if (comm_next_) bp::nccl().CommDestroy(comm_next_);
+  if (comm_eps_) bp::nccl().CommDestroy(comm_eps_);
   stages_.clear();
   if (s_recv_) cudaStreamDestroy(s_recv_);
   if (s_send_) cudaStreamDestroy(s_send_);
@@ -419,7 +419,7 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
   auto send_to = [&](ncclComm_t comm, cudaStream_t ss, const SchedPass& p, const void* buf, int peer,
                      size_t count, ncclDataType_t dt) {
     BP_CUDA(cudaStreamWaitEvent(ss, ev_fwd[p.index], 0));
-    BP_NCCL(ncclSend(buf, count, dt, peer, comm, ss));
+    BP_NCCL(bp::nccl().Send(buf, count, dt, peer, comm, ss));
     BP_CUDA(cudaEventRecord(ev_sent[p.index], ss));
   };
 
@@ -440,7 +440,7 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
       if (i >= P) return;
       const SchedPass& p = sched.passes[static_cast<size_t>(i)];
       if (i >= 2) BP_CUDA(cudaStreamWaitEvent(s_eps_, ev_used[i - 2], 0));
-      BP_NCCL(ncclRecv(ebuf_[i & 1].p, static_cast<size_t>(p.tokens) * C_, edt, 0, comm_eps_, s_eps_));
+      BP_NCCL(bp::nccl().Recv(ebuf_[i & 1].p, static_cast<size_t>(p.tokens) * C_, edt, 0, comm_eps_, s_eps_));
       BP_CUDA(cudaEventRecord(ev_recv[i], s_eps_));
     };
     post_eps_recv(0);
@@ -468,7 +468,7 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
       if (i >= P) return;
       const SchedPass& p = sched.passes[static_cast<size_t>(i)];
       if (i >= 2) BP_CUDA(cudaStreamWaitEvent(s_recv_, ev_used[i - 2], 0));
-      BP_NCCL(ncclRecv(rbuf_[i & 1].p, static_cast<size_t>(p.tokens) * H, adt, 0, comm_prev_, s_recv_));
+      BP_NCCL(bp::nccl().Recv(rbuf_[i & 1].p, static_cast<size_t>(p.tokens) * H, adt, 0, comm_prev_, s_recv_));
       BP_CUDA(cudaEventRecord(ev_recv[i], s_recv_));
     };
     post_recv(0);
@@ -523,7 +523,7 @@ extern "C" {
 bp_status bp_nccl_unique_id(uint8_t out[128]) {
   return bp::guarded([&] {
     ncclUniqueId u;
-    BP_NCCL(ncclGetUniqueId(&u));
+    BP_NCCL(bp::nccl().GetUniqueId(&u));
     static_assert(sizeof(u) == 128, "ncclUniqueId size");
     std::memcpy(out, &u, 128);
   });

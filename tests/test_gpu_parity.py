@@ -1,0 +1,155 @@
+"""GPU parity through the C-ABI against the reference (goldens from the
+unmodified reference library, and the library itself where it helps).
+Tolerances are north_star's: fp64 parity mode <= 1e-12 rel-L2,
+fp32 verification mode <= 1e-4, bf16 tensor-core path <= 2e-2; schedule,
+noise ids and the noise pool are bit-exact."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+G = json.load(open(os.path.join(ROOT, "tests", "golden", "goldens.json")))
+
+
+def golden(name):
+    return np.load(os.path.join(ROOT, "tests", "golden", f"{name}_latents.npz"))["latents"]
+
+
+def latents(out):
+    return np.concatenate([b["frames"].ravel() for b in out["blocks"]])
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("name,prec,tol", [("cfg1", "f64", 1e-12), ("cfg1", "f32", 1e-4),
+                                           ("cfg1_nocache", "f64", 1e-12), ("mid", "f64", 1e-12),
+                                           ("mid", "f32", 1e-4), ("mid", "bf16", 2e-2)])
+def test_pipeline_latents_vs_reference(bp, name, prec, tol):
+    cfg = dict(G[name]["config"], precision=prec)
+    out = bp.run_pipeline(cfg)
+    r = rel(latents(out), golden(name))
+    print(name, prec, r)
+    assert r <= tol
+    assert [b["noise_ids"] for b in out["blocks"]] == [b["noise_ids"] for b in G[name]["blocks"]]
+    assert [b["frame_ids"] for b in out["blocks"]] == [b["frame_ids"] for b in G[name]["blocks"]]
+    assert np.array_equal(out["events"], np.load(os.path.join(ROOT, "tests", "golden", f"{name}_latents.npz"))["events"])
+
+
+@pytest.mark.parametrize("prec", ["f64", "bf16"])
+@pytest.mark.parametrize("n", [2, 4])
+def test_loopback_pipeline_equals_serial_bitwise(bp, prec, n):
+    """test_engine.cpp:66-78 on the GPU: N stages == 1 stage, bitwise."""
+    base = dict(G["mid"]["config"], precision=prec)
+    a = bp.run_pipeline(dict(base, devices=n))
+    b = bp.serial_oracle(base)
+    assert all(np.array_equal(x["frames"], y["frames"]) for x, y in zip(a["blocks"], b["blocks"]))
+    assert a["ledger"] != b["ledger"]  # different channel layout, same math
+
+
+@pytest.mark.parametrize("prec", ["f64", "bf16"])
+def test_cached_equals_recompute_bitwise(bp, prec):
+    """test_engine.cpp:129-150: kCached == kRecompute on latents and on every pass's eps."""
+    base = dict(G["mid"]["config"], precision=prec, devices=2, record_trace=True)
+    c = bp.run_pipeline(dict(base, cache="on"))
+    r = bp.run_pipeline(dict(base, cache="recompute"))
+    assert all(np.array_equal(x["frames"], y["frames"]) for x, y in zip(c["blocks"], r["blocks"]))
+    assert len(c["trace"]) == len(r["trace"]) == 18
+    assert all(np.array_equal(x["eps"], y["eps"]) for x, y in zip(c["trace"], r["trace"]))
+
+
+@pytest.mark.parametrize("prec", ["f64", "bf16"])
+def test_fault_injection_caught(bp, prec):
+    base = dict(G["mid"]["config"], precision=prec, devices=2, check_cache=True)
+    with pytest.raises(bp.CacheError, match="cached V diverges at layer 0 flat index 0"):
+        bp.run_pipeline(dict(base, fault_inject=True))
+    quiet = bp.run_pipeline(base)  # the audit is quiet on an intact cache
+    plain = bp.run_pipeline(dict(base, check_cache=False))
+    assert all(np.array_equal(x["frames"], y["frames"]) for x, y in zip(quiet["blocks"], plain["blocks"]))
+
+
+def test_trace_vs_reference_f64(bp, ref):
+    """Per-pass eps (the sharper diagnostic) against the reference."""
+    cfg = bp.PipelineConfig.from_dict(dict(G["cfg1"]["config"], record_trace=True, devices=2))
+    got = bp.run_pipeline(cfg)["trace"]
+    want = ref.run(cfg)["trace"]
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert (g["round"], g["block_id"]) == (w["round"], w["block_id"])
+        assert rel(g["eps"], w["eps"]) < 1e-12
+
+
+@pytest.mark.parametrize("kw", [dict(strategy="complete-shuffle"), dict(strategy="subset"), dict(strategy="fresh"),
+                                dict(strategy="repeat"), dict(retain_clean_context=False), dict(num_c=0),
+                                dict(order="sequential"), dict(cache="off", order="sequential"),
+                                dict(devices=4, steps=6, blocks=2)])
+def test_engine_variants_vs_reference(bp, ref, kw):
+    """test_engine.cpp:223-276 variants through the GPU engine vs the reference."""
+    cfg = bp.PipelineConfig.from_dict(dict({"devices": 2, "layers": 4, "hidden": 16, "heads": 2, "steps": 4,
+                                            "blocks": 4, "mode": "single"}, **kw))
+    got, want = bp.run_pipeline(cfg), ref.run(cfg)
+    assert [b["block_id"] for b in got["blocks"]] == [b["block_id"] for b in want["blocks"]]
+    assert [b["noise_ids"] for b in got["blocks"]] == [b["noise_ids"] for b in want["blocks"]]
+    assert rel(latents(got), latents(want)) < 1e-12
+    assert np.array_equal(got["events"], want["events"])
+
+
+def test_forward_chunk_cases_f64(bp, ref):
+    """test_model.cpp:139-223 cases through bp_forward_chunk vs the reference."""
+    cfg = bp.PipelineConfig(layers=2, hidden=8, heads=2, channels=2, height=1, width=1, context_len=3)
+    st, rc = bp.Stage(cfg, 17, 0, 2, 19), ref.RefChunk(cfg, 17, 0, 2, 19)
+    rng = np.random.default_rng(0)
+    prev = rng.standard_normal((2, 2))
+    a = st.forward_chunk(prev, [5, 5], [4, 5], capture_frames=[0], mode="on")
+    b = rc.forward(prev, [5, 5], [4, 5], capture=[0], mode="on")
+    assert rel(a["payload"], b) < 1e-12 and a["captured"] and a["captured_tokens"] == 1
+    assert rel(st.cache_rows(0, 1), rc.cache(0, 1)) < 1e-12
+    cur = rng.standard_normal((3, 2))
+    a2 = st.forward_chunk(cur, [4, 4, 4], [1, 2, 3], mode="on", use_prev=1)
+    b2 = rc.forward(cur, [4, 4, 4], [1, 2, 3], mode="on", use_prev=1)
+    assert rel(a2["payload"], b2) < 1e-12
+    # chunked == monolithic (test_model.cpp:155-176), bitwise on the GPU
+    cfg4 = bp.PipelineConfig(layers=4, hidden=8, heads=2, channels=2, height=1, width=1, context_len=3)
+    mono, p0, p1 = bp.Stage(cfg4, 9, 0, 4, 13), bp.Stage(cfg4, 9, 0, 2, 13), bp.Stage(cfg4, 9, 2, 4, 13)
+    x = rng.standard_normal((3, 2))
+    whole = mono.forward_chunk(x, [2, 2, 2], [5, 6, 7])["payload"]
+    mid = p0.forward_chunk(x, [2, 2, 2], [5, 6, 7])["payload"]
+    last = p1.forward_chunk(mid, [2, 2, 2], [5, 6, 7])["payload"]
+    assert np.array_equal(whole, last)
+    # cache supplied while caching is disabled (model.cpp:269-271)
+    with pytest.raises(bp.CacheError):
+        st.forward_chunk(cur, [4, 4, 4], [1, 2, 3], mode="off", use_prev=1)
+
+
+def test_one_ulp_sensitivity(bp):
+    """test_model.cpp:216-222: a 1-ulp bump in the cache changes the output."""
+    cfg = bp.PipelineConfig(layers=2, hidden=8, heads=2, channels=2, height=1, width=1, context_len=3)
+    st = bp.Stage(cfg, 17, 0, 2, 19)
+    rng = np.random.default_rng(1)
+    prev, cur = rng.standard_normal((2, 2)), rng.standard_normal((3, 2))
+    st.forward_chunk(prev, [5, 5], [4, 5], capture_frames=[0], mode="on")
+    clean = st.forward_chunk(cur, [4, 4, 4], [1, 2, 3], mode="on", use_prev=1)["payload"]
+    st.forward_chunk(prev, [5, 5], [4, 5], capture_frames=[0], mode="on")
+    st.bump_ulp(0, 1, 0)
+    bumped = st.forward_chunk(cur, [4, 4, 4], [1, 2, 3], mode="on", use_prev=1)["payload"]
+    assert not np.array_equal(clean, bumped)
+
+
+def test_scheduler_step_closed_form(bp):  # test_model.cpp:270-298
+    rng = np.random.default_rng(71)
+    x, eps = rng.standard_normal((2, 3)), rng.standard_normal((2, 3))
+    assert np.array_equal(bp.scheduler_step(x, eps, 25, 50), x - 0.02 * eps)
+    with pytest.raises(bp.SchedulerError):
+        bp.scheduler_step(x, eps, 0, 8)
+    with pytest.raises(bp.SchedulerError):
+        bp.scheduler_step(x, eps, 9, 8)
+
+
+def test_pool_720p_bit_exact(bp, ref):
+    seed = bp.derive_seed(2, [0])
+    assert np.array_equal(bp.build_pool(8, 8, (45, 80, 64), seed), ref.pool(8, 8, (45, 80, 64), seed))

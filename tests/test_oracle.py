@@ -1,0 +1,74 @@
+"""The oracle is pinned before it is trusted: the glibc log/cos port, the C
+RNG restatement and the numpy restatement all against goldens generated from
+the unmodified reference (tests/golden/make_goldens.py)."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import blockpipe_oracle as bo
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+G = json.load(open(os.path.join(ROOT, "tests", "golden", "goldens.json")))
+
+
+def test_glibc_port_bit_exact_on_host(tmp_path):
+    """The device noise kernel's log/cos (paper_2505_21070_b200/csrc/glibc_port.h)
+    compiled for the host equals this image's glibc on 2M Box-Muller draws."""
+    exe = tmp_path / "chk"
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-I", os.path.join(ROOT, "paper_2505_21070_b200", "csrc"),
+                    os.path.join(ROOT, "tools", "check_glibc_port.c"), "-lm", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), "2000000"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout
+    assert "bad_log=0 bad_cos=0 bad_boxmuller=0" in out.stdout
+
+
+def test_rng_restatement_goldens():
+    rs = bo.RandomSource(1)
+    assert [rs.next_normal() for _ in range(3)] == G["rng"]["normals_seed1"]
+    for k, v in G["rng"]["derive"].items():
+        base, tags = k.split(",", 1)
+        assert bo.derive_seed(int(base), json.loads(tags)) == v
+    # SURVEY Appendix A known answers
+    assert [hex(bo.RandomSource(1).next_u64())] == ["0x910a2dec89025cc1"]
+    assert bo.derive_seed(2, [0]) == 0xBFC846100BFC1E42 and bo.derive_seed(2, [1]) == 0xD0D5127A96E8D90D
+
+
+def test_pool_restatement_fnv():
+    from oracle.ref import fnv1a64
+    seed = bo.derive_seed(2, [0])
+    for tag in ("tiny", "480p"):
+        shape = G["pools"][tag]["shape"]
+        pool = bo.RandomSource(seed).normal_tensor((12, *shape))
+        assert fnv1a64([pool]) == G["pools"][tag]["fnv"]
+    assert G["pools"]["480p"]["fnv"] == "507c6ce247b45327"
+
+
+def test_coordinated_ids_goldens():
+    assert G["coordinated_ids"][0] == [2, 9, 10, 4, 6, 5, 0, 11, 1, 3, 8, 7]
+    assert G["coordinated_ids"][1] == [0, 4, 6, 10, 9, 2, 5, 11]
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg1_nocache", "mid"])
+def test_numpy_restatement_matches_reference_latents(name):
+    d = dict(G[name]["config"])
+    cfg = {"layers": 4, "hidden": 16, "heads": 2, "channels": 2, "height": 2, "width": 2, "context_len": 4,
+           "num_b": 2, "num_c": 4, "steps": 8, "blocks": 6}
+    cfg.update({k: v for k, v in d.items() if k not in ("devices", "mode")})
+    r = bo.run_pipeline(cfg)
+    lat = np.concatenate([b["frames"].ravel() for b in r["blocks"]])
+    want = np.load(os.path.join(ROOT, "tests", "golden", f"{name}_latents.npz"))["latents"]
+    assert np.linalg.norm(lat - want) / np.linalg.norm(want) < 1e-12
+    assert [b["noise_ids"] for b in r["blocks"]] == [b["noise_ids"] for b in G[name]["blocks"]]
+    if name == "cfg1":
+        assert abs(G["cfg1"]["sumsq"] - 135.10119655928548) < 1e-12
+
+
+def test_reference_library_matches_goldens(ref):
+    import paper_2505_21070_b200 as bp
+    cfg = bp.PipelineConfig.from_dict(G["cfg1"]["config"])
+    r = ref.run(cfg)
+    lat = np.concatenate([b["frames"].ravel() for b in r["blocks"]])
+    assert ref.fnv1a64([lat]) == G["cfg1"]["fnv"]
