@@ -126,14 +126,22 @@ def test_forward_chunk_cases_f64(bp, ref):
         st.forward_chunk(cur, [4, 4, 4], [1, 2, 3], mode="off", use_prev=1)
 
 
-def test_one_ulp_sensitivity(bp):
-    """test_model.cpp:216-222: a 1-ulp bump in the cache changes the output."""
+def test_one_ulp_sensitivity(bp, ref):
+    """test_model.cpp:178-223 with its exact inputs (RandomSource(23) draws):
+    cached == recompute, and a 1-ulp bump of cached V[0][0] changes the output."""
+    from oracle.blockpipe_oracle import RandomSource
     cfg = bp.PipelineConfig(layers=2, hidden=8, heads=2, channels=2, height=1, width=1, context_len=3)
+    rs = RandomSource(23)
+    prev, cur = rs.normal_tensor((2, 2)), rs.normal_tensor((3, 2))
     st = bp.Stage(cfg, 17, 0, 2, 19)
-    rng = np.random.default_rng(1)
-    prev, cur = rng.standard_normal((2, 2)), rng.standard_normal((3, 2))
     st.forward_chunk(prev, [5, 5], [4, 5], capture_frames=[0], mode="on")
     clean = st.forward_chunk(cur, [4, 4, 4], [1, 2, 3], mode="on", use_prev=1)["payload"]
+    rc = ref.RefChunk(cfg, 17, 0, 2, 19)
+    rc.forward(prev, [5, 5], [4, 5], capture=[0], mode="on")
+    assert rel(clean, rc.forward(cur, [4, 4, 4], [1, 2, 3], mode="on", use_prev=1)) < 1e-12
+    st.forward_chunk(prev, [5, 5], [4, 5], capture_frames=[0], mode="recompute")
+    via_rec = st.forward_chunk(cur, [4, 4, 4], [1, 2, 3], mode="recompute", use_prev=2)["payload"]
+    assert np.array_equal(clean, via_rec)
     st.forward_chunk(prev, [5, 5], [4, 5], capture_frames=[0], mode="on")
     st.bump_ulp(0, 1, 0)
     bumped = st.forward_chunk(cur, [4, 4, 4], [1, 2, 3], mode="on", use_prev=1)["payload"]
