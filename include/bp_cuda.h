@@ -119,7 +119,14 @@ typedef struct {
   int32_t record_inputs;
   int32_t mode;                    /* bp_cache_mode */
   int32_t use_prev;                /* 0: no prefix; 1: the stage's resident captured
-                                      K/V (KVCacheEntry); 2: its recorded inputs */
+                                      K/V (KVCacheEntry); 2: its recorded inputs;
+                                      3: host K/V below; 4: host recorded inputs below */
+  /* use_prev 3: a host KVCacheEntry, per local layer [prefix_rows, h] K then V,
+   * layer-major (prefix_k[l*rows*h ...]). use_prev 4: a host RecomputeEntry,
+   * per local layer [prefix_rows, h] layer inputs in prefix_k. */
+  const double* prefix_k;
+  const double* prefix_v;
+  int64_t prefix_rows;
 } bp_chunk_in;
 
 /* ChunkOutput (model.hpp:114-118). payload is a caller buffer of
@@ -140,6 +147,12 @@ bp_status bp_forward_chunk(bp_stage* stage, const bp_chunk_in* in, bp_chunk_out*
  * layer as fp64 [rows, h]; out may be NULL to query rows. */
 bp_status bp_stage_cache_rows(bp_stage* stage, int32_t layer, int32_t which, double* out,
                               int64_t* rows);
+/* Downloads the resident recorded layer inputs of one local layer as fp64
+ * [rows, h] (RecomputeEntry::layer_inputs); out may be NULL to query rows. */
+bp_status bp_stage_recorded_rows(bp_stage* stage, int32_t layer, double* out, int64_t* rows);
+/* Replaces the cross-attention context [rows = context_len, cols = h] (host
+ * fp64) and re-derives the hoisted context K/V (model.cpp:216-217). */
+bp_status bp_stage_set_context(bp_stage* stage, const double* context, int64_t rows, int64_t cols);
 /* Bumps one resident cached value by one ulp towards +inf (engine.cpp:185-189). */
 bp_status bp_stage_cache_bump_ulp(bp_stage* stage, int32_t layer, int32_t which, int64_t index);
 /* cache_mismatch_report (model.cpp:171-199) on the resident cache vs the

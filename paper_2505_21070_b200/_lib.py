@@ -61,7 +61,8 @@ class ChunkIn(C.Structure):
     _fields_ = [("payload", P(f64)), ("rows", i64), ("cols", i64),
                 ("frame_levels", P(i32)), ("frame_ids", P(i64)), ("nframes", i32),
                 ("capture_frames", P(i32)), ("ncapture", i32), ("record_inputs", i32),
-                ("mode", i32), ("use_prev", i32)]
+                ("mode", i32), ("use_prev", i32), ("prefix_k", P(f64)), ("prefix_v", P(f64)),
+                ("prefix_rows", i64)]
 
 
 class ChunkOut(C.Structure):
@@ -88,6 +89,8 @@ _SIGS = {
     "bp_forward_chunk": (i32, [C.c_void_p, P(ChunkIn), P(ChunkOut)]),
     "bp_stage_cache_rows": (i32, [C.c_void_p, i32, i32, P(f64), P(i64)]),
     "bp_stage_cache_bump_ulp": (i32, [C.c_void_p, i32, i32, i64]),
+    "bp_stage_recorded_rows": (i32, [C.c_void_p, i32, P(f64), P(i64)]),
+    "bp_stage_set_context": (i32, [C.c_void_p, P(f64), i64, i64]),
     "bp_stage_cache_audit": (i32, [C.c_void_p, C.c_char_p, i32]),
     "bp_scheduler_step": (i32, [i32, P(f64), P(f64), i64, i32, i32, P(f64)]),
     "bp_schedule_create": (i32, [P(PipelineDesc), P(C.c_void_p)]),

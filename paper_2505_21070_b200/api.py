@@ -108,7 +108,7 @@ class Stage:
             raise errors.DimensionError("payload rows do not match frames * tokens_per_frame")
         cin = ChunkIn(_ptr(payload, f64), rows, payload.shape[1] if payload.ndim > 1 else 1,
                       _ptr(lv, i32), _ptr(fi, i64), len(lv), _ptr(cf, i32), len(cf),
-                      int(record_inputs), CACHE[mode], int(use_prev))
+                      int(record_inputs), CACHE[mode], int(use_prev), None, None, 0)
         out_cols = self.cfg.channels if self.end == self.cfg.layers else self.cfg.hidden
         out = np.empty((rows, out_cols), dtype=np.float64)
         cout = ChunkOut(_ptr(out, f64), out.size, 0, 0, 0, 0, 0)

@@ -159,6 +159,21 @@ bp_status bp_forward_chunk(bp_stage* h, const bp_chunk_in* in, bp_chunk_out* out
       BP_CUDA(cudaMemcpyAsync(h->levels.p, in->frame_levels, static_cast<size_t>(frames) * 4, cudaMemcpyHostToDevice, st));
       BP_CUDA(cudaMemcpyAsync(h->ids.p, in->frame_ids, static_cast<size_t>(frames) * 8, cudaMemcpyHostToDevice, st));
     }
+    if (in->use_prev == 3 || in->use_prev == 4) {
+      // host KVCacheEntry / RecomputeEntry (model.hpp:86-101) for this call
+      const int nl = s.local_layers();
+      const size_t n1 = static_cast<size_t>(nl) * in->prefix_rows * s.hidden();
+      if (!in->prefix_k || (in->use_prev == 3 && !in->prefix_v)) bp::fail(BP_ERR_CACHE, "missing host prefix");
+      bp::DevBuf dk, dv;
+      dk.alloc(n1 * 8 + 8);
+      BP_CUDA(cudaMemcpyAsync(dk.p, in->prefix_k, n1 * 8, cudaMemcpyHostToDevice, st));
+      if (in->use_prev == 3) {
+        dv.alloc(n1 * 8 + 8);
+        BP_CUDA(cudaMemcpyAsync(dv.p, in->prefix_v, n1 * 8, cudaMemcpyHostToDevice, st));
+      }
+      s.load_host_prefix(in->use_prev, dk.as<double>(), dv.as<double>(), in->prefix_rows);
+      BP_CUDA(cudaStreamSynchronize(st));
+    }
     si.payload = h->payload.p;
     si.d_levels = h->levels.as<int32_t>();
     si.d_frame_ids = h->ids.as<int64_t>();
@@ -189,6 +204,18 @@ bp_status bp_stage_cache_rows(bp_stage* h, int32_t layer, int32_t which, double*
     if (rows) *rows = h->s->cache_tokens();
     if (out) h->s->cache_rows(layer, which, out);
   });
+}
+
+bp_status bp_stage_recorded_rows(bp_stage* h, int32_t layer, double* out, int64_t* rows) {
+  return bp::guarded([&] {
+    if (!h->s->rec_valid()) bp::fail(BP_ERR_CACHE, "no resident recording");
+    if (rows) *rows = h->s->rec_tokens();
+    if (out) h->s->recorded_rows(layer, out);
+  });
+}
+
+bp_status bp_stage_set_context(bp_stage* h, const double* context, int64_t rows, int64_t cols) {
+  return bp::guarded([&] { h->s->set_context(context, rows, cols); });
 }
 
 bp_status bp_stage_cache_bump_ulp(bp_stage* h, int32_t layer, int32_t which, int64_t index) {

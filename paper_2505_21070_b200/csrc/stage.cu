@@ -61,6 +61,7 @@ Stage::~Stage() {
 size_t Stage::act_bytes() const { return prec_ == BP_PREC_F64 ? 8 : 4; }
 
 void Stage::build_weights(uint64_t seed_model, uint64_t seed_context) {
+  seed_model_ = seed_model;
   const int nl = end_ - begin_;
   const bool bf = prec_ == BP_PREC_BF16;
   const size_t te = prec_ == BP_PREC_F64 ? 8 : 4;  // SIMT element / fp32 side tensors
@@ -99,12 +100,9 @@ void Stage::build_weights(uint64_t seed_model, uint64_t seed_context) {
   // Scratch: fp64 draw buffer, context, and the cross K|V weights for hoisting.
   const size_t max_numel = std::max({hF, hh, static_cast<size_t>(Lc_) * h_,
                                      static_cast<size_t>(C_) * h_});
-  DevBuf gen, ctx64, ctxT, ckvT, kvT;
+  DevBuf gen, ctx64;
   gen.alloc(max_numel * 8);
   ctx64.alloc(static_cast<size_t>(Lc_) * h_ * 8);
-  ctxT.alloc(static_cast<size_t>(Lc_) * h_ * te);
-  ckvT.alloc(2 * hh * te);
-  kvT.alloc(static_cast<size_t>(Lc_) * 2 * h_ * te);
   double* g = gen.as<double>();
   cudaStream_t st = stream_;
 
@@ -132,8 +130,6 @@ void Stage::build_weights(uint64_t seed_model, uint64_t seed_context) {
 
   // context (build_context, model.cpp:150-153): RandomSource(seed_context), sigma 1
   launch_normal_fill(seed_context, static_cast<int64_t>(Lc_) * h_, 1.0, ctx64.as<double>(), st);
-  if (prec_ == BP_PREC_F64) launch_place<double>(ctx64.as<double>(), Lc_, h_, ctxT.as<double>(), h_, 0, st);
-  else launch_place<float>(ctx64.as<double>(), Lc_, h_, ctxT.as<float>(), h_, 0, st);
 
   for (int l = 0; l < nl; ++l) {
     LayerW& w = lw_[static_cast<size_t>(l)];
@@ -152,28 +148,8 @@ void Stage::build_weights(uint64_t seed_model, uint64_t seed_context) {
       draw(layer, r, H, H);
       place_side(w.ln, H, static_cast<int64_t>(r - kLn1G) * H);
     }
-    // Cross-attention K|V of the fixed context, hoisted out of the per-pass
-    // loop (model.cpp:216-217 recomputes it every pass; it is constant).
-    for (uint64_t r = kCk; r <= kCv; ++r) {
-      draw(layer, r, H * H, H);
-      const int64_t off = static_cast<int64_t>(r - kCk) * H;
-      if (prec_ == BP_PREC_F64) launch_place<double>(g, H, H, ckvT.as<double>() + off, 2 * H, 0, st);
-      else launch_place<float>(g, H, H, ckvT.as<float>() + off, 2 * H, 0, st);
-    }
-    if (prec_ == BP_PREC_F64) {
-      launch_matmul<double>(ctxT.as<double>(), H, ckvT.as<double>(), 2 * H, Lc_, 2 * h_, h_,
-                            static_cast<double*>(w.ctx_kv), 2 * H, kEpiNone, nullptr, 0, st);
-    } else if (prec_ == BP_PREC_F32) {
-      launch_matmul<float>(ctxT.as<float>(), H, ckvT.as<float>(), 2 * H, Lc_, 2 * h_, h_,
-                           static_cast<float*>(w.ctx_kv), 2 * H, kEpiNone, nullptr, 0, st);
-    } else {
-      launch_matmul<float>(ctxT.as<float>(), H, ckvT.as<float>(), 2 * H, Lc_, 2 * h_, h_,
-                           kvT.as<float>(), 2 * H, kEpiNone, nullptr, 0, st);
-      // fp32 -> bf16 via an fp64 hop through the draw scratch
-      launch_convert<float, double>(kvT.as<float>(), g, static_cast<int64_t>(Lc_) * 2 * H, st);
-      launch_place<bf16>(g, Lc_, 2 * H, static_cast<bf16*>(w.ctx_kv), 2 * H, 0, st);
-    }
   }
+  hoist_context(ctx64.as<double>());
   if (is_first()) {
     const uint64_t state = derive_seed2(seed_model, static_cast<uint64_t>(m_.layers), kPatchify);
     launch_normal_fill(state, static_cast<int64_t>(C_) * h_, 1.0 / std::sqrt(static_cast<double>(C_)),
@@ -191,6 +167,104 @@ void Stage::build_weights(uint64_t seed_model, uint64_t seed_context) {
   freq_.alloc(fr.size() * 8);
   BP_CUDA(cudaMemcpyAsync(freq_.p, fr.data(), fr.size() * 8, cudaMemcpyHostToDevice, st));
   BP_CUDA(cudaStreamSynchronize(st));
+}
+
+// Cross-attention K|V of the context, hoisted out of the per-pass loop
+// (model.cpp:216-217 recomputes ctx@Ck, ctx@Cv every pass; it is constant).
+// Ck/Cv are re-drawn from (seed, layer, role) so they need not stay resident.
+void Stage::hoist_context(const double* ctx64) {
+  const size_t te = prec_ == BP_PREC_F64 ? 8 : 4;
+  const int64_t H = h_;
+  const size_t hh = static_cast<size_t>(h_) * h_;
+  DevBuf gen, ctxT, ckvT, kvT;
+  gen.alloc(std::max(hh, static_cast<size_t>(Lc_) * 2 * h_) * 8);
+  ctxT.alloc(static_cast<size_t>(Lc_) * h_ * te);
+  ckvT.alloc(2 * hh * te);
+  kvT.alloc(static_cast<size_t>(Lc_) * 2 * h_ * te);
+  double* g = gen.as<double>();
+  cudaStream_t st = stream_;
+  if (prec_ == BP_PREC_F64) launch_place<double>(ctx64, Lc_, h_, ctxT.as<double>(), h_, 0, st);
+  else launch_place<float>(ctx64, Lc_, h_, ctxT.as<float>(), h_, 0, st);
+  for (int l = 0; l < end_ - begin_; ++l) {
+    const LayerW& w = lw_[static_cast<size_t>(l)];
+    for (uint64_t r = kCk; r <= kCv; ++r) {
+      launch_normal_fill(derive_seed2(seed_model_, static_cast<uint64_t>(begin_ + l), r), H * H,
+                         1.0 / std::sqrt(static_cast<double>(H)), g, st);
+      const int64_t off = static_cast<int64_t>(r - kCk) * H;
+      if (prec_ == BP_PREC_F64) launch_place<double>(g, H, H, ckvT.as<double>() + off, 2 * H, 0, st);
+      else launch_place<float>(g, H, H, ckvT.as<float>() + off, 2 * H, 0, st);
+    }
+    if (prec_ == BP_PREC_F64) {
+      launch_matmul<double>(ctxT.as<double>(), H, ckvT.as<double>(), 2 * H, Lc_, 2 * h_, h_,
+                            static_cast<double*>(w.ctx_kv), 2 * H, kEpiNone, nullptr, 0, st);
+    } else if (prec_ == BP_PREC_F32) {
+      launch_matmul<float>(ctxT.as<float>(), H, ckvT.as<float>(), 2 * H, Lc_, 2 * h_, h_,
+                           static_cast<float*>(w.ctx_kv), 2 * H, kEpiNone, nullptr, 0, st);
+    } else {
+      launch_matmul<float>(ctxT.as<float>(), H, ckvT.as<float>(), 2 * H, Lc_, 2 * h_, h_, kvT.as<float>(), 2 * H,
+                           kEpiNone, nullptr, 0, st);
+      launch_convert<float, double>(kvT.as<float>(), g, static_cast<int64_t>(Lc_) * 2 * H, st);
+      launch_place<bf16>(g, Lc_, 2 * H, static_cast<bf16*>(w.ctx_kv), 2 * H, 0, st);
+    }
+  }
+  BP_CUDA(cudaStreamSynchronize(st));
+}
+
+void Stage::set_context(const double* host, int64_t rows, int64_t cols) {
+  if (rows != Lc_ || cols != h_) fail(BP_ERR_DIMENSION, "context must be [context_len, hidden]");
+  BP_CUDA(cudaSetDevice(device_));
+  DevBuf d;
+  d.alloc(static_cast<size_t>(rows * cols) * 8);
+  BP_CUDA(cudaMemcpyAsync(d.p, host, static_cast<size_t>(rows * cols) * 8, cudaMemcpyHostToDevice, stream_));
+  hoist_context(d.as<double>());
+}
+
+// Host-provided prefix (reference KVCacheEntry / RecomputeEntry passed by the
+// caller): fp64 on the device -> this stage's dtype, layer-major.
+void Stage::load_host_prefix(int kind, const double* k64, const double* v64, int64_t rows) {
+  const int nl = end_ - begin_;
+  const size_t eb = prec_ == BP_PREC_F64 ? 8 : (prec_ == BP_PREC_F32 ? 4 : 2);
+  const int64_t H = h_;
+  host_rows_ = rows;
+  host_kind_ = kind;
+  if (kind == 3) {  // K|V per layer [rows][2h]
+    hostpre_.reserve(static_cast<size_t>(nl) * rows * 2 * H * eb + 16);
+    for (int l = 0; l < nl; ++l) {
+      const int64_t base = static_cast<int64_t>(l) * rows * 2 * H;
+      for (int kv = 0; kv < 2; ++kv) {
+        const double* src = (kv ? v64 : k64) + static_cast<int64_t>(l) * rows * H;
+        if (prec_ == BP_PREC_F64) launch_place<double>(src, rows, H, hostpre_.as<double>() + base + kv * H, 2 * H, 0, stream_);
+        else if (prec_ == BP_PREC_F32) launch_place<float>(src, rows, H, hostpre_.as<float>() + base + kv * H, 2 * H, 0, stream_);
+        else launch_place<bf16>(src, rows, H, hostpre_.as<bf16>() + base + kv * H, 2 * H, 0, stream_);
+      }
+    }
+  } else {  // recorded layer inputs [rows][h] (fp32 on the bf16 path)
+    const size_t xb = prec_ == BP_PREC_F64 ? 8 : 4;
+    hostpre_.reserve(static_cast<size_t>(nl) * rows * H * xb + 16);
+    if (prec_ == BP_PREC_F64) launch_place<double>(k64, nl * rows, H, hostpre_.as<double>(), H, 0, stream_);
+    else launch_place<float>(k64, nl * rows, H, hostpre_.as<float>(), H, 0, stream_);
+  }
+  if (rows > cap_capture_) {
+    kvp_.alloc(static_cast<size_t>(rows) * 2 * H * (prec_ == BP_PREC_BF16 ? 2 : eb));
+    lnp_.alloc(static_cast<size_t>(rows) * H * (prec_ == BP_PREC_BF16 ? 2 : eb));
+    cap_capture_ = rows;
+  }
+}
+
+void Stage::recorded_rows(int layer, double* host_out) {
+  if (!rec_.valid) fail(BP_ERR_CACHE, "no resident recording");
+  if (layer < 0 || layer >= end_ - begin_) fail(BP_ERR_DIMENSION, "layer out of range");
+  const int64_t n = rec_.tokens * h_;
+  DevBuf d64;
+  d64.alloc(static_cast<size_t>(n) * 8);
+  if (prec_ == BP_PREC_F64) {
+    BP_CUDA(cudaMemcpyAsync(d64.p, rec_.rec[static_cast<size_t>(layer)], static_cast<size_t>(n) * 8,
+                            cudaMemcpyDeviceToDevice, stream_));
+  } else {
+    launch_convert<float, double>(static_cast<const float*>(rec_.rec[static_cast<size_t>(layer)]), d64.as<double>(), n, stream_);
+  }
+  BP_CUDA(cudaMemcpyAsync(host_out, d64.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, stream_));
+  BP_CUDA(cudaStreamSynchronize(stream_));
 }
 
 void Stage::ensure_workspace(int64_t tokens, int64_t capture) {
@@ -253,6 +327,8 @@ const void* Stage::forward(const StageInput& in) {
     fail(BP_ERR_CACHE, "cache supplied while caching is disabled");  // model.cpp:269-271
   if (in.use_prev == 1 && !cache_.valid) fail(BP_ERR_CACHE, "no resident captured K/V on this stage");
   if (in.use_prev == 2 && !rec_.valid) fail(BP_ERR_CACHE, "no resident recorded inputs on this stage");
+  if ((in.use_prev == 3 || in.use_prev == 4) && host_kind_ != in.use_prev)
+    fail(BP_ERR_CACHE, "host prefix not loaded");
   for (int f : in.capture_frames)
     if (f < 0 || f >= in.nframes) fail(BP_ERR_DIMENSION, "capture frame out of range");
   switch (prec_) {
@@ -314,6 +390,17 @@ const void* Stage::forward_simt(const StageInput& in) {
       a.v0 = kvp_.as<T>() + H;
       a.ldk0 = a.ldv0 = 2 * H;
       a.n0 = rec_.tokens;
+    } else if (in.use_prev == 3) {
+      a.k0 = hostpre_.as<T>() + static_cast<int64_t>(li) * host_rows_ * 2 * H;
+      a.v0 = a.k0 + H;
+      a.ldk0 = a.ldv0 = 2 * H;
+      a.n0 = host_rows_;
+    } else if (in.use_prev == 4) {
+      kv_prefix_from_recording(li, hostpre_.as<T>() + static_cast<int64_t>(li) * host_rows_ * H, host_rows_, kvp_.p);
+      a.k0 = kvp_.as<T>();
+      a.v0 = kvp_.as<T>() + H;
+      a.ldk0 = a.ldv0 = 2 * H;
+      a.n0 = host_rows_;
     }
     launch_matmul<T>(ln, H, static_cast<const T*>(w.wqkv), 3 * H, static_cast<int>(S), 3 * h_, h_, qkv,
                      3 * H, kEpiNone, nullptr, 0, st);
@@ -430,6 +517,17 @@ const void* Stage::forward_bf16(const StageInput& in) {
       a.v0 = kvp_.as<bf16>() + H;
       a.ldk0 = a.ldv0 = 2 * H;
       a.n0 = rec_.tokens;
+    } else if (in.use_prev == 3) {
+      a.k0 = hostpre_.as<bf16>() + static_cast<int64_t>(li) * host_rows_ * 2 * H;
+      a.v0 = a.k0 + H;
+      a.ldk0 = a.ldv0 = 2 * H;
+      a.n0 = host_rows_;
+    } else if (in.use_prev == 4) {
+      kv_prefix_from_recording(li, hostpre_.as<float>() + static_cast<int64_t>(li) * host_rows_ * H, host_rows_, kvp_.p);
+      a.k0 = kvp_.as<bf16>();
+      a.v0 = kvp_.as<bf16>() + H;
+      a.ldk0 = a.ldv0 = 2 * H;
+      a.n0 = host_rows_;
     }
     prof_mark(2, true);
     launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.wqkv), static_cast<int>(S), 3 * h_, h_, qkv, 3 * H,

@@ -59,6 +59,12 @@ class Stage {
   void bump_ulp(int layer, int which, int64_t index);
   std::string audit();  // cache_mismatch_report (model.cpp:171-199)
 
+  void set_context(const double* host, int64_t rows, int64_t cols);
+  // use_prev 3 (host K|V) / 4 (host recorded inputs), fp64 device arrays, layer-major
+  void load_host_prefix(int kind, const double* k64, const double* v64, int64_t rows);
+  void recorded_rows(int layer, double* host_out);
+  int64_t rec_tokens() const { return rec_.tokens; }
+
   // Per-kernel-class device timing with CUDA events on this stage's stream:
   // class 0 self-attention, 1 cross-attention, 2 GEMMs.
   void set_profiling(bool on) { prof_on_ = on; }
@@ -94,6 +100,11 @@ class Stage {
   template <typename T> const void* forward_simt(const StageInput& in);
   const void* forward_bf16(const StageInput& in);
   void build_weights(uint64_t seed_model, uint64_t seed_context);
+  void hoist_context(const double* ctx64_device);
+  uint64_t seed_model_ = 0;
+  DevBuf hostpre_;
+  int64_t host_rows_ = 0;
+  int host_kind_ = 0;
   void ensure_workspace(int64_t tokens, int64_t capture_tokens);
   void kv_prefix_from_recording(int li, const void* rec_rows, int64_t rows, void* kv_out);
 
