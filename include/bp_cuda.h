@@ -187,6 +187,20 @@ int32_t bp_schedule_snapshot(const bp_schedule* s, int64_t i, int64_t* round, in
 int64_t bp_schedule_nblocks(const bp_schedule* s);
 int32_t bp_schedule_block(const bp_schedule* s, int64_t i, int64_t* block_id, int64_t* frames,
                           int32_t* noise_ids, int64_t* frame_ids);
+/* One rank's ordered program for the NCCL pipeline (2 int64 per op: kind,
+ * pass): kind 0 = stage forward (+ send downstream), kind 1 = rank 0's eps
+ * receive + Euler update. Returns the op count; out may be NULL. */
+int64_t bp_schedule_rank_program(const bp_schedule* s, int32_t rank, int64_t* out, int64_t cap);
+/* Pass record i (issue order), 20 int64: round, block, level, version, ctx
+ * source (0 none, 1 in-queue, 2 retained), ctx block, ctx frames, ctx version,
+ * ctx first frame, centre frames, tokens, centre tokens, cached-context id (-1),
+ * capture count, earliest slot, slot on device 0, completion slot,
+ * finishes-block, phase, frame count; plus per-frame levels / ids and the
+ * capture frame positions. Returns the frame count. */
+int32_t bp_schedule_pass(const bp_schedule* s, int64_t i, int64_t* rec, int32_t* levels, int64_t* frame_ids,
+                         int32_t* capture);
+/* Block meta by id: frames, append round, fresh (0/1), fresh RNG state bits. */
+void bp_schedule_block_meta(const bp_schedule* s, int64_t block_id, int64_t* rec4);
 /* Stage layer ranges actually used: begins[N], ends[N]. */
 void bp_schedule_partition(const bp_schedule* s, int32_t* begins, int32_t* ends);
 

@@ -106,6 +106,9 @@ _SIGS = {
     "bp_schedule_nblocks": (i64, [C.c_void_p]),
     "bp_schedule_block": (i32, [C.c_void_p, i64, P(i64), P(i64), P(i32), P(i64)]),
     "bp_schedule_partition": (None, [C.c_void_p, P(i32), P(i32)]),
+    "bp_schedule_rank_program": (i64, [C.c_void_p, i32, P(i64), i64]),
+    "bp_schedule_pass": (i32, [C.c_void_p, i64, P(i64), P(i32), P(i64), P(i32)]),
+    "bp_schedule_block_meta": (None, [C.c_void_p, i64, P(i64)]),
     "bp_nccl_unique_id": (i32, [P(C.c_uint8)]),
     "bp_pipeline_create": (i32, [P(PipelineDesc), i32, i32, i32, P(C.c_uint8), P(C.c_void_p)]),
     "bp_pipeline_destroy": (i32, [C.c_void_p]),

@@ -178,6 +178,37 @@ class Schedule:
         lib.bp_schedule_partition(h, b, e)
         self.partition = [(b[j], e[j]) for j in range(self.cfg.devices)]
 
+    PASS_FIELDS = ("round", "block", "level", "version", "ctx", "ctx_block", "ctx_frames", "ctx_version",
+                   "ctx_first_frame", "center_frames", "tokens", "center_tokens", "cached_context_id",
+                   "ncapture", "earliest", "slot0", "completion", "finishes_block", "phase", "nframes")
+
+    def rank_program(self, rank: int) -> List[tuple]:
+        """The ordered ops the NCCL executor issues on `rank`: (kind, pass),
+        kind 0 = stage forward (+ send), 1 = rank-0 eps receive + update."""
+        n = int(lib.bp_schedule_rank_program(self._h, rank, None, 0))
+        out = np.zeros(2 * max(n, 1), dtype=np.int64)
+        lib.bp_schedule_rank_program(self._h, rank, _ptr(out, i64), n)
+        return [(int(out[2 * k]), int(out[2 * k + 1])) for k in range(n)]
+
+    def pass_record(self, i: int) -> Dict[str, Any]:
+        rec = np.zeros(20, dtype=np.int64)
+        lib.bp_schedule_pass(self._h, i, _ptr(rec, i64), None, None, None)
+        d = dict(zip(self.PASS_FIELDS, rec.tolist()))
+        lv = np.zeros(max(d["nframes"], 1), dtype=np.int32)
+        fi = np.zeros(max(d["nframes"], 1), dtype=np.int64)
+        cp = np.zeros(max(d["ncapture"], 1), dtype=np.int32)
+        lib.bp_schedule_pass(self._h, i, _ptr(rec, i64), _ptr(lv, i32), _ptr(fi, i64), _ptr(cp, i32))
+        d["frame_levels"] = lv[:d["nframes"]].tolist()
+        d["frame_ids"] = fi[:d["nframes"]].tolist()
+        d["capture_frames"] = cp[:d["ncapture"]].tolist()
+        return d
+
+    def block_meta(self, block_id: int) -> Dict[str, Any]:
+        rec = np.zeros(4, dtype=np.int64)
+        lib.bp_schedule_block_meta(self._h, block_id, _ptr(rec, i64))
+        return {"frames": int(rec[0]), "append_round": int(rec[1]), "fresh": bool(rec[2]),
+                "fresh_state": int(rec[3]) & ((1 << 64) - 1)}
+
     def __del__(self):
         try:
             if self._h:

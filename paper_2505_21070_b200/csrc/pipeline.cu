@@ -425,14 +425,8 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
 
   if (j == 0) {
     build_pool_and_check(st_);
-    // merge stage-0 passes and eps updates by logical time
-    struct Op { double t; int kind; int64_t pass; };
-    std::vector<Op> ops;
-    for (const SchedPass& p : sched.passes) {
-      ops.push_back({static_cast<double>(p.slots[0]), 0, p.index});
-      ops.push_back({static_cast<double>(p.completion) + 0.5, 1, p.index});
-    }
-    std::stable_sort(ops.begin(), ops.end(), [](const Op& a, const Op& b) { return a.t < b.t; });
+    // stage-0 passes and eps updates merged by the logical slot clock
+    const std::vector<RankOp> ops = rank_program(sched, 0);
     // eps receives are posted in pass order; receive i reuses the ring slot
     // of receive i-2, so it is posted right after STEP(i-2) is enqueued
     // (an event must be recorded before another stream can wait on it).
@@ -446,7 +440,7 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
     post_eps_recv(0);
     post_eps_recv(1);
     size_t next_append = 0;
-    for (const Op& op : ops) {
+    for (const RankOp& op : ops) {
       const SchedPass& p = sched.passes[static_cast<size_t>(op.pass)];
       if (op.kind == 0) {
         while (next_append < sched.blocks.size() && sched.blocks[next_append].append_round <= p.round)

@@ -360,6 +360,23 @@ Schedule build_schedule(const bp_pipeline_desc& d) {
   return s;
 }
 
+std::vector<RankOp> rank_program(const Schedule& s, int rank) {
+  std::vector<RankOp> ops;
+  if (rank != 0) {
+    for (const SchedPass& p : s.passes) ops.push_back({0, p.index});
+    return ops;
+  }
+  struct Timed { double t; RankOp op; };
+  std::vector<Timed> v;
+  for (const SchedPass& p : s.passes) {
+    v.push_back({static_cast<double>(p.slots[0]), {0, p.index}});
+    v.push_back({static_cast<double>(p.completion) + 0.5, {1, p.index}});
+  }
+  std::stable_sort(v.begin(), v.end(), [](const Timed& a, const Timed& b) { return a.t < b.t; });
+  for (const Timed& t : v) ops.push_back(t.op);
+  return ops;
+}
+
 }  // namespace bp
 
 // ---- C-ABI accessors ---------------------------------------------------------
@@ -425,6 +442,41 @@ int32_t bp_schedule_block(const bp_schedule* s, int64_t i, int64_t* block_id, in
     if (frame_ids) frame_ids[k] = b.frame_ids[k];
   return static_cast<int32_t>(b.noise_ids.size());
 }
+int64_t bp_schedule_rank_program(const bp_schedule* s, int32_t rank, int64_t* out, int64_t cap) {
+  const std::vector<bp::RankOp> ops = bp::rank_program(s->s, rank);
+  for (size_t i = 0; i < ops.size() && static_cast<int64_t>(i) < cap && out; ++i) {
+    out[2 * i] = ops[i].kind;
+    out[2 * i + 1] = ops[i].pass;
+  }
+  return static_cast<int64_t>(ops.size());
+}
+
+int32_t bp_schedule_pass(const bp_schedule* s, int64_t i, int64_t* rec, int32_t* levels, int64_t* frame_ids,
+                         int32_t* capture) {
+  const bp::SchedPass& p = s->s.passes[static_cast<size_t>(i)];
+  const int64_t v[20] = {p.round, p.block, p.level, p.version, static_cast<int64_t>(p.ctx), p.ctx_block,
+                         p.ctx_frames, p.ctx_version, p.ctx_first_frame, p.center_frames, p.tokens,
+                         p.center_tokens, p.cached_context_id, static_cast<int64_t>(p.capture_frames.size()),
+                         p.earliest, p.slots.empty() ? 0 : p.slots[0], p.completion, p.finishes_block ? 1 : 0,
+                         p.phase, static_cast<int64_t>(p.frame_levels.size())};
+  if (rec) std::memcpy(rec, v, sizeof(v));
+  for (size_t k = 0; k < p.frame_levels.size(); ++k) {
+    if (levels) levels[k] = p.frame_levels[k];
+    if (frame_ids) frame_ids[k] = p.frame_ids[k];
+  }
+  for (size_t k = 0; k < p.capture_frames.size(); ++k)
+    if (capture) capture[k] = p.capture_frames[k];
+  return static_cast<int32_t>(p.frame_levels.size());
+}
+
+void bp_schedule_block_meta(const bp_schedule* s, int64_t block_id, int64_t* rec4) {
+  const bp::SchedBlock& b = s->s.blocks[static_cast<size_t>(block_id - 1)];
+  rec4[0] = b.frames;
+  rec4[1] = b.append_round;
+  rec4[2] = b.fresh ? 1 : 0;
+  rec4[3] = static_cast<int64_t>(b.fresh_state);
+}
+
 void bp_schedule_partition(const bp_schedule* s, int32_t* begins, int32_t* ends) {
   for (size_t j = 0; j < s->s.begins.size(); ++j) {
     begins[j] = s->s.begins[j];

@@ -78,6 +78,18 @@ struct Schedule {
   std::vector<SchedSnapshot> snapshots;
 };
 
+// One rank's ordered program for the one-process-per-GPU pipeline:
+// kind 0 = stage forward of a pass (rank 0 also appends due blocks and
+// assembles the payload; every rank then sends its output downstream),
+// kind 1 = rank 0 receives a pass's eps and applies the Euler update.
+// Rank 0 merges both kinds by the logical slot clock (forward at slot_0(p),
+// update at completion(p) + 0.5); other ranks run forwards in pass order.
+struct RankOp {
+  int kind;
+  int64_t pass;
+};
+std::vector<RankOp> rank_program(const Schedule& s, int rank);
+
 int ffn_width(const bp_model_desc& m);
 void validate_model(const bp_model_desc& m);
 // Stage layer ranges: the reference's even split (model.cpp:134-148), or the
