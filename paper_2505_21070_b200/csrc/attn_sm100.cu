@@ -36,7 +36,7 @@ constexpr uint32_t SMEM_K = SMEM_Q + TILE;           // 2 stages
 constexpr uint32_t SMEM_V = SMEM_K + 2 * TILE;       // 2 stages
 constexpr uint32_t SMEM_P = SMEM_V + 2 * TILE;
 constexpr uint32_t SMEM_BAR = SMEM_P + TILE;
-constexpr uint32_t SMEM_BYTES = SMEM_BAR + 256 + 1024;
+constexpr uint32_t SMEM_BYTES = SMEM_BAR + 256 + 1024;  // 17 mbarriers + TMEM slot
 constexpr int kThreads = 192;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P values up to 2^8 before O is rescaled
 
@@ -48,6 +48,17 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA pipe for x <= 8: round-to-integer via the 1.5*2^23 trick,
+// degree-3 minimax polynomial for 2^f on [-0.5, 0.5] (rel. error ~1e-4, far
+// below the bf16 rounding of P), exponent added with an integer shift.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float j = x + 12582912.f;
+  const float f = x - (j - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.0555041086f, f, 0.2402264923f), f, 0.6931471806f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -62,13 +73,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;    // [2]
-  uint64_t* kv_empty = bars + 3;   // [2]
-  uint64_t* s_full = bars + 5;     // [2]
-  uint64_t* s_free = bars + 7;     // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* pv_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* k_full = bars + 1;     // [2] K ring: freed once S_j is computed
+  uint64_t* k_empty = bars + 3;    // [2]
+  uint64_t* v_full = bars + 5;     // [2] V ring: freed once PV_j is computed
+  uint64_t* v_empty = bars + 7;    // [2]
+  uint64_t* s_full = bars + 9;     // [2]
+  uint64_t* s_free = bars + 11;    // [2]
+  uint64_t* p_full = bars + 13;
+  uint64_t* pv_done = bars + 14;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qtile = blockIdx.x, head = blockIdx.y;
@@ -82,8 +95,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tma_prefetch(&maps.v1);
     tc::mbar_init(q_full, 1);
     for (int s = 0; s < 2; ++s) {
-      tc::mbar_init(&kv_full[s], 1);
-      tc::mbar_init(&kv_empty[s], 1);
+      tc::mbar_init(&k_full[s], 1);
+      tc::mbar_init(&k_empty[s], 1);
+      tc::mbar_init(&v_full[s], 1);
+      tc::mbar_init(&v_empty[s], 1);
       tc::mbar_init(&s_full[s], 1);
       tc::mbar_init(&s_free[s], 128);
     }
@@ -99,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_o = tmem + 256;
 
   if (warp == 0) {
-    // ---- TMA producer -----------------------------------------------------------------
+    // ---- TMA producer: Q, then K_j / V_j into their own 2-stage rings ------------------
     if (lane == 0) {
       tc::mbar_arrive_expect_tx(q_full, TILE);
       tc::tma_load_2d(smem + SMEM_Q, &maps.q, q_full, head * kDh, qtile * BQ);
@@ -107,30 +122,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int j = 0; j < T; ++j) {
       const int s = j & 1;
-      tc::mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+      const uint32_t ph = ((j >> 1) & 1) ^ 1;
+      const bool seg0 = j < t0;
+      const int row0 = (seg0 ? j : j - t0) * BKV;
+      tc::mbar_wait(&k_empty[s], ph);
       if (lane == 0) {
-        const bool seg0 = j < t0;
         const CUtensorMap* mk = seg0 ? &maps.k0 : &maps.k1;
-        const CUtensorMap* mv = seg0 ? &maps.v0 : &maps.v1;
-        const int row0 = (seg0 ? j : j - t0) * BKV;
-        tc::mbar_arrive_expect_tx(&kv_full[s], 2 * TILE);
         uint8_t* kd = smem + SMEM_K + s * TILE;
+        tc::mbar_arrive_expect_tx(&k_full[s], TILE);
+        tc::tma_load_2d(kd, mk, &k_full[s], head * kDh, row0);
+        tc::tma_load_2d(kd + HALF, mk, &k_full[s], head * kDh + 64, row0);
+      }
+      __syncwarp();
+      tc::mbar_wait(&v_empty[s], ph);
+      if (lane == 0) {
+        const CUtensorMap* mv = seg0 ? &maps.v0 : &maps.v1;
         uint8_t* vd = smem + SMEM_V + s * TILE;
-        tc::tma_load_2d(kd, mk, &kv_full[s], head * kDh, row0);
-        tc::tma_load_2d(kd + HALF, mk, &kv_full[s], head * kDh + 64, row0);
-        tc::tma_load_2d(vd, mv, &kv_full[s], head * kDh, row0);
-        tc::tma_load_2d(vd + HALF, mv, &kv_full[s], head * kDh + 64, row0);
+        tc::mbar_arrive_expect_tx(&v_full[s], TILE);
+        tc::tma_load_2d(vd, mv, &v_full[s], head * kDh, row0);
+        tc::tma_load_2d(vd + HALF, mv, &v_full[s], head * kDh + 64, row0);
       }
       __syncwarp();
     }
   } else if (warp == 1) {
-    // ---- MMA issuer -------------------------------------------------------------------
+    // ---- MMA issuer: S_0, S_1, PV_0, S_2, PV_1, ... ----------------------------------------
     constexpr uint32_t idesc_s = tc::idesc_bf16(BQ, BKV, 0, 0);   // Q (K-major) x K^T (K-major)
     constexpr uint32_t idesc_o = tc::idesc_bf16(BQ, kDh, 0, 1);   // P (K-major) x V (MN-major)
     const uint32_t q_addr = tc::smem_u32(smem + SMEM_Q);
     const uint32_t p_addr = tc::smem_u32(smem + SMEM_P);
     tc::mbar_wait(q_full, 0);
     auto issue_pv = [&](int jj) {
+      tc::mbar_wait(&v_full[jj & 1], (jj >> 1) & 1);
       tc::mbar_wait(p_full, jj & 1);
       tc::fence_after_sync();
       if (lane == 0) {
@@ -143,13 +165,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::mma_bf16(tmem_o, ad, bd, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit(pv_done);
-        tc::mma_commit(&kv_empty[jj & 1]);
+        tc::mma_commit(&v_empty[jj & 1]);
       }
       __syncwarp();
     };
     for (int j = 0; j < T; ++j) {
       const int s = j & 1;
-      tc::mbar_wait(&kv_full[s], (j >> 1) & 1);
+      tc::mbar_wait(&k_full[s], (j >> 1) & 1);
       tc::mbar_wait(&s_free[s], ((j >> 1) & 1) ^ 1);
       tc::fence_after_sync();
       if (lane == 0) {
@@ -162,6 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                        idesc_s, kk > 0 ? 1u : 0u);
         }
         tc::mma_commit(&s_full[s]);
+        tc::mma_commit(&k_empty[s]);
       }
       __syncwarp();
       if (j >= 1) issue_pv(j - 1);
@@ -190,26 +213,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tmem_ld_wait();
       tc::fence_before_sync();
       tc::mbar_arrive(&s_free[s]);
-      float mx = -INFINITY;
+      if (valid < BKV) {  // keys past the segment end (only a segment's last tile)
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        const float v = c < valid ? __uint_as_float(sr[c]) * scale_log2 : -INFINITY;
-        sr[c] = __float_as_uint(v);
-        mx = fmaxf(mx, v);
+        for (int c = 0; c < 128; ++c)
+          if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
       }
+      // raw row max (scale > 0 commutes with max), four chains for ILP
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 128; ++c) m4[c & 3] = fmaxf(m4[c & 3], __uint_as_float(sr[c]));
+      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
       const bool need = mx > m_used + kRescaleThreshold;
       const float m_new = need ? mx : m_used;
       const float corr = need ? ex2(m_used - m_new) : 1.f;  // 0 on the first tile
+      const float neg_m = -m_new;
       uint32_t pk[64];
-      float ls = 0.f;
+      float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
       for (int c = 0; c < 64; ++c) {
-        const float p0 = ex2(__uint_as_float(sr[2 * c]) - m_new);
-        const float p1 = ex2(__uint_as_float(sr[2 * c + 1]) - m_new);
-        ls += p0 + p1;
+        const float x0 = fmaf(__uint_as_float(sr[2 * c]), scale_log2, neg_m);
+        const float x1 = fmaf(__uint_as_float(sr[2 * c + 1]), scale_log2, neg_m);
+        // 1 pair in 8 on the FMA pipe, the rest on MUFU (balances the two pipes)
+        const float p0 = (c & 7) == 7 ? ex2_poly(x0) : ex2(x0);
+        const float p1 = (c & 7) == 7 ? ex2_poly(x1) : ex2(x1);
+        ls0 += p0;
+        ls1 += p1;
         pk[c] = pack_bf16(p0, p1);
       }
-      l = l * corr + ls;
+      l = l * corr + (ls0 + ls1);
       m_used = m_new;
       // P buffer and O are free once PV_{j-1} completed
       if (j >= 1) {
@@ -230,13 +261,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       // P row -> smem, K-major SW128: 16-byte chunk c of row r at (c ^ (r & 7))
+      const uint32_t p_row = tc::smem_u32(p_smem) + static_cast<uint32_t>(r * 128);
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         const int half = c >> 3, ch = c & 7;
-        uint4* dst = reinterpret_cast<uint4*>(p_smem + half * HALF + r * 128 + ((ch ^ (r & 7)) << 4));
-        *dst = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        tc::st_shared_v4(p_row + half * HALF + ((ch ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
+                         pk[4 * c + 3]);
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc::fence_proxy_async_smem();
       tc::fence_before_sync();
       tc::mbar_arrive(p_full);
     }
