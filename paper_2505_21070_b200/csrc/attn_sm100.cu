@@ -29,16 +29,20 @@ void launch_attn_simt(const AttnBf16Args& a, int64_t rows, cudaStream_t st);
 namespace {
 
 constexpr int kDh = 128, BQ = 128, BKV = 128;
-constexpr uint32_t HALF = 128 * 64 * 2;      // [128 rows][64 bf16] swizzled box
+constexpr uint32_t HALF = 128 * 64 * 2;      // [128 rows][64 bf16] swizzled TMA box
 constexpr uint32_t TILE = 2 * HALF;          // 32 KB
+constexpr int KST = 3;                       // K ring depth
+constexpr int VST = 3;                       // V ring depth
 constexpr uint32_t SMEM_Q = 0;
-constexpr uint32_t SMEM_K = SMEM_Q + TILE;           // 2 stages
-constexpr uint32_t SMEM_V = SMEM_K + 2 * TILE;       // 2 stages
-constexpr uint32_t SMEM_P = SMEM_V + 2 * TILE;
-constexpr uint32_t SMEM_BAR = SMEM_P + TILE;
-constexpr uint32_t SMEM_BYTES = SMEM_BAR + 256 + 1024;  // 17 mbarriers + TMEM slot
-constexpr int kThreads = 192;
+constexpr uint32_t SMEM_K = SMEM_Q + TILE;
+constexpr uint32_t SMEM_V = SMEM_K + KST * TILE;
+constexpr uint32_t SMEM_BAR = SMEM_V + VST * TILE;
+constexpr uint32_t SMEM_BYTES = SMEM_BAR + 256 + 1024;  // mbarriers + TMEM slot + alignment
+constexpr int kThreads = 192;  // TMA warp, MMA warp, 4 softmax warps
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P values up to 2^8 before O is rescaled
+// TMEM columns: S_0 [0,128), S_1 [128,256) (P_j overwrites the first 64
+// columns of S_j as packed bf16 pairs), O [256,384), Q [384,448).
+constexpr uint32_t TM_O = 256, TM_Q = 384;
 
 struct AttnMaps {
   CUtensorMap q, k0, v0, k1, v1;
@@ -66,22 +70,26 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Shared-memory traffic is the binding budget for attention (each SMEM-SMEM
+// 128x128x16 MMA reads 8 KB in 64 cycles): both MMAs therefore take their A
+// operand from TMEM (Q staged once; P written by the softmax over its S
+// buffer) and only K / V stream through shared memory.
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_tc(const __grid_constant__ AttnMaps maps, int64_t rows, int64_t n0, int64_t n1, float scale_log2,
               bf16* __restrict__ out, int64_t ldo) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;     // [2] K ring: freed once S_j is computed
-  uint64_t* k_empty = bars + 3;    // [2]
-  uint64_t* v_full = bars + 5;     // [2] V ring: freed once PV_j is computed
-  uint64_t* v_empty = bars + 7;    // [2]
-  uint64_t* s_full = bars + 9;     // [2]
-  uint64_t* s_free = bars + 11;    // [2]
-  uint64_t* p_full = bars + 13;
-  uint64_t* pv_done = bars + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* q_full = bars + 0;     // Q landed in smem (TMA)
+  uint64_t* q_tmem = bars + 1;     // Q staged into TMEM (128 softmax threads)
+  uint64_t* k_full = bars + 2;     // [KST]
+  uint64_t* k_empty = bars + 5;    // [KST] freed once S_j is computed
+  uint64_t* v_full = bars + 8;     // [VST]
+  uint64_t* v_empty = bars + 11;   // [VST] freed once PV_j is computed
+  uint64_t* s_full = bars + 14;    // [2]
+  uint64_t* p_full = bars + 16;    // [2] P_j written into TMEM (also frees S_j)
+  uint64_t* pv_done = bars + 18;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qtile = blockIdx.x, head = blockIdx.y;
@@ -94,15 +102,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::tma_prefetch(&maps.k1);
     tc::tma_prefetch(&maps.v1);
     tc::mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    tc::mbar_init(q_tmem, 128);
+    for (int s = 0; s < KST; ++s) {
       tc::mbar_init(&k_full[s], 1);
       tc::mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < VST; ++s) {
       tc::mbar_init(&v_full[s], 1);
       tc::mbar_init(&v_empty[s], 1);
-      tc::mbar_init(&s_full[s], 1);
-      tc::mbar_init(&s_free[s], 128);
     }
-    tc::mbar_init(p_full, 128);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&s_full[s], 1);
+      tc::mbar_init(&p_full[s], 128);
+    }
     tc::mbar_init(pv_done, 1);
     tc::fence_barrier_init();
   }
@@ -111,91 +123,92 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_o = tmem + 256;
 
   if (warp == 0) {
-    // ---- TMA producer: Q, then K_j / V_j into their own 2-stage rings ------------------
-    if (lane == 0) {
-      tc::mbar_arrive_expect_tx(q_full, TILE);
-      tc::tma_load_2d(smem + SMEM_Q, &maps.q, q_full, head * kDh, qtile * BQ);
-      tc::tma_load_2d(smem + SMEM_Q + HALF, &maps.q, q_full, head * kDh + 64, qtile * BQ);
-    }
+    // ---- TMA producer: Q, then K_j / V_j into their rings -----------------------------
+    tc::mbar_arrive_expect_tx_elect(q_full, TILE);
+    tc::tma_load_2d_elect(smem + SMEM_Q, &maps.q, q_full, head * kDh, qtile * BQ);
+    tc::tma_load_2d_elect(smem + SMEM_Q + HALF, &maps.q, q_full, head * kDh + 64, qtile * BQ);
     for (int j = 0; j < T; ++j) {
-      const int s = j & 1;
-      const uint32_t ph = ((j >> 1) & 1) ^ 1;
       const bool seg0 = j < t0;
       const int row0 = (seg0 ? j : j - t0) * BKV;
-      tc::mbar_wait(&k_empty[s], ph);
-      if (lane == 0) {
-        const CUtensorMap* mk = seg0 ? &maps.k0 : &maps.k1;
-        uint8_t* kd = smem + SMEM_K + s * TILE;
-        tc::mbar_arrive_expect_tx(&k_full[s], TILE);
-        tc::tma_load_2d(kd, mk, &k_full[s], head * kDh, row0);
-        tc::tma_load_2d(kd + HALF, mk, &k_full[s], head * kDh + 64, row0);
-      }
-      __syncwarp();
-      tc::mbar_wait(&v_empty[s], ph);
-      if (lane == 0) {
-        const CUtensorMap* mv = seg0 ? &maps.v0 : &maps.v1;
-        uint8_t* vd = smem + SMEM_V + s * TILE;
-        tc::mbar_arrive_expect_tx(&v_full[s], TILE);
-        tc::tma_load_2d(vd, mv, &v_full[s], head * kDh, row0);
-        tc::tma_load_2d(vd + HALF, mv, &v_full[s], head * kDh + 64, row0);
-      }
-      __syncwarp();
+      const int ks = j % KST, vs = j % VST;
+      tc::mbar_wait(&k_empty[ks], ((j / KST) & 1) ^ 1);
+      uint8_t* kd = smem + SMEM_K + ks * TILE;
+      const CUtensorMap* mk = seg0 ? &maps.k0 : &maps.k1;
+      tc::mbar_arrive_expect_tx_elect(&k_full[ks], TILE);
+      tc::tma_load_2d_elect(kd, mk, &k_full[ks], head * kDh, row0);
+      tc::tma_load_2d_elect(kd + HALF, mk, &k_full[ks], head * kDh + 64, row0);
+      tc::mbar_wait(&v_empty[vs], ((j / VST) & 1) ^ 1);
+      uint8_t* vd = smem + SMEM_V + vs * TILE;
+      const CUtensorMap* mv = seg0 ? &maps.v0 : &maps.v1;
+      tc::mbar_arrive_expect_tx_elect(&v_full[vs], TILE);
+      tc::tma_load_2d_elect(vd, mv, &v_full[vs], head * kDh, row0);
+      tc::tma_load_2d_elect(vd + HALF, mv, &v_full[vs], head * kDh + 64, row0);
     }
   } else if (warp == 1) {
-    // ---- MMA issuer: S_0, S_1, PV_0, S_2, PV_1, ... ----------------------------------------
-    constexpr uint32_t idesc_s = tc::idesc_bf16(BQ, BKV, 0, 0);   // Q (K-major) x K^T (K-major)
-    constexpr uint32_t idesc_o = tc::idesc_bf16(BQ, kDh, 0, 1);   // P (K-major) x V (MN-major)
-    const uint32_t q_addr = tc::smem_u32(smem + SMEM_Q);
-    const uint32_t p_addr = tc::smem_u32(smem + SMEM_P);
-    tc::mbar_wait(q_full, 0);
+    // ---- MMA issuer: S_0, S_1, PV_0, S_2, PV_1, ... (tensor core runs them in order) ----
+    constexpr uint32_t idesc_s = tc::idesc_bf16(BQ, BKV, 0, 0);   // Q (TMEM) x K^T (smem, K-major)
+    constexpr uint32_t idesc_o = tc::idesc_bf16(BQ, kDh, 0, 1);   // P (TMEM) x V (smem, MN-major)
+    tc::mbar_wait(q_tmem, 0);
+    tc::fence_after_sync();
     auto issue_pv = [&](int jj) {
-      tc::mbar_wait(&v_full[jj & 1], (jj >> 1) & 1);
-      tc::mbar_wait(p_full, jj & 1);
+      const int vs = jj % VST;
+      tc::mbar_wait(&v_full[vs], (jj / VST) & 1);
+      tc::mbar_wait(&p_full[jj & 1], (jj >> 1) & 1);
       tc::fence_after_sync();
-      if (lane == 0) {
-        const uint32_t v_addr = tc::smem_u32(smem + SMEM_V + (jj & 1) * TILE);
+      const uint32_t v_addr = tc::smem_u32(smem + SMEM_V + vs * TILE);
+      const uint32_t p_tm = tmem + static_cast<uint32_t>((jj & 1) * BKV);
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint64_t ad = tc::desc_sw128(p_addr + (kk >> 2) * HALF + (kk & 3) * 32, 1024, 16);
-          // V tile [keys][d]: MN-major (d contiguous); 16 keys = two 8-row groups
-          const uint64_t bd = tc::desc_sw128(v_addr + kk * 2048, 1024, HALF);
-          tc::mma_bf16(tmem_o, ad, bd, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc::mma_commit(pv_done);
-        tc::mma_commit(&v_empty[jj & 1]);
+      for (int kk = 0; kk < BKV / 16; ++kk) {
+        // V tile [keys][d]: MN-major (d contiguous); 16 keys = two 8-row groups
+        const uint64_t bd = tc::desc_sw128(v_addr + kk * 2048, 1024, HALF);
+        tc::mma_bf16_ts_elect(tmem + TM_O, p_tm + kk * 8, bd, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
       }
-      __syncwarp();
+      tc::mma_commit_elect(pv_done);
+      tc::mma_commit_elect(&v_empty[vs]);
     };
     for (int j = 0; j < T; ++j) {
-      const int s = j & 1;
-      tc::mbar_wait(&k_full[s], (j >> 1) & 1);
-      tc::mbar_wait(&s_free[s], ((j >> 1) & 1) ^ 1);
+      const int ks = j % KST;
+      tc::mbar_wait(&k_full[ks], (j / KST) & 1);
+      if (j >= 2) tc::mbar_wait(&p_full[j & 1], ((j >> 1) - 1) & 1);  // S_{j-2} buffer consumed
       tc::fence_after_sync();
-      if (lane == 0) {
-        const uint32_t k_addr = tc::smem_u32(smem + SMEM_K + s * TILE);
-        const uint32_t d = tmem + static_cast<uint32_t>(s * BKV);
+      const uint32_t k_addr = tc::smem_u32(smem + SMEM_K + ks * TILE);
+      const uint32_t d = tmem + static_cast<uint32_t>((j & 1) * BKV);
 #pragma unroll
-        for (int kk = 0; kk < kDh / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
-          tc::mma_bf16(d, tc::desc_sw128(q_addr + off, 1024, 16), tc::desc_sw128(k_addr + off, 1024, 16),
-                       idesc_s, kk > 0 ? 1u : 0u);
-        }
-        tc::mma_commit(&s_full[s]);
-        tc::mma_commit(&k_empty[s]);
+      for (int kk = 0; kk < kDh / 16; ++kk) {
+        const uint64_t bd = tc::desc_sw128(k_addr + (kk >> 2) * HALF + (kk & 3) * 32, 1024, 16);
+        tc::mma_bf16_ts_elect(d, tmem + TM_Q + kk * 8, bd, idesc_s, kk > 0 ? 1u : 0u);
       }
-      __syncwarp();
+      tc::mma_commit_elect(&s_full[j & 1]);
+      tc::mma_commit_elect(&k_empty[ks]);
       if (j >= 1) issue_pv(j - 1);
     }
     if (T >= 1) issue_pv(T - 1);
   } else {
-    // ---- softmax + epilogue: thread <-> query row ------------------------------------------
+    // ---- softmax + epilogue: thread <-> query row <-> TMEM lane ---------------------------
     const int qq = warp & 3;
-    const int r = qq * 32 + lane;  // row within the tile (= TMEM lane)
+    const int r = qq * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(qq * 32) << 16;
-    uint8_t* p_smem = smem + SMEM_P;
+    {  // stage Q row r into TMEM columns [TM_Q, TM_Q + 64): packed bf16 pairs along d
+      tc::mbar_wait(q_full, 0);
+      const uint32_t q_row = tc::smem_u32(smem + SMEM_Q) + static_cast<uint32_t>(r * 128);
+      uint32_t qa[32], qb[32];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(qa[4 * c]), "=r"(qa[4 * c + 1]), "=r"(qa[4 * c + 2]), "=r"(qa[4 * c + 3])
+                     : "r"(q_row + ((c ^ (r & 7)) << 4)));
+        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(qb[4 * c]), "=r"(qb[4 * c + 1]), "=r"(qb[4 * c + 2]), "=r"(qb[4 * c + 3])
+                     : "r"(q_row + HALF + ((c ^ (r & 7)) << 4)));
+      }
+      tc::tmem_st32(tmem + lane_off + TM_Q, qa);
+      tc::tmem_st32(tmem + lane_off + TM_Q + 32, qb);
+      tc::tmem_st_wait();
+      tc::fence_before_sync();
+      tc::mbar_arrive(q_tmem);
+    }
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < T; ++j) {
       const int s = j & 1;
@@ -203,26 +216,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t seg_n = seg0 ? n0 : n1;
       const int row0 = (seg0 ? j : j - t0) * BKV;
       const int valid = static_cast<int>(seg_n - row0 < BKV ? seg_n - row0 : BKV);
+      const uint32_t tm_s = tmem + lane_off + static_cast<uint32_t>(s * BKV);
       tc::mbar_wait(&s_full[s], (j >> 1) & 1);
       tc::fence_after_sync();
       uint32_t sr[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        tc::tmem_ld32(tmem + lane_off + static_cast<uint32_t>(s * BKV + c * 32),
-                      *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+        tc::tmem_ld32(tm_s + static_cast<uint32_t>(c * 32), *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
       tc::tmem_ld_wait();
-      tc::fence_before_sync();
-      tc::mbar_arrive(&s_free[s]);
       if (valid < BKV) {  // keys past the segment end (only a segment's last tile)
 #pragma unroll
         for (int c = 0; c < 128; ++c)
           if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
       }
-      // raw row max (scale > 0 commutes with max), four chains for ILP
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
       for (int c = 0; c < 128; ++c) m4[c & 3] = fmaxf(m4[c & 3], __uint_as_float(sr[c]));
-      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
+      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;  // scale > 0
       const bool need = mx > m_used + kRescaleThreshold;
       const float m_new = need ? mx : m_used;
       const float corr = need ? ex2(m_used - m_new) : 1.f;  // 0 on the first tile
@@ -242,35 +252,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       l = l * corr + (ls0 + ls1);
       m_used = m_new;
-      // P buffer and O are free once PV_{j-1} completed
-      if (j >= 1) {
+      // O is stable once PV_{j-1} completed; only rescales need to wait for it
+      if (j >= 1 && __any_sync(0xffffffffu, need)) {
         tc::mbar_wait(pv_done, (j - 1) & 1);
         tc::fence_after_sync();
-        if (__any_sync(0xffffffffu, need)) {
 #pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t o[32];
-            const uint32_t ta = tmem_o + lane_off + static_cast<uint32_t>(c * 32);
-            tc::tmem_ld32(ta, o);
-            tc::tmem_ld_wait();
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          const uint32_t ta = tmem + lane_off + TM_O + static_cast<uint32_t>(c * 32);
+          tc::tmem_ld32(ta, o);
+          tc::tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
-            tc::tmem_st32(ta, o);
-          }
-          tc::tmem_st_wait();
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+          tc::tmem_st32(ta, o);
         }
       }
-      // P row -> smem, K-major SW128: 16-byte chunk c of row r at (c ^ (r & 7))
-      const uint32_t p_row = tc::smem_u32(p_smem) + static_cast<uint32_t>(r * 128);
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const int half = c >> 3, ch = c & 7;
-        tc::st_shared_v4(p_row + half * HALF + ((ch ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
-                         pk[4 * c + 3]);
-      }
-      tc::fence_proxy_async_smem();
+      // P_j (bf16 pairs along keys) over the first 64 columns of S_j
+      tc::tmem_st32(tm_s, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      tc::tmem_st32(tm_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+      tc::tmem_st_wait();
       tc::fence_before_sync();
-      tc::mbar_arrive(p_full);
+      tc::mbar_arrive(&p_full[s]);
     }
     // epilogue: O / l
     if (T >= 1) {
@@ -282,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
     for (int c = 0; c < 4; ++c) {
       uint32_t o[32];
-      tc::tmem_ld32(tmem_o + lane_off + static_cast<uint32_t>(c * 32), o);
+      tc::tmem_ld32(tmem + lane_off + TM_O + static_cast<uint32_t>(c * 32), o);
       tc::tmem_ld_wait();
       if (row < rows) {
         uint4* dst = reinterpret_cast<uint4*>(out + row * ldo + head * kDh + c * 32);

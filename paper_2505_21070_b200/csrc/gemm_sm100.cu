@@ -80,12 +80,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m_blk = tile / n_tiles, n_blk = tile - m_blk * n_tiles;
       for (int kb = 0; kb < num_k; ++kb) {
         tc::mbar_wait(&empty[stage], phase ^ 1);
-        if (lane == 0) {
-          tc::mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
-          tc::tma_load_2d(sa + stage * A_BYTES, &map_a, &full[stage], kb * BK, m_blk * BM);
-          tc::tma_load_2d(sb + stage * B_BYTES, &map_b, &full[stage], kb * BK, n_blk * BN);
-        }
-        __syncwarp();
+        tc::mbar_arrive_expect_tx_elect(&full[stage], A_BYTES + B_BYTES);
+        tc::tma_load_2d_elect(sa + stage * A_BYTES, &map_a, &full[stage], kb * BK, m_blk * BM);
+        tc::tma_load_2d_elect(sb + stage * B_BYTES, &map_b, &full[stage], kb * BK, n_blk * BN);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -103,22 +100,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < num_k; ++kb) {
         tc::mbar_wait(&full[stage], phase);
         tc::fence_after_sync();
-        if (lane == 0) {
-          const uint32_t a0 = tc::smem_u32(sa + stage * A_BYTES);
-          const uint32_t b0 = tc::smem_u32(sb + stage * B_BYTES);
+        const uint32_t a0 = tc::smem_u32(sa + stage * A_BYTES);
+        const uint32_t b0 = tc::smem_u32(sb + stage * B_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = tc::desc_sw128(a0 + kk * 32, 1024, 16);
-            const uint64_t bd = tc::desc_sw128(b0 + kk * 32, 1024, 16);
-            tc::mma_bf16(d, ad, bd, idesc, (kb | kk) ? 1u : 0u);
-          }
-          tc::mma_commit(&empty[stage]);  // smem slot free once these MMAs finish
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint64_t ad = tc::desc_sw128(a0 + kk * 32, 1024, 16);
+          const uint64_t bd = tc::desc_sw128(b0 + kk * 32, 1024, 16);
+          tc::mma_bf16_ss_elect(d, ad, bd, idesc, (kb | kk) ? 1u : 0u);
         }
-        __syncwarp();
+        tc::mma_commit_elect(&empty[stage]);  // smem slot free once these MMAs finish
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (lane == 0) tc::mma_commit(&tfull[acc]);  // accumulator ready
-      __syncwarp();
+      tc::mma_commit_elect(&tfull[acc]);  // accumulator ready
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
