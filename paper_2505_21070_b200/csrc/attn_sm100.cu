@@ -3,12 +3,16 @@
 // resident in HBM) ++ current block] without concatenating them in memory
 // (model.cpp:201-211, 302-318: vcat_rows(prefix, k) then attention()).
 //
-//   warp 0      TMA producer: Q once, then K/V tiles of 128 keys into a 2-stage ring
-//   warp 1      MMA issuer: S_j = Q K_j^T (TMEM, double-buffered), O += P_{j-1} V_{j-1}
-//   warps 2..5  softmax: one thread per query row reads S from TMEM, online
-//               softmax in the log2 domain, P (bf16) -> swizzled smem; lazy
-//               rescaling of O in TMEM only when the row max grows by > 2^8;
+//   warp 0      TMA producer: Q once, then K and V tiles of 128 keys into two
+//               separate 3-deep rings (K is freed as soon as S_j is computed)
+//   warp 1      MMA issuer (warp-converged, elect-in-PTX): S_j = Q K_j^T with Q
+//               staged in TMEM, O += P_{j-1} V_{j-1} with P in TMEM; S double-buffered
+//   warps 2..5  softmax: one thread per query row stages Q into TMEM, then per
+//               tile reads S from TMEM, online softmax in the log2 domain (1/8
+//               of exp2 on an FMA polynomial), writes P (bf16 pairs) over S in
+//               TMEM; O is rescaled in TMEM only when the row max grows by > 2^8;
 //               epilogue O / l -> bf16 -> global
+// Only K and V stream through shared memory (A operands come from TMEM).
 // Keys past a segment's end (a tile that straddles it) are masked; TMA
 // zero-fills the rows.
 #include <cuda.h>
