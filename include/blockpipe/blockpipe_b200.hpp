@@ -192,6 +192,10 @@ struct RunResult {
 
 RunResult run_pipeline(const PipelineConfig& cfg);
 RunResult serial_oracle(PipelineConfig cfg);
+// Extension: the RunResult the static schedule determines -- event log,
+// ledger, rounds, queue snapshots and each emitted block's ids and frame
+// shape -- without any device work (frames carry a shape but no data).
+RunResult plan_pipeline(const PipelineConfig& cfg);
 
 struct BubbleStats {
   int64_t first_slot = 0, last_slot = 0, busy_per_device = 0, idle_per_device = 0;

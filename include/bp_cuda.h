@@ -23,6 +23,13 @@
 
 #include <stdint.h>
 
+/* Only the C-ABI is exported; everything else in libbp_cuda.so is hidden. */
+#if defined(__GNUC__)
+#define BP_API __attribute__((visibility("default")))
+#else
+#define BP_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -43,8 +50,8 @@ typedef enum {
   BP_ERR_INTERNAL = 11
 } bp_status;
 
-const char* bp_last_error(void);
-const char* bp_version(void);
+BP_API const char* bp_last_error(void);
+BP_API const char* bp_version(void);
 
 /* ---- enums mirroring the reference ---------------------------------------- */
 typedef enum { BP_ORDER_REVERSE = 0, BP_ORDER_SEQUENTIAL = 1 } bp_order; /* block_queue.hpp:13 */
@@ -85,16 +92,16 @@ typedef struct {
 
 /* ---- rng.hpp ---------------------------------------------------------------- */
 /* derive_seed (rng.cpp:51-60). Host-only. */
-uint64_t bp_derive_seed(uint64_t base, const uint64_t* tags, int32_t ntags);
+BP_API uint64_t bp_derive_seed(uint64_t base, const uint64_t* tags, int32_t ntags);
 /* RandomSource(state).normal_tensor({n}, sigma) (rng.cpp:35-39) on the GPU,
  * bit-exact (glibc log/cos port). Writes n doubles; returns the final state. */
-bp_status bp_normals(int32_t device, uint64_t state, int64_t n, double sigma, double* out,
+BP_API bp_status bp_normals(int32_t device, uint64_t state, int64_t n, double sigma, double* out,
                      int32_t out_is_device, uint64_t* final_state);
 
 /* ---- noise.hpp -------------------------------------------------------------- */
 /* build_pool (noise.cpp:26-48): M = num_b + num_c/2 entries of H*W*C normals,
  * drawn on the GPU. out holds M*H*W*C doubles (entry-major). */
-bp_status bp_noise_pool(int32_t device, int32_t num_b, int32_t num_c, const int64_t frame_shape[3],
+BP_API bp_status bp_noise_pool(int32_t device, int32_t num_b, int32_t num_c, const int64_t frame_shape[3],
                         uint64_t noise_seed, double* out, int32_t out_is_device);
 
 /* ---- model.hpp: one pipeline stage (ModelChunk) -------------------------------- */
@@ -102,10 +109,10 @@ typedef struct bp_stage bp_stage;
 
 /* build_chunk (model.cpp:109-128) + build_context (model.cpp:150-153): the
  * stage's weights are generated on the device from (seed_model, layer, role). */
-bp_status bp_stage_create(int32_t device, const bp_model_desc* model, uint64_t seed_model,
+BP_API bp_status bp_stage_create(int32_t device, const bp_model_desc* model, uint64_t seed_model,
                           uint64_t seed_context, int32_t layer_begin, int32_t layer_end,
                           int32_t precision, bp_stage** out);
-bp_status bp_stage_destroy(bp_stage* stage);
+BP_API bp_status bp_stage_destroy(bp_stage* stage);
 
 /* ChunkInput (model.hpp:106-112), host fp64 payload. */
 typedef struct {
@@ -142,79 +149,89 @@ typedef struct {
 /* forward_chunk (model.cpp:227-336). The captured K/V / recorded inputs stay
  * resident on the device and replace the stage's previous entry, like
  * DeviceWorker::cache_ (engine.cpp:195-196). */
-bp_status bp_forward_chunk(bp_stage* stage, const bp_chunk_in* in, bp_chunk_out* out);
+BP_API bp_status bp_forward_chunk(bp_stage* stage, const bp_chunk_in* in, bp_chunk_out* out);
 /* Downloads the resident captured K (which=0) or V (which=1) rows of one local
  * layer as fp64 [rows, h]; out may be NULL to query rows. */
-bp_status bp_stage_cache_rows(bp_stage* stage, int32_t layer, int32_t which, double* out,
+BP_API bp_status bp_stage_cache_rows(bp_stage* stage, int32_t layer, int32_t which, double* out,
                               int64_t* rows);
 /* Downloads the resident recorded layer inputs of one local layer as fp64
  * [rows, h] (RecomputeEntry::layer_inputs); out may be NULL to query rows. */
-bp_status bp_stage_recorded_rows(bp_stage* stage, int32_t layer, double* out, int64_t* rows);
+BP_API bp_status bp_stage_recorded_rows(bp_stage* stage, int32_t layer, double* out, int64_t* rows);
 /* Replaces the cross-attention context [rows = context_len, cols = h] (host
  * fp64) and re-derives the hoisted context K/V (model.cpp:216-217). */
-bp_status bp_stage_set_context(bp_stage* stage, const double* context, int64_t rows, int64_t cols);
+BP_API bp_status bp_stage_set_context(bp_stage* stage, const double* context, int64_t rows, int64_t cols);
 /* Bumps one resident cached value by one ulp towards +inf (engine.cpp:185-189). */
-bp_status bp_stage_cache_bump_ulp(bp_stage* stage, int32_t layer, int32_t which, int64_t index);
+BP_API bp_status bp_stage_cache_bump_ulp(bp_stage* stage, int32_t layer, int32_t which, int64_t index);
 /* cache_mismatch_report (model.cpp:171-199) on the resident cache vs the
  * resident recording; report gets "" when they agree bitwise. */
-bp_status bp_stage_cache_audit(bp_stage* stage, char* report, int32_t report_len);
+BP_API bp_status bp_stage_cache_audit(bp_stage* stage, char* report, int32_t report_len);
 
 /* scheduler_step (model.cpp:338-345): out = x - eps*(1/steps), n doubles, host. */
-bp_status bp_scheduler_step(int32_t device, const double* x, const double* eps, int64_t n,
+BP_API bp_status bp_scheduler_step(int32_t device, const double* x, const double* eps, int64_t n,
                             int32_t level, int32_t steps, double* out);
+
+/* ---- tensor.hpp primitives on the GPU (fp64, host buffers, row-major) ---------- */
+/* matmul (tensor.cpp:84-109): out[m,n] = a[m,k] @ b[k,n]; ascending-k accumulation. */
+BP_API bp_status bp_matmul(int32_t device, const double* a, const double* b, int64_t m, int64_t k, int64_t n,
+                           double* out);
+/* softmax_rows (tensor.cpp:111-126) over [rows, cols]. */
+BP_API bp_status bp_softmax_rows(int32_t device, const double* x, int64_t rows, int64_t cols, double* out);
+/* layer_norm (tensor.cpp:128-146), no affine, over [rows, cols]. */
+BP_API bp_status bp_layer_norm(int32_t device, const double* x, int64_t rows, int64_t cols, double eps,
+                               double* out);
 
 /* ---- engine.hpp: static schedule (host-only; no GPU needed) -------------------- */
 typedef struct bp_schedule bp_schedule;
 /* Builds the data-independent schedule of run_pipeline (engine.cpp:255-497):
  * queue states, pass order, noise ids, logical slots, ledger. */
-bp_status bp_schedule_create(const bp_pipeline_desc* desc, bp_schedule** out);
-void bp_schedule_destroy(bp_schedule* s);
-int64_t bp_schedule_rounds(const bp_schedule* s);
-int64_t bp_schedule_npasses(const bp_schedule* s);
+BP_API bp_status bp_schedule_create(const bp_pipeline_desc* desc, bp_schedule** out);
+BP_API void bp_schedule_destroy(bp_schedule* s);
+BP_API int64_t bp_schedule_rounds(const bp_schedule* s);
+BP_API int64_t bp_schedule_npasses(const bp_schedule* s);
 /* ScheduleEvent list (engine.hpp:46-58) sorted by (slot, device):
  * 6 int64 per event: slot, device, block_id, level, phase, round. */
-int64_t bp_schedule_nevents(const bp_schedule* s);
-void bp_schedule_events(const bp_schedule* s, int64_t* out);
+BP_API int64_t bp_schedule_nevents(const bp_schedule* s);
+BP_API void bp_schedule_events(const bp_schedule* s, int64_t* out);
 /* TransferLedger (engine.hpp:62-71): channel name (<=31 chars), round, passes, scalars. */
-int64_t bp_schedule_nledger(const bp_schedule* s);
-void bp_schedule_ledger(const bp_schedule* s, int64_t i, char* channel, int64_t* round,
+BP_API int64_t bp_schedule_nledger(const bp_schedule* s);
+BP_API void bp_schedule_ledger(const bp_schedule* s, int64_t i, char* channel, int64_t* round,
                         int64_t* passes, int64_t* scalars);
 /* QueueSnapshot per round (engine.hpp:90-94); returns the block count. */
-int64_t bp_schedule_nsnapshots(const bp_schedule* s);
-int32_t bp_schedule_snapshot(const bp_schedule* s, int64_t i, int64_t* round, int64_t* ids,
+BP_API int64_t bp_schedule_nsnapshots(const bp_schedule* s);
+BP_API int32_t bp_schedule_snapshot(const bp_schedule* s, int64_t i, int64_t* round, int64_t* ids,
                              int32_t* levels);
 /* Emitted blocks in emission order: id, frame count, noise ids (<= frames). */
-int64_t bp_schedule_nblocks(const bp_schedule* s);
-int32_t bp_schedule_block(const bp_schedule* s, int64_t i, int64_t* block_id, int64_t* frames,
+BP_API int64_t bp_schedule_nblocks(const bp_schedule* s);
+BP_API int32_t bp_schedule_block(const bp_schedule* s, int64_t i, int64_t* block_id, int64_t* frames,
                           int32_t* noise_ids, int64_t* frame_ids);
 /* One rank's ordered program for the NCCL pipeline (2 int64 per op: kind,
  * pass): kind 0 = stage forward (+ send downstream), kind 1 = rank 0's eps
  * receive + Euler update. Returns the op count; out may be NULL. */
-int64_t bp_schedule_rank_program(const bp_schedule* s, int32_t rank, int64_t* out, int64_t cap);
+BP_API int64_t bp_schedule_rank_program(const bp_schedule* s, int32_t rank, int64_t* out, int64_t cap);
 /* Pass record i (issue order), 20 int64: round, block, level, version, ctx
  * source (0 none, 1 in-queue, 2 retained), ctx block, ctx frames, ctx version,
  * ctx first frame, centre frames, tokens, centre tokens, cached-context id (-1),
  * capture count, earliest slot, slot on device 0, completion slot,
  * finishes-block, phase, frame count; plus per-frame levels / ids and the
  * capture frame positions. Returns the frame count. */
-int32_t bp_schedule_pass(const bp_schedule* s, int64_t i, int64_t* rec, int32_t* levels, int64_t* frame_ids,
+BP_API int32_t bp_schedule_pass(const bp_schedule* s, int64_t i, int64_t* rec, int32_t* levels, int64_t* frame_ids,
                          int32_t* capture);
 /* Block meta by id: frames, append round, fresh (0/1), fresh RNG state bits. */
-void bp_schedule_block_meta(const bp_schedule* s, int64_t block_id, int64_t* rec4);
+BP_API void bp_schedule_block_meta(const bp_schedule* s, int64_t block_id, int64_t* rec4);
 /* Stage layer ranges actually used: begins[N], ends[N]. */
-void bp_schedule_partition(const bp_schedule* s, int32_t* begins, int32_t* ends);
+BP_API void bp_schedule_partition(const bp_schedule* s, int32_t* begins, int32_t* ends);
 
 /* ---- engine.hpp: the pipeline ------------------------------------------------ */
 typedef struct bp_pipeline bp_pipeline;
 
 /* NCCL unique id for the transport (128 bytes). */
-bp_status bp_nccl_unique_id(uint8_t out[128]);
+BP_API bp_status bp_nccl_unique_id(uint8_t out[128]);
 /* Loopback: rank=0, world=1, all N stages on `device`, nccl_ids NULL.
  * NCCL: one process per GPU, rank j owns stage j, world = N; nccl_ids holds
  * N unique ids made by rank 0 and shared by the caller (128 bytes each). */
-bp_status bp_pipeline_create(const bp_pipeline_desc* desc, int32_t rank, int32_t world,
+BP_API bp_status bp_pipeline_create(const bp_pipeline_desc* desc, int32_t rank, int32_t world,
                              int32_t device, const uint8_t* nccl_ids, bp_pipeline** out);
-bp_status bp_pipeline_destroy(bp_pipeline* p);
+BP_API bp_status bp_pipeline_destroy(bp_pipeline* p);
 
 /* EmittedBlock (engine.hpp:73-78) callback, rank 0 only, emission order. */
 typedef void (*bp_emit_fn)(void* user, int64_t block_id, int64_t frames, const double* data,
@@ -223,7 +240,7 @@ typedef void (*bp_emit_fn)(void* user, int64_t block_id, int64_t frames, const d
 /* run_pipeline (engine.cpp:255-497): one whole generation. emit may be NULL:
  * the emitted latents then stay on the device (no device->host copies;
  * bp_pipeline_block returns their device pointers). */
-bp_status bp_pipeline_run(bp_pipeline* p, bp_emit_fn emit, void* user);
+BP_API bp_status bp_pipeline_run(bp_pipeline* p, bp_emit_fn emit, void* user);
 
 typedef struct {
   double gpu_ms;            /* device time of the last run (CUDA events) */
@@ -235,15 +252,15 @@ typedef struct {
   double cross_ms;          /* cross-attention device time (profiling)             */
   int64_t attn_launches, gemm_launches, cross_launches;
 } bp_pipeline_stats;
-bp_status bp_pipeline_get_stats(bp_pipeline* p, bp_pipeline_stats* out);
+BP_API bp_status bp_pipeline_get_stats(bp_pipeline* p, bp_pipeline_stats* out);
 /* Per-kernel-class timing with CUDA events on the launching stream (0/1). */
-bp_status bp_pipeline_set_profiling(bp_pipeline* p, int32_t on);
+BP_API bp_status bp_pipeline_set_profiling(bp_pipeline* p, int32_t on);
 /* TraceRecord (engine.hpp:83-87) of pass i when record_trace is set. */
-int64_t bp_pipeline_ntrace(bp_pipeline* p);
-bp_status bp_pipeline_trace(bp_pipeline* p, int64_t i, int64_t* round, int64_t* block_id,
+BP_API int64_t bp_pipeline_ntrace(bp_pipeline* p);
+BP_API bp_status bp_pipeline_trace(bp_pipeline* p, int64_t i, int64_t* round, int64_t* block_id,
                             int64_t* rows, int64_t* cols, double* eps /* may be NULL */);
 /* Device pointer + element count of emitted block i's latents (fp64). */
-bp_status bp_pipeline_block(bp_pipeline* p, int64_t i, const double** dev_data, int64_t* count);
+BP_API bp_status bp_pipeline_block(bp_pipeline* p, int64_t i, const double** dev_data, int64_t* count);
 
 #ifdef __cplusplus
 }

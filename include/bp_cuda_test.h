@@ -14,24 +14,24 @@ extern "C" {
 
 /* Selects the bf16 GEMM / attention implementation: 1 = tcgen05 (default),
  * 0 = SIMT check kernels. Applies to subsequent launches in this process. */
-bp_status bp_set_kernel_impl(int32_t gemm_impl, int32_t attn_impl);
+BP_API bp_status bp_set_kernel_impl(int32_t gemm_impl, int32_t attn_impl);
 
 /* C[M,N] (+)= A[M,K] . W[N,K]^T on the device, host buffers. A, W are bf16
  * bit patterns; C is bf16 (epi 0/1) or fp32 (epi 2/3), row stride ldc. */
-bp_status bp_selftest_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int32_t epi,
+BP_API bp_status bp_selftest_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int32_t epi,
                            const uint16_t* A, int64_t lda, const uint16_t* W, void* C, int64_t ldc);
 
 /* Attention of q rows against [k0/v0 (n0 rows) ++ k1/v1 (n1 rows)], bf16 bit
  * patterns, all with row stride heads*dh; out bf16 [rows, heads*dh]. */
-bp_status bp_selftest_attn(int32_t device, int64_t rows, int32_t heads, int32_t dh, const uint16_t* q,
+BP_API bp_status bp_selftest_attn(int32_t device, int64_t rows, int32_t heads, int32_t dh, const uint16_t* q,
                            const uint16_t* k0, const uint16_t* v0, int64_t n0, const uint16_t* k1,
                            const uint16_t* v1, int64_t n1, float scale, uint16_t* out);
 
 /* Device time (ms, CUDA events on the launching stream) of `iters` back-to-back
  * launches of the current GEMM implementation on device-resident random data. */
-bp_status bp_bench_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int32_t epi, int32_t iters,
+BP_API bp_status bp_bench_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int32_t epi, int32_t iters,
                         double* ms);
-bp_status bp_bench_attn(int32_t device, int64_t rows, int32_t heads, int32_t dh, int64_t n0, int64_t n1,
+BP_API bp_status bp_bench_attn(int32_t device, int64_t rows, int32_t heads, int32_t dh, int64_t n0, int64_t n1,
                         int32_t iters, double* ms);
 
 #ifdef __cplusplus

@@ -73,6 +73,10 @@ def lib():
         L.bpref_run_trace_info.argtypes = [C.c_void_p, i64, P(i64), P(i64), P(i64), P(i64)]
         L.bpref_run_trace_data.argtypes = [C.c_void_p, i64, P(f64)]
         L.bpref_run_bubbles.argtypes = [C.c_void_p, P(i64), P(f64)]
+        L.bpref_bubble.argtypes = [C.c_int, C.c_int, i64, C.c_int, P(i64), P(f64)]
+        L.bpref_method_cost.argtypes = [C.c_char_p, P(i64), P(f64), C.c_int, P(f64)]
+        L.bpref_noise_walk.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, u64, C.c_int, P(C.c_int),
+                                       P(C.c_int)]
         _lib = L
     return _lib
 
@@ -242,3 +246,48 @@ def fnv1a64(arrays) -> str:
             h ^= byte
             h = (h * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
     return f"{h:016x}"
+
+
+# ---- analytics.hpp / noise-demo (operator surface goldens) -----------------------------
+def _ck(rc: int) -> None:
+    if rc != 0:
+        _raise()
+
+
+def bubble(n: int, t: int, blocks: int, order: str = "reverse"):
+    """(bubble_size, bubble_ratio) (analytics.cpp:13-31)."""
+    size, ratio = i64(), f64()
+    _ck(lib().bpref_bubble(n, t, blocks, 1 if order == "sequential" else 0, C.byref(size), C.byref(ratio)))
+    return size.value, ratio.value
+
+
+COST_KEYS = ("frames", "height", "width", "hidden", "channels", "layers", "devices", "num_b", "num_c")
+COST_DEFAULTS = dict(frames=16, height=4, width=4, hidden=8, channels=4, layers=8, devices=2, num_b=8,
+                     num_c=8, model_mem=1.0, kv_mem=1.0, ring_refinement=False)
+
+
+def method_cost(method: str, **kw) -> Dict[str, Any]:
+    """method_cost (analytics.cpp:67-117) with CostParams defaults (analytics.hpp:31-47)."""
+    p = dict(COST_DEFAULTS, **kw)
+    ints = (i64 * 9)(*[int(p[k]) for k in COST_KEYS])
+    mem = (f64 * 2)(float(p["model_mem"]), float(p["kv_mem"]))
+    out = (f64 * 4)()
+    _ck(lib().bpref_method_cost(method.encode(), ints, mem, 1 if p["ring_refinement"] else 0, out))
+    return {"method": method, "comm_scalars": out[0], "comm_overlap": bool(out[1]), "model_mem": out[2],
+            "kv_mem": out[3]}
+
+
+def noise_walk(strategy: str, appends: int, num_b: int, num_c: int, seed: int):
+    """Noise ids per block as cli.cpp:499-529 (noise-demo) draws them."""
+    cap = num_b + num_c // 2
+    ids = (C.c_int * ((appends + 1) * cap))()
+    counts = (C.c_int * (appends + 1))()
+    _ck(lib().bpref_noise_walk(strategy.encode(), appends, num_b, num_c, seed, cap, ids, counts))
+    return [[ids[r * cap + k] for k in range(counts[r])] for r in range(appends + 1)]
+
+
+def permutation(seed: int, n: int) -> np.ndarray:
+    """RandomSource(seed).permutation(n) (rng.cpp:41-49)."""
+    out = (C.c_int * max(n, 1))()
+    lib().bpref_permutation(seed, n, out)  # void
+    return np.array(out[:n], dtype=np.int64)

@@ -320,3 +320,61 @@ void bpref_run_bubbles(void* hv, int64_t* out7, double* ratio) {
 }
 
 }  // extern "C"
+
+// ---- artifacts.hpp / run_config.hpp (operator surface, for byte-level goldens) ----
+#include "blockpipe/artifacts.hpp"
+#include "blockpipe/run_config.hpp"
+extern "C" int bpref_write_artifacts(const char* config_json, const char* out_dir) {
+  return guard([&] {
+    RunConfig cfg = run_config_from_json_text(config_json);
+    cfg.out_dir = out_dir;
+    run_and_write_artifacts(cfg);
+  });
+}
+
+// ---- analytics.hpp (closed-form formulas) and the noise-demo id walk ----------
+#include "blockpipe/analytics.hpp"
+extern "C" int bpref_bubble(int n, int t, int64_t blocks, int order, int64_t* size, double* ratio) {
+  return guard([&] {
+    const BubbleParams bp{n, t, blocks, order ? Order::kSequential : Order::kReverse};
+    *size = bubble_size(bp);   // analytics.cpp:13-24
+    *ratio = bubble_ratio(bp); // analytics.cpp:26-31
+  });
+}
+// p = {frames,height,width,hidden,channels,layers,devices,num_b,num_c}; mem = {model_mem, kv_mem}
+// out = {comm_scalars, comm_overlap, model_mem, kv_mem}
+extern "C" int bpref_method_cost(const char* method, const int64_t* p, const double* mem, int ring,
+                                 double* out) {
+  return guard([&] {
+    CostParams cp;
+    cp.frames = p[0]; cp.height = p[1]; cp.width = p[2]; cp.hidden = p[3]; cp.channels = p[4];
+    cp.layers = p[5]; cp.devices = p[6]; cp.num_b = p[7]; cp.num_c = p[8];
+    cp.model_mem = mem[0]; cp.kv_mem = mem[1]; cp.ring_refinement = ring != 0;
+    const MethodCost c = method_cost(parse_method(method), cp);  // analytics.cpp:67-117
+    out[0] = c.comm_scalars; out[1] = c.comm_overlap ? 1.0 : 0.0; out[2] = c.model_mem; out[3] = c.kv_mem;
+  });
+}
+// Noise ids of the first block and `appends` appends, drawn by the reference's
+// draw_first_block / draw_next_block exactly as cli.cpp:499-529 drives them.
+// ids is a row-major [appends+1][cap_per] array (-1 padded); counts per block.
+extern "C" int bpref_noise_walk(const char* strategy, int appends, int num_b, int num_c, uint64_t seed,
+                                int cap_per, int* ids, int* counts) {
+  return guard([&] {
+    const InitStrategy s = parse_strategy(strategy);
+    NoisePool pool = build_pool(num_b, num_c, {2, 2, 1}, seed);
+    RandomSource rng(derive_seed(seed, {1}));
+    NoiseDraw cur = draw_first_block(s, pool, rng);
+    auto put = [&](int row, const std::vector<int>& v) {
+      counts[row] = static_cast<int>(v.size());
+      for (int k = 0; k < cap_per; ++k) ids[row * cap_per + k] = k < static_cast<int>(v.size()) ? v[k] : -1;
+    };
+    put(0, cur.noise_ids);
+    for (int i = 1; i <= appends; ++i) {
+      std::vector<int> window;
+      const int w = num_c / 2;
+      if (w > 0 && static_cast<int>(cur.noise_ids.size()) >= w) window.assign(cur.noise_ids.end() - w, cur.noise_ids.end());
+      cur = draw_next_block(s, pool, window, rng);
+      put(i, cur.noise_ids);
+    }
+  });
+}

@@ -93,6 +93,9 @@ _SIGS = {
     "bp_stage_set_context": (i32, [C.c_void_p, P(f64), i64, i64]),
     "bp_stage_cache_audit": (i32, [C.c_void_p, C.c_char_p, i32]),
     "bp_scheduler_step": (i32, [i32, P(f64), P(f64), i64, i32, i32, P(f64)]),
+    "bp_matmul": (i32, [i32, P(f64), P(f64), i64, i64, i64, P(f64)]),
+    "bp_softmax_rows": (i32, [i32, P(f64), i64, i64, P(f64)]),
+    "bp_layer_norm": (i32, [i32, P(f64), i64, i64, f64, P(f64)]),
     "bp_schedule_create": (i32, [P(PipelineDesc), P(C.c_void_p)]),
     "bp_schedule_destroy": (None, [C.c_void_p]),
     "bp_schedule_rounds": (i64, [C.c_void_p]),

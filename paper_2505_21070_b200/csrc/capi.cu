@@ -253,4 +253,74 @@ bp_status bp_scheduler_step(int32_t device, const double* x, const double* eps, 
   });
 }
 
+namespace {
+// Host-buffer round trip for the tensor primitives: copy in, launch, copy out.
+struct HostOp {
+  std::vector<bp::DevBuf> bufs;
+  double* in(const double* h, int64_t n) {
+    bufs.emplace_back();
+    bufs.back().alloc(static_cast<size_t>(n) * 8 + 8);
+    if (n > 0) BP_CUDA(cudaMemcpy(bufs.back().p, h, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice));
+    return bufs.back().as<double>();
+  }
+  double* scratch(int64_t n) {
+    bufs.emplace_back();
+    bufs.back().alloc(static_cast<size_t>(n) * 8 + 8);
+    return bufs.back().as<double>();
+  }
+  static void out(double* h, const double* d, int64_t n) {
+    BP_CUDA(cudaDeviceSynchronize());
+    if (n > 0) BP_CUDA(cudaMemcpy(h, d, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+  }
+};
+void require_2d(int64_t rows, int64_t cols, const char* what) {
+  if (rows < 0 || cols < 0) bp::fail(BP_ERR_DIMENSION, std::string(what) + ": negative extent");
+  if (rows > INT32_MAX || cols > INT32_MAX) bp::fail(BP_ERR_DIMENSION, std::string(what) + ": extent too large");
+}
+}  // namespace
+
+bp_status bp_matmul(int32_t device, const double* a, const double* b, int64_t m, int64_t k, int64_t n,
+                    double* out) {
+  return bp::guarded([&] {
+    require_2d(m, k, "matmul");
+    require_2d(k, n, "matmul");
+    bp::require_device(device);
+    HostOp op;
+    const double* da = op.in(a, m * k);
+    const double* db = op.in(b, k * n);
+    double* dc = op.scratch(m * n);
+    if (m > 0 && n > 0) {
+      if (k == 0) BP_CUDA(cudaMemset(dc, 0, static_cast<size_t>(m * n) * 8));
+      else bp::launch_matmul<double>(da, k, db, n, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k),
+                                     dc, n, bp::kEpiNone, nullptr, 0, nullptr);
+    }
+    HostOp::out(out, dc, m * n);
+  });
+}
+
+bp_status bp_softmax_rows(int32_t device, const double* x, int64_t rows, int64_t cols, double* out) {
+  return bp::guarded([&] {
+    require_2d(rows, cols, "softmax_rows");
+    bp::require_device(device);
+    HostOp op;
+    const double* dx = op.in(x, rows * cols);
+    double* dy = op.scratch(rows * cols);
+    bp::launch_softmax_rows(dx, rows, cols, dy, nullptr);
+    HostOp::out(out, dy, rows * cols);
+  });
+}
+
+bp_status bp_layer_norm(int32_t device, const double* x, int64_t rows, int64_t cols, double eps, double* out) {
+  return bp::guarded([&] {
+    require_2d(rows, cols, "layer_norm");
+    if (cols < 1) bp::fail(BP_ERR_DIMENSION, "layer_norm needs at least one column");
+    bp::require_device(device);
+    HostOp op;
+    const double* dx = op.in(x, rows * cols);
+    double* dy = op.scratch(rows * cols);
+    bp::launch_layer_norm(dx, rows, static_cast<int>(cols), eps, dy, nullptr);
+    HostOp::out(out, dy, rows * cols);
+  });
+}
+
 }  // extern "C"

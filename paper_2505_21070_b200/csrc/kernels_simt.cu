@@ -114,7 +114,7 @@ __global__ void k_ln(const T* __restrict__ x, const T* __restrict__ g, const T* 
   const T inv = Ar<T>::div(static_cast<T>(1), Ar<T>::sqrt_(Ar<T>::add(var, eps)));
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     const T yn = Ar<T>::mul(Ar<T>::sub(xr[j], mean), inv);
-    y[r * n + j] = Ar<T>::add(Ar<T>::mul(yn, g[j]), b[j]);
+    y[r * n + j] = g ? Ar<T>::add(Ar<T>::mul(yn, g[j]), b[j]) : yn;  // g == nullptr: plain layer_norm
   }
 }
 
@@ -125,6 +125,38 @@ void launch_ln(const T* x, const T* g, const T* b, int64_t rows, int n, T* y, cu
   count_launch();
 }
 template void launch_ln<double>(const double*, const double*, const double*, int64_t, int, double*, cudaStream_t);
+
+// Plain layer_norm(x, eps) (tensor.cpp:128-146): no affine.
+void launch_layer_norm(const double* x, int64_t rows, int n, double eps, double* y, cudaStream_t st) {
+  if (rows <= 0) return;
+  k_ln<double><<<static_cast<unsigned>(rows), 128, 0, st>>>(x, nullptr, nullptr, rows, n, eps, y);
+  count_launch();
+}
+
+// ---- softmax_rows (tensor.cpp:111-126) -------------------------------------------
+// One block per row: row max, then e = exp(x - max) and their sum, then e / sum.
+__global__ void k_softmax_rows(const double* __restrict__ x, int64_t n, double* __restrict__ y) {
+  __shared__ double red[32];
+  const double* xr = x + blockIdx.x * n;
+  double* yr = y + blockIdx.x * n;
+  double mx = -INFINITY;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) mx = fmax(mx, xr[j]);
+  mx = block_reduce<double>(mx, red, true);
+  double s = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const double e = exp(xr[j] - mx);
+    yr[j] = e;
+    s += e;
+  }
+  s = block_reduce<double>(s, red, false);
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) yr[j] = yr[j] / s;
+}
+
+void launch_softmax_rows(const double* x, int64_t rows, int64_t n, double* y, cudaStream_t st) {
+  if (rows <= 0 || n <= 0) return;
+  k_softmax_rows<<<static_cast<unsigned>(rows), 128, 0, st>>>(x, n, y);
+  count_launch();
+}
 template void launch_ln<float>(const float*, const float*, const float*, int64_t, int, float*, cudaStream_t);
 
 // ---- matmul (tensor.cpp:84-109) with fused epilogues ---------------------------

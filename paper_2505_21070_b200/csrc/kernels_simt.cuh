@@ -25,6 +25,8 @@ void launch_embed(const double* lat, const double* w_in, const double* freq, con
                   cudaStream_t st);
 template <typename T>
 void launch_ln(const T* x, const T* g, const T* b, int64_t rows, int n, T* y, cudaStream_t st);
+void launch_layer_norm(const double* x, int64_t rows, int n, double eps, double* y, cudaStream_t st);
+void launch_softmax_rows(const double* x, int64_t rows, int64_t n, double* y, cudaStream_t st);
 template <typename T>
 void launch_matmul(const T* A, int64_t lda, const T* B, int64_t ldb, int M, int N, int K, T* C,
                    int64_t ldc, int epi, const T* R, int64_t ldr, cudaStream_t st);

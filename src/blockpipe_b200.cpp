@@ -365,21 +365,10 @@ void on_emit(void* user, int64_t block_id, int64_t frames, const double* data, c
 }
 }  // namespace
 
-RunResult run_pipeline(const PipelineConfig& cfg) {
-  cfg.validate();
-  const bp_pipeline_desc d = pipe_desc(cfg);
-  RunResult r;
-  bp_schedule* s = nullptr;
-  ck(bp_schedule_create(&d, &s));
-  std::unique_ptr<bp_schedule, void (*)(bp_schedule*)> sg(s, bp_schedule_destroy);
-  bp_pipeline* p = nullptr;
-  ck(bp_pipeline_create(&d, 0, 1, cfg.model.device, nullptr, &p));
-  std::unique_ptr<bp_pipeline, bp_status (*)(bp_pipeline*)> pg(p, bp_pipeline_destroy);
-  Collector col{&r.blocks, {cfg.model.height, cfg.model.width, cfg.model.channels}};
-  ck(bp_pipeline_run(p, on_emit, &col));
-  bp_pipeline_stats st{};
-  ck(bp_pipeline_get_stats(p, &st));
-  r.gpu_ms = st.gpu_ms;
+namespace {
+// Everything in a RunResult that the data-independent schedule determines
+// (event log, ledger, rounds, queue snapshots) -- engine.cpp:343-414 (D6).
+void load_schedule(const bp_schedule* s, const PipelineConfig& cfg, RunResult& r) {
   r.rounds = bp_schedule_rounds(s);
   r.log.devices = cfg.devices;
   std::vector<int64_t> ev(static_cast<size_t>(bp_schedule_nevents(s)) * 6);
@@ -403,6 +392,30 @@ RunResult run_pipeline(const PipelineConfig& cfg) {
     q.levels.assign(lv.begin(), lv.end());
     r.queue_snapshots.push_back(std::move(q));
   }
+}
+
+using ScheduleGuard = std::unique_ptr<bp_schedule, void (*)(bp_schedule*)>;
+ScheduleGuard make_schedule(const bp_pipeline_desc& d) {
+  bp_schedule* s = nullptr;
+  ck(bp_schedule_create(&d, &s));
+  return ScheduleGuard(s, bp_schedule_destroy);
+}
+}  // namespace
+
+RunResult run_pipeline(const PipelineConfig& cfg) {
+  cfg.validate();
+  const bp_pipeline_desc d = pipe_desc(cfg);
+  RunResult r;
+  ScheduleGuard s = make_schedule(d);
+  bp_pipeline* p = nullptr;
+  ck(bp_pipeline_create(&d, 0, 1, cfg.model.device, nullptr, &p));
+  std::unique_ptr<bp_pipeline, bp_status (*)(bp_pipeline*)> pg(p, bp_pipeline_destroy);
+  Collector col{&r.blocks, {cfg.model.height, cfg.model.width, cfg.model.channels}};
+  ck(bp_pipeline_run(p, on_emit, &col));
+  bp_pipeline_stats st{};
+  ck(bp_pipeline_get_stats(p, &st));
+  r.gpu_ms = st.gpu_ms;
+  load_schedule(s.get(), cfg, r);
   for (int64_t i = 0; i < bp_pipeline_ntrace(p); ++i) {
     TraceRecord t;
     int64_t rows = 0, cols = 0;
@@ -410,6 +423,25 @@ RunResult run_pipeline(const PipelineConfig& cfg) {
     t.eps = Tensor({rows, cols});
     ck(bp_pipeline_trace(p, i, &t.round, &t.block_id, &rows, &cols, t.eps.data.data()));
     r.trace.push_back(std::move(t));
+  }
+  return r;
+}
+
+RunResult plan_pipeline(const PipelineConfig& cfg) {
+  cfg.validate();
+  const bp_pipeline_desc d = pipe_desc(cfg);
+  RunResult r;
+  ScheduleGuard s = make_schedule(d);
+  load_schedule(s.get(), cfg, r);
+  for (int64_t i = 0; i < bp_schedule_nblocks(s.get()); ++i) {
+    EmittedBlock b;
+    int64_t frames = 0;
+    const int32_t nids = bp_schedule_block(s.get(), i, &b.block_id, &frames, nullptr, nullptr);
+    b.noise_ids.resize(static_cast<size_t>(nids));
+    b.frame_ids.resize(static_cast<size_t>(frames));
+    bp_schedule_block(s.get(), i, &b.block_id, &frames, b.noise_ids.data(), b.frame_ids.data());
+    b.frames.shape = {frames, cfg.model.height, cfg.model.width, cfg.model.channels};
+    r.blocks.push_back(std::move(b));
   }
   return r;
 }

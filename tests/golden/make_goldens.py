@@ -50,5 +50,34 @@ def main():
         json.dump(out, f, indent=1)
 
 
+ARTIFACT_CONFIGS = {
+    "default": {},
+    "n2_single": {"devices": 2, "mode": "single", "steps": 5, "blocks": 4},
+    "n4_seq_trim": {"devices": 4, "order": "sequential", "cache": "off", "emit_first_surplus": False,
+                    "steps": 4, "blocks": 3},
+    "n2_fresh": {"devices": 2, "strategy": "fresh", "steps": 3, "blocks": 5, "retain_clean_context": False},
+}
+
+
+def make_artifacts():
+    """Reference artifacts (artifacts.cpp:25-143) for byte-level comparison."""
+    import shutil
+    import subprocess
+    import tempfile
+    script = os.path.abspath(os.path.join(HERE, "..", "..", "oracle", "ref_artifacts.py"))
+    for name, cfg in ARTIFACT_CONFIGS.items():
+        dst = os.path.join(HERE, "artifacts", name)
+        shutil.rmtree(dst, ignore_errors=True)
+        with tempfile.TemporaryDirectory() as tmp:
+            # relative out_dir "out": the reference prints out_dir into the
+            # artifacts, tests reproduce it by writing from a temp cwd.
+            subprocess.run([sys.executable, script, json.dumps(cfg), "out"], check=True, cwd=tmp)
+            shutil.copytree(os.path.join(tmp, "out"), dst)
+        with open(os.path.join(dst, "config.json"), "w") as f:
+            json.dump(cfg, f)
+
+
 if __name__ == "__main__":
-    main()
+    if not os.environ.get("ARTIFACTS_ONLY"):
+        main()
+    make_artifacts()

@@ -8,9 +8,9 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_functions():
+def declared_functions(headers=("bp_cuda.h", "bp_cuda_test.h")):
     names = set()
-    for h in ("bp_cuda.h", "bp_cuda_test.h"):
+    for h in headers:
         text = open(os.path.join(ROOT, "include", h)).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         for m in re.finditer(r"\b(bp_[a-z0-9_]+)\s*\(", text):
@@ -28,6 +28,27 @@ def test_library_exports_every_declared_symbol(bp):
     assert set(_lib.EXPORTED) <= names
 
 
+def test_operator_library_exports_every_declared_symbol(bp):
+    """include/bp_operator.h is served by lib/libblockpipe_b200.so."""
+    import ctypes
+    from paper_2505_21070_b200 import operator
+    names = declared_functions(("bp_operator.h",))
+    assert {"bp_cli_main", "bp_write_artifacts", "bp_bubble", "bp_method_cost"} <= names
+    lib = ctypes.CDLL(operator.OP_LIB_PATH)
+    for n in sorted(names):
+        assert hasattr(lib, n), n
+
+
+def test_only_c_abi_is_exported(bp):
+    """libbp_cuda.so is built with -fvisibility=hidden: its dynamic symbol
+    table holds the declared C entry points and nothing of the internals."""
+    import subprocess
+    from paper_2505_21070_b200 import _lib
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    assert exported == declared_functions()
+
+
 def test_compute_entry_points_fail_loudly_without_gpu(bp):
     import torch
     if torch.cuda.is_available():
@@ -36,3 +57,12 @@ def test_compute_entry_points_fail_loudly_without_gpu(bp):
         bp.normals(1, 10)
     with pytest.raises(bp.CudaError):
         bp.run_pipeline({"devices": 1})
+    import _blockpipe
+    import numpy as np
+    for fn in (lambda: _blockpipe.matmul(np.eye(2), np.eye(2)), lambda: _blockpipe.softmax_rows(np.eye(2)),
+               lambda: _blockpipe.layer_norm(np.eye(2)), lambda: _blockpipe.RandomSource(1).next_normal()):
+        with pytest.raises(bp.CudaError):
+            fn()
+    from paper_2505_21070_b200 import operator
+    code, out, err = operator.cli_main(["run", "--out", "/tmp/bp_nogpu_run"])
+    assert (code, out) == (1, "") and "no CUDA device" in err, err
