@@ -63,7 +63,8 @@ std::vector<SweepPoint> sweep_frames(const CostParams& cp, const std::vector<Met
                                      const std::vector<int64_t>& frame_counts);
 
 // Extension: predicted boundary traffic of one whole run in bytes, from the
-// transfer ledger (scalars x element size of the activation dtype), next to
+// transfer ledger (scalars x boundary element size: 8 for f64, 4 for f32 and
+// for bf16, whose residual stream crosses stages in fp32), next to
 // what the engine actually moved (bp_pipeline_stats.boundary_bytes).
 struct TrafficReport {
   int64_t ledger_scalars = 0;

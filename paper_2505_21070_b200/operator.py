@@ -54,6 +54,7 @@ _op.bp_method_cost.restype = i32
 
 METHODS = ("ring-attention", "ulysses", "video-infinity", "fifo", "dualparal")
 DTYPE_BYTES = {"f64": 8, "f32": 4, "bf16": 2, "fp8": 1}
+BOUNDARY_BYTES = {"f64": 8, "f32": 4, "bf16": 4}  # stage-boundary activation element size per precision
 
 
 def _check(code: int) -> None:
@@ -150,10 +151,12 @@ def method_cost(method: str, **kwargs: Any) -> Dict[str, Any]:
 def traffic_report(ledger: Sequence[Dict[str, Any]], precision: str = "f64",
                    measured_bytes: Optional[int] = None) -> Dict[str, Any]:
     """Predicted device->device bytes of one run (ledger scalars x element
-    size of the activation dtype) beside the engine's measured boundary_bytes."""
+    size of the boundary activation) beside the engine's measured
+    boundary_bytes. The bf16 path keeps its residual stream in fp32 and ships
+    it as fp32, so an N-stage split stays bitwise equal to one stage."""
     scalars = sum(int(e["scalars"]) for e in ledger
                   if e["channel"].startswith("dev") and "->dev" in e["channel"])
-    elem = {"f64": 8, "f32": 4, "bf16": 2}[precision]
+    elem = BOUNDARY_BYTES[precision]
     return {"ledger_scalars": scalars, "predicted_bytes": scalars * elem,
             "measured_bytes": measured_bytes,
             "match": None if measured_bytes is None else measured_bytes == scalars * elem}

@@ -149,8 +149,9 @@ std::vector<SweepPoint> sweep_frames(const CostParams& cp, const std::vector<Met
 
 TrafficReport traffic_report(const TransferLedger& ledger, Precision p, int64_t measured_bytes) {
   // Only device->device channels cross a GPU boundary; host->dev0 latents and
-  // the eps return stay on rank 0 (loopback) or are counted separately.
-  const int64_t elem = p == Precision::kF64 ? 8 : p == Precision::kF32 ? 4 : 2;
+  // the eps return stay on rank 0 (loopback) or are counted separately. The
+  // bf16 path ships its fp32 residual stream, so N stages == 1 stage bitwise.
+  const int64_t elem = p == Precision::kF64 ? 8 : 4;
   TrafficReport r;
   for (const LedgerEntry& e : ledger.entries)
     if (e.channel.rfind("dev", 0) == 0 && e.channel.find("->dev") != std::string::npos)
