@@ -12,7 +12,8 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libbp_cuda.so")
+# BP_LIB_PATH points at an alternative build (A/B kernel experiments only)
+LIB_PATH = os.environ.get("BP_LIB_PATH") or os.path.join(_HERE, "lib", "libbp_cuda.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -1,7 +1,13 @@
-// tcgen05 flash attention over two KV segments (K6/K7): every query tile of
-// 128 rows of one head attends to [cached prefix (previous pass on this GPU,
-// resident in HBM) ++ current block] without concatenating them in memory
+// tcgen05 flash attention over two KV segments (K6/K7): every query row of
+// one head attends to [cached prefix (previous pass on this GPU, resident in
+// HBM) ++ current block] without concatenating them in memory
 // (model.cpp:201-211, 302-318: vcat_rows(prefix, k) then attention()).
+//
+// Two implementations (launch_attn_tc variant):
+//   2 (default) k_attn_pp: two 128-row query tiles per CTA, 64-key K/V tiles,
+//     double-buffered S per tile, both softmax warpgroups running concurrently
+//     (see the comment above k_attn_pp).
+//   1 k_attn_tc: one 128-row query tile per CTA, Q and P as TMEM A operands:
 //
 //   warp 0      TMA producer: Q once, then K and V tiles of 128 keys into two
 //               separate 3-deep rings (K is freed as soon as S_j is computed)
@@ -74,10 +80,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// Shared-memory traffic is the binding budget for attention (each SMEM-SMEM
-// 128x128x16 MMA reads 8 KB in 64 cycles): both MMAs therefore take their A
-// operand from TMEM (Q staged once; P written by the softmax over its S
-// buffer) and only K / V stream through shared memory.
+// Both MMAs take their A operand from TMEM (Q staged once; P written by the
+// softmax over its S buffer), so only K / V stream through shared memory.
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_tc(const __grid_constant__ AttnMaps maps, int64_t rows, int64_t n0, int64_t n1, float scale_log2,
               bf16* __restrict__ out, int64_t ldo) {
@@ -310,35 +314,312 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ============================================================================
+// Ping-pong variant: two query tiles per CTA, 64-key tiles, S double-buffered
+// ============================================================================
+// One CTA owns query rows [256*blockIdx.x, +256) of one head as tiles A and B.
+// K_j / V_j (64 keys each) stream through smem once for both tiles. Each tile
+// has two S buffers, so QK_x(j+1) runs on the tensor core while the softmax of
+// tile x works on S_x(j), and the softmax warpgroups of A and B run
+// concurrently (two latency-bound softmax warps per SM sub-partition instead
+// of one). TMEM: S_A0 [0,64) S_A1 [64,128) S_B0 [128,192) S_B1 [192,256)
+// O_A [256,384) O_B [384,512); P_x(j) overwrites the first 32 columns of its S
+// buffer as packed bf16 pairs. Q is an smem (SS) operand: an SS MMA sustains
+// the tcgen05 issue floor (tools/micro/mma_floor.cu).
+//   warp 0        TMA producer (Q_A, Q_B once; K / V rings of 64-key tiles)
+//   warp 1        MMA issuer: QK (M128 N64 K128, 8 MMAs), PV (M128 N128 K64, 4)
+//   warps 2..5    softmax + epilogue of tile A  (thread <-> row <-> TMEM lane
+//   warps 6..9    softmax + epilogue of tile B   quarter warp & 3)
+// Softmax arithmetic is packed (FFMA2 / FADD2, three-input FMNMX); one exp2
+// pair in four runs on the FMA pipe.
+constexpr int PBK = 64;                              // keys per K/V tile
+constexpr uint32_t PHALF = PBK * 64 * 2;            // [64 keys][64 d] swizzled box, 8 KB
+constexpr uint32_t PTILE = 2 * PHALF;               // 16 KB
+constexpr int PP_KST = 4, PP_VST = 4;
+constexpr uint32_t PP_Q = 0;                        // Q_A, Q_B (32 KB each)
+constexpr uint32_t PP_K = PP_Q + 2 * TILE;
+constexpr uint32_t PP_V = PP_K + PP_KST * PTILE;
+constexpr uint32_t PP_BAR = PP_V + PP_VST * PTILE;
+constexpr uint32_t PP_SMEM_BYTES = PP_BAR + 256 + 1024;
+constexpr int PP_THREADS = 320;
+static_assert(PP_SMEM_BYTES <= 232448, "ping-pong attention exceeds the 227 KB smem limit");
+
+struct AttnMapsPP {
+  CUtensorMap q, k0, v0, k1, v1;  // q: 128-row boxes; k/v: 64-row boxes
+};
+
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  // ex2_poly on a packed pair: round via 1.5*2^23, cubic on the fraction.
+  const float2 big = make_float2(12582912.f, 12582912.f);
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 j = __fadd2_rn(x, big);
+  const float2 jr = __fadd2_rn(j, make_float2(-12582912.f, -12582912.f));  // round(x)
+  const float2 f = __fadd2_rn(x, make_float2(-jr.x, -jr.y));
+  float2 p = __ffma2_rn(make_float2(0.0555041086f, 0.0555041086f), f, make_float2(0.2402264923f, 0.2402264923f));
+  p = __ffma2_rn(p, f, make_float2(0.6931471806f, 0.6931471806f));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
+
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+__global__ void __launch_bounds__(PP_THREADS, 1)
+    k_attn_pp(const __grid_constant__ AttnMapsPP maps, int64_t rows, int64_t n0, int64_t n1, float scale_log2,
+              bf16* __restrict__ out, int64_t ldo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + PP_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;              // [PP_KST]
+  uint64_t* k_empty = k_full + PP_KST;      // [PP_KST]
+  uint64_t* v_full = k_empty + PP_KST;      // [PP_VST]
+  uint64_t* v_empty = v_full + PP_VST;      // [PP_VST]
+  uint64_t* s_full = v_empty + PP_VST;      // [tile][buffer]
+  uint64_t* p_full = s_full + 4;            // [tile][buffer] (128 arrivals)
+  uint64_t* pv_done = p_full + 4;           // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+
+  // warp index through a shuffle: provably warp-uniform, so the MMA / TMA
+  // branches keep their descriptors in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int qpair = blockIdx.x, head = blockIdx.y;
+  const int t0 = static_cast<int>((n0 + PBK - 1) / PBK);
+  const int t1 = static_cast<int>((n1 + PBK - 1) / PBK);
+  const int T = t0 + t1;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&maps.q);
+    tc::tma_prefetch(&maps.k1);
+    tc::tma_prefetch(&maps.v1);
+    tc::mbar_init(q_full, 1);
+    for (int s = 0; s < PP_KST; ++s) {
+      tc::mbar_init(&k_full[s], 1);
+      tc::mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < PP_VST; ++s) {
+      tc::mbar_init(&v_full[s], 1);
+      tc::mbar_init(&v_empty[s], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      tc::mbar_init(&s_full[i], 1);
+      tc::mbar_init(&p_full[i], 128);
+    }
+    tc::mbar_init(&pv_done[0], 1);
+    tc::mbar_init(&pv_done[1], 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- TMA producer -------------------------------------------------------------------
+    tc::mbar_arrive_expect_tx_elect(q_full, 2 * TILE);
+    for (int x = 0; x < 2; ++x) {
+      const int qrow = qpair * 2 * BQ + x * BQ;
+      tc::tma_load_2d_elect(smem + PP_Q + x * TILE, &maps.q, q_full, head * kDh, qrow);
+      tc::tma_load_2d_elect(smem + PP_Q + x * TILE + HALF, &maps.q, q_full, head * kDh + 64, qrow);
+    }
+    for (int j = 0; j < T; ++j) {
+      const bool seg0 = j < t0;
+      const int row0 = (seg0 ? j : j - t0) * PBK;
+      const int ks = j % PP_KST, vs = j % PP_VST;
+      tc::mbar_wait(&k_empty[ks], ((j / PP_KST) & 1) ^ 1);
+      uint8_t* kd = smem + PP_K + ks * PTILE;
+      const CUtensorMap* mk = seg0 ? &maps.k0 : &maps.k1;
+      tc::mbar_arrive_expect_tx_elect(&k_full[ks], PTILE);
+      tc::tma_load_2d_elect(kd, mk, &k_full[ks], head * kDh, row0);
+      tc::tma_load_2d_elect(kd + PHALF, mk, &k_full[ks], head * kDh + 64, row0);
+      tc::mbar_wait(&v_empty[vs], ((j / PP_VST) & 1) ^ 1);
+      uint8_t* vd = smem + PP_V + vs * PTILE;
+      const CUtensorMap* mv = seg0 ? &maps.v0 : &maps.v1;
+      tc::mbar_arrive_expect_tx_elect(&v_full[vs], PTILE);
+      tc::tma_load_2d_elect(vd, mv, &v_full[vs], head * kDh, row0);
+      tc::tma_load_2d_elect(vd + PHALF, mv, &v_full[vs], head * kDh + 64, row0);
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer -----------------------------------------------------------------------
+    constexpr uint32_t idesc_s = tc::idesc_bf16(BQ, PBK, 0, 0);  // Q (smem, K-major) x K^T (smem, K-major)
+    constexpr uint32_t idesc_o = tc::idesc_bf16(BQ, kDh, 0, 1);  // P (TMEM) x V (smem, MN-major)
+    const uint32_t q_base = tc::smem_u32(smem + PP_Q);
+    auto qk = [&](int x, int j) {  // S_x(j) into buffer j & 1 of tile x
+      const uint32_t k_addr = tc::smem_u32(smem + PP_K + (j % PP_KST) * PTILE);
+      const uint32_t q_addr = q_base + x * TILE;
+      const uint32_t d = tmem + static_cast<uint32_t>(x * 2 * PBK + (j & 1) * PBK);
+      tc::mma_ss_k128_elect<HALF / 16, PHALF / 16>(d, tc::desc_sw128(q_addr, 1024, 16), tc::desc_sw128(k_addr, 1024, 16),
+                                                   idesc_s, 0u);
+      tc::mma_commit_elect(&s_full[x * 2 + (j & 1)]);
+    };
+    auto pv = [&](int x, int j) {
+      const uint32_t v_addr = tc::smem_u32(smem + PP_V + (j % PP_VST) * PTILE);
+      const uint32_t p_tm = tmem + static_cast<uint32_t>(x * 2 * PBK + (j & 1) * PBK);
+      tc::mma_ts_k64_elect<2048 / 16>(tmem + 256 + x * kDh, p_tm, tc::desc_sw128(v_addr, 1024, PHALF), idesc_o,
+                                      j > 0 ? 1u : 0u);
+      tc::mma_commit_elect(&pv_done[x]);
+    };
+    auto qk_pair = [&](int j) {
+      tc::mbar_wait(&k_full[j % PP_KST], (j / PP_KST) & 1);
+      tc::fence_after_sync();
+      qk(0, j);
+      qk(1, j);
+      tc::mma_commit_elect(&k_empty[j % PP_KST]);
+    };
+    tc::mbar_wait(q_full, 0);
+    if (T > 0) qk_pair(0);
+    if (T > 1) qk_pair(1);
+    for (int j = 0; j < T; ++j) {
+      tc::mbar_wait(&v_full[j % PP_VST], (j / PP_VST) & 1);
+      for (int x = 0; x < 2; ++x) {
+        tc::mbar_wait(&p_full[x * 2 + (j & 1)], (j >> 1) & 1);
+        tc::fence_after_sync();
+        pv(x, j);
+      }
+      tc::mma_commit_elect(&v_empty[j % PP_VST]);
+      if (j + 2 < T) qk_pair(j + 2);  // S buffer j & 1 is free once PV(j) is issued (in-order)
+    }
+  } else {
+    // ---- softmax + epilogue of tile x ------------------------------------------------------
+    const int x = (warp - 2) >> 2;
+    const int qq = warp & 3;
+    const int r = qq * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(qq * 32) << 16;
+    const uint32_t tm_o = tmem + lane_off + 256u + static_cast<uint32_t>(x * kDh);
+    const float2 sc2 = make_float2(scale_log2, scale_log2);
+    float m_used = -INFINITY;
+    float2 l2 = make_float2(0.f, 0.f);
+    const int n0i = static_cast<int>(n0), n1i = static_cast<int>(n1);
+    for (int j = 0; j < T; ++j) {
+      const int b = j & 1;
+      const bool seg0 = j < t0;
+      const int row0 = (seg0 ? j : j - t0) * PBK;
+      const int rem = (seg0 ? n0i : n1i) - row0;
+      const uint32_t tm_s = tmem + lane_off + static_cast<uint32_t>(x * 2 * PBK + b * PBK);
+      tc::mbar_wait(&s_full[x * 2 + b], (j >> 1) & 1);
+      tc::fence_after_sync();
+      uint32_t sr[64];
+      tc::tmem_ld32(tm_s, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tc::tmem_ld32(tm_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tc::tmem_ld_wait();
+      if (rem < PBK) {  // keys past the segment end (a segment's last tile)
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+          if (c >= rem) sr[c] = __float_as_uint(-INFINITY);
+      }
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 64; c += 8) {
+        m4[0] = max3f(m4[0], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+        m4[1] = max3f(m4[1], __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
+        m4[2] = max3f(m4[2], __uint_as_float(sr[c + 4]), __uint_as_float(sr[c + 5]));
+        m4[3] = max3f(m4[3], __uint_as_float(sr[c + 6]), __uint_as_float(sr[c + 7]));
+      }
+      const float mx = max3f(m4[0], m4[1], fmaxf(m4[2], m4[3])) * scale_log2;  // scale > 0
+      const bool need = mx > m_used + kRescaleThreshold;
+      const float m_new = need ? mx : m_used;
+      const float corr = need ? ex2(m_used - m_new) : 1.f;  // 0 on the first tile
+      const float2 neg_m2 = make_float2(-m_new, -m_new);
+      uint32_t pk[32];
+      float2 ls_a = make_float2(0.f, 0.f), ls_b = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const float2 xv = __ffma2_rn(make_float2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sc2,
+                                     neg_m2);
+        const float2 p = (c & 3) == 3 ? ex2_poly2(xv) : make_float2(ex2(xv.x), ex2(xv.y));
+        if (c & 1) ls_b = __fadd2_rn(ls_b, p);
+        else ls_a = __fadd2_rn(ls_a, p);
+        pk[c] = pack_bf16(p.x, p.y);
+      }
+      l2 = __ffma2_rn(l2, make_float2(corr, corr), __fadd2_rn(ls_a, ls_b));
+      m_used = m_new;
+      if (j >= 1 && __any_sync(0xffffffffu, need)) {  // O must hold PV(j-1) before it is rescaled
+        tc::mbar_wait(&pv_done[x], (j - 1) & 1);
+        tc::fence_after_sync();
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          const uint32_t ta = tm_o + static_cast<uint32_t>(c * 32);
+          tc::tmem_ld32(ta, o);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+          tc::tmem_st32(ta, o);
+        }
+      }
+      tc::tmem_st32(tm_s, pk);
+      tc::tmem_st_wait();
+      tc::fence_before_sync();
+      tc::mbar_arrive(&p_full[x * 2 + b]);
+    }
+    if (T >= 1) {
+      tc::mbar_wait(&pv_done[x], (T - 1) & 1);
+      tc::fence_after_sync();
+    }
+    const int64_t row = static_cast<int64_t>(qpair) * 2 * BQ + x * BQ + r;
+    const float inv_l = 1.f / (l2.x + l2.y);
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      tc::tmem_ld32(tm_o + static_cast<uint32_t>(c * 32), o);
+      tc::tmem_ld_wait();
+      if (row < rows) {
+        uint4* dst = reinterpret_cast<uint4*>(out + row * ldo + head * kDh + c * 32);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          dst[v] = make_uint4(pack_bf16(__uint_as_float(o[8 * v]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l),
+                              pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l),
+                              pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l),
+                              pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l));
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<512>(tmem);
+  }
+}
+
 std::mutex g_mu;
 struct Key {
-  const void* p; int64_t rows, cols, ld;
-  bool operator==(const Key& o) const { return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld; }
+  const void* p; int64_t rows, cols, ld, box_rows;
+  bool operator==(const Key& o) const {
+    return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows;
+  }
 };
 struct KeyHash {
   size_t operator()(const Key& k) const {
     return (reinterpret_cast<size_t>(k.p) * 1000003u) ^ (static_cast<size_t>(k.rows) * 7919u) ^
-           (static_cast<size_t>(k.cols) << 20) ^ static_cast<size_t>(k.ld);
+           (static_cast<size_t>(k.cols) << 20) ^ static_cast<size_t>(k.ld) ^ (static_cast<size_t>(k.box_rows) << 40);
   }
 };
 std::unordered_map<Key, CUtensorMap, KeyHash> g_maps;
 
-CUtensorMap map_for(const bf16* p, int64_t rows, int64_t cols, int64_t ld) {
+CUtensorMap map_for(const bf16* p, int64_t rows, int64_t cols, int64_t ld, uint32_t box_rows = 128) {
   std::lock_guard<std::mutex> lock(g_mu);
-  const Key k{p, rows, cols, ld};
+  const Key k{p, rows, cols, ld, box_rows};
   auto it = g_maps.find(k);
   if (it != g_maps.end()) return it->second;
   if (g_maps.size() > 4096) g_maps.clear();
   CUtensorMap m;
   make_tmap_2d_bf16(&m, p, static_cast<uint64_t>(rows < 1 ? 1 : rows), static_cast<uint64_t>(cols),
-                    static_cast<uint64_t>(ld), 128, 64);
+                    static_cast<uint64_t>(ld), box_rows, 64);
   g_maps.emplace(k, m);
   return m;
 }
 
 }  // namespace
 
-void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st) {
+void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int variant) {
   const int64_t H = static_cast<int64_t>(a.heads) * a.dh;
   const bool aligned = ((a.ldq | a.ldk1 | a.ldv1 | a.ldo) * 2) % 16 == 0 &&
                        (a.n0 == 0 || ((a.ldk0 | a.ldv0) * 2) % 16 == 0);
@@ -349,6 +630,7 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     BP_CUDA(cudaFuncSetAttribute(k_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_attn_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
     configured = true;
   }
   AttnMaps maps;
@@ -362,8 +644,25 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st) {
     maps.k0 = maps.k1;
     maps.v0 = maps.v1;
   }
-  dim3 grid(static_cast<unsigned>((rows + BQ - 1) / BQ), static_cast<unsigned>(a.heads));
-  k_attn_tc<<<grid, kThreads, SMEM_BYTES, st>>>(maps, rows, a.n0, a.n1, a.scale * 1.4426950408889634f, a.out, a.ldo);
+  const float scale_log2 = a.scale * 1.4426950408889634f;
+  if (variant == 2) {  // ping-pong: 256 query rows per CTA, 64-key tiles
+    AttnMapsPP pm;
+    pm.q = maps.q;
+    pm.k1 = map_for(a.k1, a.n1, H, a.ldk1, PBK);
+    pm.v1 = map_for(a.v1, a.n1, H, a.ldv1, PBK);
+    if (a.n0 > 0) {
+      pm.k0 = map_for(a.k0, a.n0, H, a.ldk0, PBK);
+      pm.v0 = map_for(a.v0, a.n0, H, a.ldv0, PBK);
+    } else {
+      pm.k0 = pm.k1;
+      pm.v0 = pm.v1;
+    }
+    dim3 grid(static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(a.heads));
+    k_attn_pp<<<grid, PP_THREADS, PP_SMEM_BYTES, st>>>(pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
+  } else {
+    dim3 grid(static_cast<unsigned>((rows + BQ - 1) / BQ), static_cast<unsigned>(a.heads));
+    k_attn_tc<<<grid, kThreads, SMEM_BYTES, st>>>(maps, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
+  }
   count_launch();
 }
 

@@ -3,6 +3,8 @@
 // kernels on the device. The production GEMM/attention live in
 // gemm_sm100.cu / attn_sm100.cu.
 #include <cuda_bf16.h>
+
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "device.cuh"
@@ -179,11 +181,17 @@ namespace bp {
 
 void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C, int64_t ldc,
                     int epi, cudaStream_t st);
-void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st);
+void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int variant);
 
 namespace {
 int g_gemm_impl = 1;  // 0 = SIMT check path, 1 = tcgen05
-int g_attn_impl = 1;
+// 0 = SIMT check path, 1 = tcgen05 one Q tile/CTA, 2 = tcgen05 ping-pong.
+// BP_ATTN_IMPL overrides the default (A/B runs of the whole suite).
+int default_attn_impl() {
+  const char* e = std::getenv("BP_ATTN_IMPL");
+  return e ? std::atoi(e) : 2;
+}
+int g_attn_impl = default_attn_impl();
 }  // namespace
 
 void set_gemm_impl(int impl) { g_gemm_impl = impl; }
@@ -200,7 +208,7 @@ void launch_gemm_bf16(const bf16* A, int64_t lda, const bf16* W, int M, int N, i
 
 void launch_attn_bf16(const AttnBf16Args& a, int64_t rows, cudaStream_t st) {
   if (rows <= 0) return;
-  if (g_attn_impl == 1) launch_attn_tc(a, rows, st);
+  if (g_attn_impl >= 1) launch_attn_tc(a, rows, st, g_attn_impl);
   else launch_attn_simt(a, rows, st);
 }
 

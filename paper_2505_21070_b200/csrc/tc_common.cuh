@@ -178,6 +178,85 @@ __device__ __forceinline__ void mma_bf16_ts_elect(uint32_t tmem_d, uint32_t tmem
       "}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// A whole K=128 chain (8 x K=16) of SS MMAs from one elected lane. Operands
+// are 128-byte-swizzled K-major tiles stored as two 64-element halves: step
+// kk advances a descriptor by 32 B (2 units) inside a half and jumps by the
+// half stride (AH / BH, in 16-byte units) every 4 steps. One elect and no
+// per-step address arithmetic outside the asm keeps the issuing warp cheap.
+template <uint32_t AH, uint32_t BH>
+__device__ __forceinline__ void mma_ss_k128_elect(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t;\n"
+      ".reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.b32 t, 0, 0;\n"
+      "add.s64 a1, %1, 2;  add.s64 b1, %2, 2;\n"
+      "add.s64 a2, %1, 4;  add.s64 b2, %2, 4;\n"
+      "add.s64 a3, %1, 6;  add.s64 b3, %2, 6;\n"
+      "add.s64 a4, %1, %5; add.s64 b4, %2, %6;\n"
+      "add.s64 a5, a4, 2;  add.s64 b5, b4, 2;\n"
+      "add.s64 a6, a4, 4;  add.s64 b6, b4, 4;\n"
+      "add.s64 a7, a4, 6;  add.s64 b7, b4, 6;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, t;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "n"(static_cast<uint64_t>(AH)), "n"(static_cast<uint64_t>(BH)));
+}
+
+// A K=64 chain (4 x K=16) of SS MMAs inside one 128-byte swizzle atom: both
+// descriptors advance by 32 B (2 units) per step.
+__device__ __forceinline__ void mma_ss_k64_elect(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t;\n"
+      ".reg .b64 a1, a2, a3, b1, b2, b3;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.b32 t, 0, 0;\n"
+      "add.s64 a1, %1, 2; add.s64 b1, %2, 2;\n"
+      "add.s64 a2, %1, 4; add.s64 b2, %2, 4;\n"
+      "add.s64 a3, %1, 6; add.s64 b3, %2, 6;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// A K=64 chain (4 x K=16) of TS MMAs: A from TMEM (8 columns per step), B an
+// MN-major smem tile advancing BSTEP 16-byte units per step.
+template <uint32_t BSTEP>
+__device__ __forceinline__ void mma_ts_k64_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t;\n"
+      ".reg .b32 x1, x2, x3;\n"
+      ".reg .b64 b1, b2, b3;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.b32 t, 0, 0;\n"
+      "add.u32 x1, %1, 8;  add.u32 x2, %1, 16; add.u32 x3, %1, 24;\n"
+      "add.s64 b1, %2, %5; add.s64 b2, b1, %5; add.s64 b3, b2, %5;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x1], b1, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x2], b2, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x3], b3, %3, t;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate), "n"(static_cast<uint64_t>(BSTEP)));
+}
+
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n"

@@ -1,6 +1,8 @@
 """Helpers for kernel-level GPU tests (bf16 packing, self-test wrappers)."""
 import ctypes as C
 
+import os
+
 import numpy as np
 
 
@@ -47,3 +49,7 @@ def ref_attn(q, k, v, heads, dh, scale):
         p /= p.sum(axis=1, keepdims=True)
         out[:, sl] = p @ v[:, sl].astype(np.float64)
     return out
+
+
+# the library's default attention implementation (kernels_bf16.cu), restored after A/B tests
+DEFAULT_ATTN_IMPL = int(os.environ.get("BP_ATTN_IMPL", "2"))

@@ -2,7 +2,7 @@
 import numpy as np
 import pytest
 
-from kernels import attn, from_bf16_bits, gemm, ref_attn, to_bf16_bits
+from kernels import DEFAULT_ATTN_IMPL, attn, from_bf16_bits, gemm, ref_attn, to_bf16_bits
 
 pytestmark = pytest.mark.gpu
 
@@ -61,9 +61,12 @@ def test_gemm_bench(lib):
         print(f"gemm {M}x{N}x{K}: {ms.value:.3f} ms  {tf:.0f} TFLOP/s")
 
 
+@pytest.mark.parametrize("impl", [1, 2])
 @pytest.mark.parametrize("rows,n0,n1,heads", [(128, 0, 128, 1), (300, 0, 300, 2), (300, 200, 300, 2),
-                                              (257, 256, 129, 2), (96, 0, 512, 3), (1000, 640, 1000, 1)])
-def test_attention_tcgen05(lib, rows, n0, n1, heads):
+                                              (257, 256, 129, 2), (96, 0, 512, 3), (1000, 640, 1000, 1),
+                                              (513, 65, 63, 2), (256, 0, 1, 1), (40, 7, 100, 2)])
+def test_attention_tcgen05(lib, rows, n0, n1, heads, impl):
+    """impl 1: one 128-row Q tile per CTA; impl 2: ping-pong over two Q tiles, 64-key tiles."""
     dh = 128
     rng = np.random.default_rng(rows + n0 * 3 + n1 + heads)
     H = heads * dh
@@ -76,14 +79,16 @@ def test_attention_tcgen05(lib, rows, n0, n1, heads):
     kk = from_bf16_bits(np.concatenate([k0, k1]) if n0 else k1)
     vv = from_bf16_bits(np.concatenate([v0, v1]) if n0 else v1)
     want = ref_attn(from_bf16_bits(q), kk, vv, heads, dh, scale)
-    lib.bp_set_kernel_impl(1, 1)
-    got = from_bf16_bits(attn(lib, q, k0, v0, k1, v1, heads, dh, scale)).astype(np.float64)
-    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
-    assert rel < 1e-2, rel
-    lib.bp_set_kernel_impl(1, 0)
-    chk = from_bf16_bits(attn(lib, q, k0, v0, k1, v1, heads, dh, scale)).astype(np.float64)
-    lib.bp_set_kernel_impl(1, 1)
-    assert np.linalg.norm(chk - want) / np.linalg.norm(want) < 1e-2
+    lib.bp_set_kernel_impl(1, impl)
+    try:
+        got = from_bf16_bits(attn(lib, q, k0, v0, k1, v1, heads, dh, scale)).astype(np.float64)
+        rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert rel < 1e-2, rel
+        lib.bp_set_kernel_impl(1, 0)
+        chk = from_bf16_bits(attn(lib, q, k0, v0, k1, v1, heads, dh, scale)).astype(np.float64)
+        assert np.linalg.norm(chk - want) / np.linalg.norm(want) < 1e-2
+    finally:
+        lib.bp_set_kernel_impl(1, DEFAULT_ATTN_IMPL)
 
 
 def test_attention_bench(lib):

@@ -1,5 +1,8 @@
 """Kernel micro-benchmarks through the self-test hooks (include/bp_cuda_test.h),
-used for ncu captures: python tools/bench_kernels.py attn|gemm [iters]"""
+used for A/B runs and ncu captures:
+    python tools/bench_kernels.py attn|gemm|all [iters]
+The attention implementation follows BP_ATTN_IMPL (1 = one Q tile per CTA,
+2 = ping-pong over two Q tiles)."""
 import ctypes
 import os
 import sys
@@ -9,10 +12,22 @@ from paper_2505_21070_b200._lib import lib  # noqa: E402
 
 what = sys.argv[1] if len(sys.argv) > 1 else "attn"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+only = sys.argv[3] if len(sys.argv) > 3 else ""  # substring filter on the case tag
 ms = ctypes.c_double()
-if what == "attn":
-    assert lib.bp_bench_attn(0, 18720, 12, 128, 6240, 18720, iters, ctypes.byref(ms)) == 0
-    print("attn ms", ms.value, "TF", 4 * 18720 * 24960 * 1536 / ms.value / 1e9)
-else:
-    assert lib.bp_bench_gemm(0, 18720, 1536, 1536, 2, iters, ctypes.byref(ms)) == 0
-    print("gemm ms", ms.value)
+impl = os.environ.get("BP_ATTN_IMPL", "2")
+if what in ("attn", "all"):
+    # (rows, heads, dh, prefix n0, block n1): prefix pass, plain pass, cross-attention
+    for rows, n0, n1, tag in ((18720, 6240, 18720, "self+prefix"), (18720, 0, 18720, "self"),
+                              (18720, 0, 512, "cross")):
+        if only not in tag:
+            continue
+        assert lib.bp_bench_attn(0, rows, 12, 128, n0, n1, iters, ctypes.byref(ms)) == 0
+        tf = 4 * rows * (n0 + n1) * 1536 / ms.value / 1e9
+        print(f"attn impl={impl} {tag:12s} ms {ms.value:.4f} TF {tf:.1f}")
+if what in ("gemm", "all"):
+    for m, n, k, epi, tag in ((18720, 4608, 1536, 0, "qkv bf16"), (18720, 1536, 1536, 2, "o resid"),
+                              (18720, 8960, 1536, 1, "ffn1 gelu"), (18720, 1536, 8960, 2, "ffn2 resid")):
+        if only not in tag:
+            continue
+        assert lib.bp_bench_gemm(0, m, n, k, epi, iters, ctypes.byref(ms)) == 0
+        print(f"gemm {tag:10s} {m}x{n}x{k} ms {ms.value:.4f} TF {2 * m * n * k / ms.value / 1e9:.1f}")
