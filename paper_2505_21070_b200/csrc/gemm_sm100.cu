@@ -1,6 +1,8 @@
 // tcgen05 GEMM for the DiT projections (K5a-K5f): C[M,N] = A[M,K] . W[N,K]^T
 // with bf16 operands, fp32 accumulation in TMEM and fused epilogues (bf16
-// store, erf-GELU, fp32 residual add). Persistent kernel, one CTA per SM:
+// store, erf-GELU, fp32 residual add). Two variants (launch_gemm_tc): the
+// default k_gemm_pair (2-CTA clusters sharing the weight tile, smem-transposed
+// epilogue; see its comment) and k_gemm_tc below. Persistent, one CTA per SM:
 //   warp 0      TMA producer (one elected lane) into a 4-stage smem ring
 //   warp 1      MMA issuer (one elected lane), 128x256x16 UMMA, TMEM alloc
 //   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> global
@@ -174,6 +176,197 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---- cluster-pair variant -------------------------------------------------------------
+// The two CTAs of a (2,1,1) cluster compute vertically adjacent 128x256 tiles
+// (m-blocks 2p, 2p+1) that share one weight tile. Each CTA loads its own A
+// tile and one half (128 rows) of the weight tile, multicast into both CTAs'
+// shared memory, so the L2->SM bytes per k-block and CTA drop from 48 KB to
+// 32 KB (the 128x256 tile alone needs ~96 B/cycle/SM at the MMA rate). A stage
+// is refilled only after both CTAs' MMAs consumed it: `empty` counts two
+// arrivals and every MMA commit is multicast to both CTAs. Row results do not
+// depend on which CTA computes them (same K order, no split-K), so cached ==
+// recompute still holds bitwise.
+//
+// Epilogue: each 32-row x 32-column chunk goes TMEM -> registers (thread =
+// row) -> a 4 KB per-warp smem slab (16-byte units XOR-swizzled by row) ->
+// back with threads along columns, so every global load/store covers whole
+// 128-byte rows (4 rows fp32, 8 rows bf16) instead of 32 scattered 16-byte
+// pieces: the L1 work per tile drops 8x, which is what bounded the K = 1536
+// residual GEMMs.
+constexpr uint32_t B_HALF = B_BYTES / 2;
+constexpr uint32_t PAIR_STAGING = STAGES * (A_BYTES + B_BYTES) + 256;  // after the ring + mbarriers
+constexpr uint32_t PAIR_SMEM_BYTES = PAIR_STAGING + 4 * 4096 + 1024;
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_gemm_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bh, int M, int N,
+                int K, void* __restrict__ Cv, int64_t ldc) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* staging = smem + PAIR_STAGING;  // 4 epilogue warps x 4 KB
+
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int rank = static_cast<int>(tc::cluster_ctarank());
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int m_pairs = ((M + BM - 1) / BM + 1) / 2;
+  const int total = n_tiles * m_pairs;
+  const int num_k = (K + BK - 1) / BK;
+  constexpr uint16_t kBoth = 0x3;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&map_a);
+    tc::tma_prefetch(&map_bh);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 2);  // both CTAs' MMAs
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 128);
+    }
+    tc::fence_mbarrier_init_cluster();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();  // barrier inits visible to the peer before any remote arrive / multicast
+  tc::fence_after_sync();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- TMA producer: own A tile + own half of the shared weight tile (multicast) ----
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int pair = cluster; pair < total; pair += nclusters) {
+      const int m_blk = (pair / n_tiles) * 2 + rank, n_blk = pair % n_tiles;
+      for (int kb = 0; kb < num_k; ++kb) {
+        tc::mbar_wait(&empty[stage], phase ^ 1);
+        tc::mbar_arrive_expect_tx_elect(&full[stage], A_BYTES + B_BYTES);
+        tc::tma_load_2d_elect(sa + stage * A_BYTES, &map_a, &full[stage], kb * BK, m_blk * BM);
+        tc::tma_load_2d_multicast_elect(sb + stage * B_BYTES + rank * B_HALF, &map_bh, &full[stage], kb * BK,
+                                        n_blk * BN + rank * (BN / 2), kBoth);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer ---------------------------------------------------------------------
+    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int pair = cluster; pair < total; pair += nclusters) {
+      tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc::fence_after_sync();
+      const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+      for (int kb = 0; kb < num_k; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
+        tc::fence_after_sync();
+        const uint32_t a0 = tc::smem_u32(sa + stage * A_BYTES);
+        const uint32_t b0 = tc::smem_u32(sb + stage * B_BYTES);
+        tc::mma_ss_k64_elect(d, tc::desc_sw128(a0, 1024, 16), tc::desc_sw128(b0, 1024, 16), idesc, kb ? 1u : 0u);
+        tc::mma_commit_multicast_elect(&empty[stage], kBoth);  // frees the stage in both CTAs
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      tc::mma_commit_elect(&tfull[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else {
+    // ---- epilogue (warps 2..5 -> TMEM lane quarters 2,3,0,1), transposed through smem ----
+    const int q = warp & 3;
+    const uint32_t slab = tc::smem_u32(staging + (warp - 2) * 4096);
+    auto slab_addr = [&](int row, int unit) {
+      return slab + static_cast<uint32_t>(row * 128 + ((unit ^ (row & 7)) << 4));
+    };
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int pair = cluster; pair < total; pair += nclusters) {
+      const int m_blk = (pair / n_tiles) * 2 + rank, n_blk = pair % n_tiles;
+      const int row0 = m_blk * BM + q * 32;  // this warp's 32 rows
+      tc::mbar_wait(&tfull[acc], acc_phase);
+      tc::fence_after_sync();
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tc::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c), r);
+        tc::tmem_ld_wait();
+        const int col0 = n_blk * BN + c;
+        if (EPI == kGemmStoreBf16 || EPI == kGemmGeluBf16) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+            if (EPI == kGemmGeluBf16) { x0 = gelu_erf_f(x0); x1 = gelu_erf_f(x1); }
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
+            pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            tc::st_shared_v4(slab_addr(lane, u), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {  // 8 rows x 64 bytes per instruction
+            const int rr = 8 * i + (lane >> 2), u = lane & 3;
+            const uint4 v = tc::ld_shared_v4(slab_addr(rr, u));
+            const int grow = row0 + rr, gcol = col0 + u * 8;
+            if (grow < M && gcol < N)
+              *reinterpret_cast<uint4*>(static_cast<bf16*>(Cv) + static_cast<int64_t>(grow) * ldc + gcol) = v;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            tc::st_shared_v4(slab_addr(lane, u), r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]);
+          __syncwarp();
+          float4 old[8];
+          if (EPI == kGemmResidualF32) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {  // 4 rows x 128 bytes per instruction
+              const int rr = 4 * i + (lane >> 3), gcol = col0 + (lane & 7) * 4;
+              if (row0 + rr < M && gcol < N)
+                old[i] = *reinterpret_cast<const float4*>(static_cast<float*>(Cv) + static_cast<int64_t>(row0 + rr) * ldc +
+                                                          gcol);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = 4 * i + (lane >> 3), u = lane & 7;
+            const uint4 v = tc::ld_shared_v4(slab_addr(rr, u));
+            float4 o = make_float4(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w));
+            const int grow = row0 + rr, gcol = col0 + u * 4;
+            if (grow < M && gcol < N) {
+              if (EPI == kGemmResidualF32) {
+                o.x = old[i].x + o.x; o.y = old[i].y + o.y; o.z = old[i].z + o.z; o.w = old[i].w + o.w;
+              }
+              *reinterpret_cast<float4*>(static_cast<float*>(Cv) + static_cast<int64_t>(grow) * ldc + gcol) = o;
+            }
+          }
+        }
+        __syncwarp();  // the slab is rewritten by the next chunk
+      }
+      tc::fence_before_sync();
+      tc::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();  // the peer may still multicast into / arrive on this CTA's shared memory until here
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<512>(tmem_base);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::mutex g_map_mu;
 
@@ -194,6 +387,19 @@ struct MapKeyHash {
   }
 };
 std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+template <int EPI>
+void launch_pair(const CUtensorMap& ma, const CUtensorMap& mbh, int M, int N, int K, void* C, int64_t ldc,
+                 cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    BP_CUDA(cudaFuncSetAttribute(k_gemm_pair<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM_BYTES));
+    configured = true;
+  }
+  const int pairs = (((M + BM - 1) / BM + 1) / 2) * ((N + BN - 1) / BN);
+  const int clusters = pairs < kNumSms / 2 ? pairs : kNumSms / 2;
+  k_gemm_pair<EPI><<<2 * clusters, kThreads, PAIR_SMEM_BYTES, st>>>(ma, mbh, M, N, K, C, ldc);
+}
 
 template <int EPI>
 void launch_epi(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, void* C, int64_t ldc,
@@ -242,12 +448,24 @@ static const CUtensorMap& cached_map(const void* p, uint64_t rows, uint64_t cols
 }
 
 void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C, int64_t ldc, int epi,
-                    cudaStream_t st) {
+                    cudaStream_t st, int variant) {
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15)
     fail(BP_ERR_INTERNAL, "GEMM operands must be 16-byte aligned");
   if ((lda * 2) % 16 || (K * 2) % 16 || N % 32 || ldc % 8)
     fail(BP_ERR_INTERNAL, "GEMM strides must be 16-byte multiples and N % 32 == 0");
   const CUtensorMap ma = cached_map(A, static_cast<uint64_t>(M), static_cast<uint64_t>(K), static_cast<uint64_t>(lda), BM, BK);
+  if (variant == 2) {  // cluster pair sharing the weight tile (128-row weight boxes)
+    const CUtensorMap mbh =
+        cached_map(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(K), BN / 2, BK);
+    switch (epi) {
+      case kGemmStoreBf16: launch_pair<kGemmStoreBf16>(ma, mbh, M, N, K, C, ldc, st); break;
+      case kGemmGeluBf16: launch_pair<kGemmGeluBf16>(ma, mbh, M, N, K, C, ldc, st); break;
+      case kGemmResidualF32: launch_pair<kGemmResidualF32>(ma, mbh, M, N, K, C, ldc, st); break;
+      default: launch_pair<kGemmStoreF32>(ma, mbh, M, N, K, C, ldc, st); break;
+    }
+    count_launch();
+    return;
+  }
   const CUtensorMap mb = cached_map(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(K), BN, BK);
   switch (epi) {
     case kGemmStoreBf16: launch_epi<kGemmStoreBf16>(ma, mb, M, N, K, C, ldc, st); break;

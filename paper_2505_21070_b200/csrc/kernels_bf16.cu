@@ -180,11 +180,17 @@ void launch_attn_simt(const AttnBf16Args& a, int64_t rows, cudaStream_t st) {
 namespace bp {
 
 void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C, int64_t ldc,
-                    int epi, cudaStream_t st);
+                    int epi, cudaStream_t st, int variant);
 void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int variant);
 
 namespace {
-int g_gemm_impl = 1;  // 0 = SIMT check path, 1 = tcgen05
+// GEMM: 0 = SIMT check path, 1 = tcgen05 one CTA per tile, 2 = tcgen05 cluster
+// pair sharing the weight tile. BP_GEMM_IMPL overrides the default.
+int default_gemm_impl() {
+  const char* e = std::getenv("BP_GEMM_IMPL");
+  return e ? std::atoi(e) : 2;
+}
+int g_gemm_impl = default_gemm_impl();
 // 0 = SIMT check path, 1 = tcgen05 one Q tile/CTA, 2 = tcgen05 ping-pong.
 // BP_ATTN_IMPL overrides the default (A/B runs of the whole suite).
 int default_attn_impl() {
@@ -202,7 +208,7 @@ int attn_impl() { return g_attn_impl; }
 void launch_gemm_bf16(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C, int64_t ldc,
                       int epi, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
-  if (g_gemm_impl == 1) launch_gemm_tc(A, lda, W, M, N, K, C, ldc, epi, st);
+  if (g_gemm_impl >= 1) launch_gemm_tc(A, lda, W, M, N, K, C, ldc, epi, st, g_gemm_impl);
   else launch_gemm_simt(A, lda, W, M, N, K, C, ldc, epi, st);
 }
 

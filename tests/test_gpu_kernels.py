@@ -2,7 +2,7 @@
 import numpy as np
 import pytest
 
-from kernels import DEFAULT_ATTN_IMPL, attn, from_bf16_bits, gemm, ref_attn, to_bf16_bits
+from kernels import DEFAULT_ATTN_IMPL, DEFAULT_GEMM_IMPL, attn, from_bf16_bits, gemm, ref_attn, to_bf16_bits
 
 pytestmark = pytest.mark.gpu
 
@@ -11,13 +11,15 @@ pytestmark = pytest.mark.gpu
 def lib(bp):
     from paper_2505_21070_b200._lib import lib as L
     yield L
-    L.bp_set_kernel_impl(1, 1)
+    L.bp_set_kernel_impl(DEFAULT_GEMM_IMPL, DEFAULT_ATTN_IMPL)
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 512, 128), (1000, 1536, 1536), (257, 4608, 256),
                                    (64, 96, 64), (130, 8960, 128)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
-def test_gemm_tcgen05(lib, M, N, K, epi):
+@pytest.mark.parametrize("impl", [1, 2])
+def test_gemm_tcgen05(lib, M, N, K, epi, impl):
+    """impl 1: one CTA per 128x256 tile; impl 2: 2-CTA cluster sharing the weight tile (multicast)."""
     rng = np.random.default_rng(M * 7 + N + K + epi)
     A = to_bf16_bits(rng.standard_normal((M, K)))
     W = to_bf16_bits(rng.standard_normal((N, K)) / np.sqrt(K))
@@ -26,7 +28,7 @@ def test_gemm_tcgen05(lib, M, N, K, epi):
         C0 = np.zeros((M, N), dtype=np.uint16)
     else:
         C0 = rng.standard_normal((M, N)).astype(np.float32)
-    lib.bp_set_kernel_impl(1, 1)
+    lib.bp_set_kernel_impl(impl, DEFAULT_ATTN_IMPL)
     got = gemm(lib, A, W, C0, epi)
     if epi == 1:
         from scipy.special import erf
@@ -36,21 +38,40 @@ def test_gemm_tcgen05(lib, M, N, K, epi):
     g = from_bf16_bits(got).astype(np.float64) if epi in (0, 1) else got.astype(np.float64)
     rel = np.linalg.norm(g - want) / np.linalg.norm(want)
     assert rel < (5e-3 if epi in (0, 1) else 1e-5), rel
-    lib.bp_set_kernel_impl(0, 1)
+    lib.bp_set_kernel_impl(0, DEFAULT_ATTN_IMPL)
     chk = gemm(lib, A, W, C0, epi)
-    lib.bp_set_kernel_impl(1, 1)
+    lib.bp_set_kernel_impl(DEFAULT_GEMM_IMPL, DEFAULT_ATTN_IMPL)
     c = from_bf16_bits(chk).astype(np.float64) if epi in (0, 1) else chk.astype(np.float64)
     assert np.linalg.norm(g - c) / np.linalg.norm(c) < (5e-3 if epi in (0, 1) else 1e-5)
 
 
-def test_gemm_row_position_invariance(lib):
-    """A row's result does not depend on its M position (cached == recompute)."""
+@pytest.mark.parametrize("impl", [1, 2])
+def test_gemm_row_position_invariance(lib, impl):
+    """A row's result does not depend on its M position (cached == recompute),
+    nor on which GEMM implementation or cluster CTA computed it."""
+    lib.bp_set_kernel_impl(impl, DEFAULT_ATTN_IMPL)
     rng = np.random.default_rng(5)
     A = to_bf16_bits(rng.standard_normal((700, 384)))
     W = to_bf16_bits(rng.standard_normal((768, 384)) / 20)
     full = gemm(lib, A, W, np.zeros((700, 768), dtype=np.uint16), 0)
     part = gemm(lib, np.ascontiguousarray(A[333:333 + 97]), W, np.zeros((97, 768), dtype=np.uint16), 0)
+    lib.bp_set_kernel_impl(DEFAULT_GEMM_IMPL, DEFAULT_ATTN_IMPL)
     assert np.array_equal(full[333:333 + 97], part)
+
+
+@pytest.mark.parametrize("epi", [0, 2])
+def test_gemm_implementations_bitwise_equal(lib, epi):
+    """Both tcgen05 GEMMs run the same MMA sequence per tile: identical bits."""
+    rng = np.random.default_rng(11 + epi)
+    A = to_bf16_bits(rng.standard_normal((1000, 512)))
+    W = to_bf16_bits(rng.standard_normal((1536, 512)) / 20)
+    C0 = np.zeros((1000, 1536), dtype=np.uint16) if epi == 0 else rng.standard_normal((1000, 1536)).astype(np.float32)
+    out = []
+    for impl in (1, 2):
+        lib.bp_set_kernel_impl(impl, DEFAULT_ATTN_IMPL)
+        out.append(gemm(lib, A, W, C0, epi))
+    lib.bp_set_kernel_impl(DEFAULT_GEMM_IMPL, DEFAULT_ATTN_IMPL)
+    assert np.array_equal(out[0], out[1])
 
 
 def test_gemm_bench(lib):
@@ -79,21 +100,21 @@ def test_attention_tcgen05(lib, rows, n0, n1, heads, impl):
     kk = from_bf16_bits(np.concatenate([k0, k1]) if n0 else k1)
     vv = from_bf16_bits(np.concatenate([v0, v1]) if n0 else v1)
     want = ref_attn(from_bf16_bits(q), kk, vv, heads, dh, scale)
-    lib.bp_set_kernel_impl(1, impl)
+    lib.bp_set_kernel_impl(DEFAULT_GEMM_IMPL, impl)
     try:
         got = from_bf16_bits(attn(lib, q, k0, v0, k1, v1, heads, dh, scale)).astype(np.float64)
         rel = np.linalg.norm(got - want) / np.linalg.norm(want)
         assert rel < 1e-2, rel
-        lib.bp_set_kernel_impl(1, 0)
+        lib.bp_set_kernel_impl(DEFAULT_GEMM_IMPL, 0)
         chk = from_bf16_bits(attn(lib, q, k0, v0, k1, v1, heads, dh, scale)).astype(np.float64)
         assert np.linalg.norm(chk - want) / np.linalg.norm(want) < 1e-2
     finally:
-        lib.bp_set_kernel_impl(1, DEFAULT_ATTN_IMPL)
+        lib.bp_set_kernel_impl(DEFAULT_GEMM_IMPL, DEFAULT_ATTN_IMPL)
 
 
 def test_attention_bench(lib):
     ms = __import__("ctypes").c_double()
-    lib.bp_set_kernel_impl(1, 1)
+    lib.bp_set_kernel_impl(DEFAULT_GEMM_IMPL, DEFAULT_ATTN_IMPL)
     for (rows, n0, n1) in [(18720, 6240, 18720), (18720, 0, 512)]:
         assert lib.bp_bench_attn(0, rows, 12, 128, n0, n1, 5, ms) == 0, lib.bp_last_error()
         tf = 4 * rows * (n0 + n1) * 12 * 128 / (ms.value * 1e-3) / 1e12
