@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(128, 1) k_floor(int reps, unsigned long long* 
     const uint32_t a = tc::smem_u32(smem), b = tc::smem_u32(smem + 32768);
     const uint32_t id128 = tc::idesc_bf16(128, 128, 0, 0), id256 = tc::idesc_bf16(128, 256, 0, 0);
     const uint32_t idv = tc::idesc_bf16(128, 128, 0, 1);
+    const uint32_t id64 = tc::idesc_bf16(128, 64, 0, 0);
     long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
 #pragma unroll
@@ -49,6 +50,8 @@ __global__ void __launch_bounds__(128, 1) k_floor(int reps, unsigned long long* 
           tc::mma_bf16_ts_elect(tmem + 128, tmem + 384 + kk * 8, vd, idv, 1u);
         }
         if constexpr (mode == 4) tc::mma_bf16_ts_elect(tmem + 128, tmem + 384 + kk * 8, vd, idv, 1u);  // TS MN-major
+        if constexpr (mode == 5) tc::mma_bf16_ss_elect(tmem, ad, bd, id64, 1u);                   // SS N=64
+        if constexpr (mode == 6) tc::mma_bf16_ts_elect(tmem, tmem + 384 + kk * 8, bd, id64, 1u);  // TS N=64
       }
     }
     tc::mma_commit_elect(&bar);
@@ -83,16 +86,18 @@ __global__ void k_packed(const float2* x, float2* y, float s, float m) {
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 8);
-  void (*kern[5])(int, unsigned long long*) = {k_floor<0>, k_floor<1>, k_floor<2>, k_floor<3>, k_floor<4>};
-  const char* names[] = {"SS 128x128x16", "TS 128x128x16", "SS 128x256x16", "SS+TS pairs", "TS MN-major B"};
-  for (int mode = 0; mode < 5; ++mode) {
+  void (*kern[7])(int, unsigned long long*) = {k_floor<0>, k_floor<1>, k_floor<2>, k_floor<3>,
+                                                k_floor<4>, k_floor<5>, k_floor<6>};
+  const char* names[] = {"SS 128x128x16", "TS 128x128x16", "SS 128x256x16", "SS+TS pairs", "TS MN-major B",
+                         "SS 128x64x16", "TS 128x64x16"};
+  for (int mode = 0; mode < 7; ++mode) {
     cudaFuncSetAttribute(kern[mode], cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     const int reps = mode == 3 ? 1000 : 2000;
     for (int it = 0; it < 2; ++it) kern[mode]<<<148, 128, 100 * 1024>>>(reps, d);
     cudaError_t e = cudaDeviceSynchronize();
     unsigned long long cyc = 0;
     cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
-    const int n = mode == 2 ? 256 : 128;
+    const int n = mode == 2 ? 256 : mode >= 5 ? 64 : 128;
     const double per = static_cast<double>(cyc) / (reps * 8.0 * (mode == 3 ? 2 : 1));
     printf("%-20s %8.2f cyc/mma  floor %d  -> %.1f%% of floor (%s)\n", names[mode], per, 128 * n / 256,
            100.0 * (128.0 * n / 256) / per, cudaGetErrorString(e));
