@@ -44,6 +44,19 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def pipeline_roofline(flops_video, n, peak_tflops, link_bytes_video, s_video):
+    """Whole-pipeline roofline of one video: compute at the sustained bf16
+    peak on N GPUs vs the busiest stage boundary's bytes over one NVLink
+    direction (900 GB/s); frac = that ideal time / the measured time."""
+    compute_s = flops_video / (n * peak_tflops * 1e12)
+    nvlink_s = link_bytes_video / 900e9 if n > 1 else 0.0
+    ideal = max(compute_s, nvlink_s)
+    return {"bound": "tensor" if compute_s >= nvlink_s else "nvlink", "compute_s": compute_s, "nvlink_s": nvlink_s,
+            "ideal_s": ideal, "measured_s": s_video, "frac": ideal / s_video if s_video > 0 else None,
+            "link_bytes_per_video": link_bytes_video, "peak_tflops": peak_tflops, "nvlink_gbs": 900.0,
+            "note": "N = 1 has no stage boundary; the loopback transport keeps every stage on one GPU"}
+
+
 def pass_flops(w, tokens, prefix, reference_algorithm=False):
     """Algorithmic FLOPs of one forward through all layers:
     4 S C h + L [8 S h^2 + 4 S Skv h + 4 S h^2 + 4 S Lc h + 4 S h F] (+ head),
@@ -271,6 +284,12 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     stats = pipe.stats()
+    link_bytes = float(stats["boundary_bytes"])  # this rank's stage-boundary bytes of the last video
+    if dist is not None:
+        import torch
+        t = torch.tensor([link_bytes], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # busiest stage-boundary link
+        link_bytes = float(t.item())
 
     # e2e: the public API with host buffers (emitted latents copied to host
     # and handed to the caller), wall clock per step
@@ -326,6 +345,9 @@ def main():
         "e2e": {"value": statistics.mean(e2e_vals), "unit": "frames/s",
                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h,
                 "note": "noise is drawn on the device from seeds; the host input per step is the config only"},
+        # north_star: the slower of compute at peak and stage-boundary bytes over
+        # NVLink (900 GB/s per direction) bounds the whole pipeline
+        "pipeline_roofline": pipeline_roofline(fl_video, n, peak, link_bytes, s_video),
         "gpu_launches": int(statistics.mean(lib_launch)),
         "clocks": clk.summary(),
         "build_s": build_s,
