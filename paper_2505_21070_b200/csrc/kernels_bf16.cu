@@ -9,6 +9,7 @@
 
 #include "device.cuh"
 #include "kernels_bf16.cuh"
+#include "kernels_simt.cuh"
 
 namespace bp {
 
@@ -52,13 +53,137 @@ __global__ void __launch_bounds__(256) k_ln_bf16(const float* __restrict__ x, in
   }
 }
 
+// Same statistics in the same order as k_ln_bf16, with the row held in
+// registers: one global read per element (k_ln_bf16 reads the row three
+// times) and all NV loads in flight at once. NV = hidden / 128.
+template <int NV>
+__global__ void __launch_bounds__(256) k_ln_bf16_reg(const float* __restrict__ x, int64_t ldx,
+                                                     const float* __restrict__ g, const float* __restrict__ b,
+                                                     int64_t rows, int n, bf16* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const float4* x4 = reinterpret_cast<const float4*>(x + r * ldx);
+  float4 v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = x4[lane + 32 * i];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / static_cast<float>(n);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const float a = v[i].x - mean, bb = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
+    q += (a * a + bb * bb) + (c * c + d * d);
+  }
+  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float inv = 1.0f / sqrtf(q / static_cast<float>(n) + 1e-5f);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+  uint2* y2 = reinterpret_cast<uint2*>(y + r * n);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int j = lane + 32 * i;
+    const float4 gg = g4[j], bbv = b4[j];
+    const float o0 = (v[i].x - mean) * inv * gg.x + bbv.x;
+    const float o1 = (v[i].y - mean) * inv * gg.y + bbv.y;
+    const float o2 = (v[i].z - mean) * inv * gg.z + bbv.z;
+    const float o3 = (v[i].w - mean) * inv * gg.w + bbv.w;
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(o0, o1), h1 = __floats2bfloat162_rn(o2, o3);
+    y2[j] = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+  }
+}
+
 void launch_ln_bf16(const float* x, int64_t ldx, const float* g, const float* b, int64_t rows,
                     int n, bf16* y, cudaStream_t st) {
   if (rows <= 0) return;
   if (n % 4 != 0 || ldx % 4 != 0) fail(BP_ERR_CONFIG, "bf16 path needs hidden % 4 == 0");
-  const int64_t blocks = (rows + 7) / 8;
-  k_ln_bf16<<<static_cast<unsigned>(blocks), 256, 0, st>>>(x, ldx, g, b, rows, n, y);
+  const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
+  switch (n) {  // register-resident rows for the hidden sizes in use (Wan 1.3B / 14B, test models)
+    case 128: k_ln_bf16_reg<1><<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
+    case 256: k_ln_bf16_reg<2><<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
+    case 512: k_ln_bf16_reg<4><<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
+    case 1536: k_ln_bf16_reg<12><<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
+    case 5120: k_ln_bf16_reg<40><<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
+    default: k_ln_bf16<<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
+  }
   count_launch();
+}
+
+// ---- embeddings for the fp32 residual stream (bf16 / f32 modes) ----------------------
+// x[r, 2k] = sin(pos*f_k) + sin(tpos*f_k), x[r, 2k+1] = cos(..) + cos(..) with
+// pos = frame_id*tpf + t (model.cpp:155-169), by angle addition: sin/cos(t*f_k)
+// comes from a per-stage table, sin/cos(frame_id*tpf*f_k) and the timestep
+// terms once per frame. The split argument differs from fl(pos*f_k) by at most
+// an ulp of ~4e5 rad (~6e-11), far below the fp32 output's resolution; the fp64
+// parity mode keeps the exact per-element k_embed.
+__global__ void k_embed_frames(const double* __restrict__ freq, const int32_t* __restrict__ levels,
+                               const int64_t* __restrict__ frame_ids, int nframes, int hk, int tpf,
+                               double4* __restrict__ ftab) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nframes * hk) return;
+  const int f = i / hk, k = i - f * hk;
+  const double fr = freq[k];
+  const double a = __dmul_rn(static_cast<double>(frame_ids[f] * tpf), fr);
+  const double at = __dmul_rn(static_cast<double>(static_cast<int64_t>(levels[f]) + 1000000), fr);
+  double sa, ca, st, ct;
+  sincos(a, &sa, &ca);
+  sincos(at, &st, &ct);
+  ftab[i] = make_double4(sa, ca, st, ct);
+}
+
+__global__ void k_embed_table(const double* __restrict__ freq, int hk, int tpf, double2* __restrict__ ttab) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= tpf * hk) return;
+  const int t = i / hk, k = i - t * hk;
+  double s, c;
+  sincos(__dmul_rn(static_cast<double>(t), freq[k]), &s, &c);
+  ttab[i] = make_double2(s, c);
+}
+
+__global__ void k_embed_pos(const double2* __restrict__ ttab, const double4* __restrict__ ftab, int64_t tokens,
+                            int hk, int tpf, float2* __restrict__ x) {
+  const int64_t total = tokens * hk;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / hk;
+    const int k = static_cast<int>(e - r * hk);
+    const int f = static_cast<int>(r / tpf), t = static_cast<int>(r - static_cast<int64_t>(f) * tpf);
+    const double2 tb = ttab[static_cast<int64_t>(t) * hk + k];
+    const double4 fa = ftab[static_cast<int64_t>(f) * hk + k];
+    const double pe_s = fma(fa.x, tb.y, fa.y * tb.x);   // sin(A + B)
+    const double pe_c = fma(fa.y, tb.y, -fa.x * tb.x);  // cos(A + B)
+    x[e] = make_float2(static_cast<float>(pe_s + fa.z), static_cast<float>(pe_c + fa.w));
+  }
+}
+
+void launch_embed_table(const double* freq, int h, int tpf, double* ttab, cudaStream_t st) {
+  const int hk = h / 2, n = tpf * hk;
+  k_embed_table<<<(n + 255) / 256, 256, 0, st>>>(freq, hk, tpf, reinterpret_cast<double2*>(ttab));
+  count_launch();
+}
+
+void launch_embed_fast(const double* lat, const float* w_in32, const double* freq, const double* ttab,
+                       double* ftab, const int32_t* levels, const int64_t* frame_ids, int64_t tokens, int C, int h,
+                       int tpf, float* lat32, float* x, cudaStream_t st) {
+  if (tokens <= 0) return;
+  if (h % 2) fail(BP_ERR_CONFIG, "embedding needs an even hidden size");
+  const int hk = h / 2;
+  const int nframes = static_cast<int>(tokens / tpf);
+  k_embed_frames<<<(nframes * hk + 255) / 256, 256, 0, st>>>(freq, levels, frame_ids, nframes, hk, tpf,
+                                                             reinterpret_cast<double4*>(ftab));
+  count_launch();
+  const int64_t total = tokens * hk;
+  const int64_t want = (total + 255) / 256;
+  k_embed_pos<<<static_cast<unsigned>(want < kNumSms * 16 ? want : kNumSms * 16), 256, 0, st>>>(
+      reinterpret_cast<const double2*>(ttab), reinterpret_cast<const double4*>(ftab), tokens, hk, tpf,
+      reinterpret_cast<float2*>(x));
+  count_launch();
+  launch_convert<double, float>(lat, lat32, tokens * C, st);
+  // x += lat @ w_in (fp32 SIMT GEMM, residual epilogue)
+  launch_matmul<float>(lat32, C, w_in32, h, static_cast<int>(tokens), h, C, x, h, kEpiResidual, x, h, st);
 }
 
 __device__ __forceinline__ float gelu_erf(float v) {

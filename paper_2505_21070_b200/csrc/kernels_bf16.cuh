@@ -12,6 +12,13 @@ namespace bp {
 using bf16 = __nv_bfloat16;
 
 // ln_affine (model.cpp:32-41): fp32 x [rows, n] -> bf16 y, fp32 stats.
+// Embedding into the fp32 residual stream (bf16 path): per-stage table of
+// (sin, cos)(t * f_k), t < tpf (ttab: tpf * h/2 double2), then per pass the
+// per-frame terms (ftab: frames * h/2 double4) and x = pe + te + lat @ w_in.
+void launch_embed_table(const double* freq, int h, int tpf, double* ttab, cudaStream_t st);
+void launch_embed_fast(const double* lat, const float* w_in32, const double* freq, const double* ttab,
+                       double* ftab, const int32_t* levels, const int64_t* frame_ids, int64_t tokens, int C, int h,
+                       int tpf, float* lat32, float* x, cudaStream_t st);
 void launch_ln_bf16(const float* x, int64_t ldx, const float* g, const float* b, int64_t rows,
                     int n, bf16* y, cudaStream_t st);
 

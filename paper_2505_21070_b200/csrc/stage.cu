@@ -166,6 +166,13 @@ void Stage::build_weights(uint64_t seed_model, uint64_t seed_context) {
   for (size_t i = 0; i < fr.size(); ++i) fr[i] = std::pow(10000.0, -2.0 * static_cast<double>(i) / h_);
   freq_.alloc(fr.size() * 8);
   BP_CUDA(cudaMemcpyAsync(freq_.p, fr.data(), fr.size() * 8, cudaMemcpyHostToDevice, st));
+  if (is_first() && prec_ == BP_PREC_BF16) {
+    w_in32_.alloc(static_cast<size_t>(C_) * h_ * 4);
+    launch_convert<double, float>(static_cast<const double*>(w_in_), w_in32_.as<float>(),
+                                  static_cast<int64_t>(C_) * h_, st);
+    ttab_.alloc(static_cast<size_t>(tpf_) * (h_ / 2) * 16);
+    launch_embed_table(freq_.as<double>(), h_, tpf_, ttab_.as<double>(), st);
+  }
   BP_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -280,6 +287,10 @@ void Stage::ensure_workspace(int64_t tokens, int64_t capture) {
     cq_.alloc(S * H * me);
     hmid_.alloc(S * static_cast<size_t>(F_) * me);
     eps_.alloc(S * static_cast<size_t>(C_) * te);
+    if (bf && is_first()) {
+      ftab_.alloc((S / static_cast<size_t>(tpf_) + 1) * static_cast<size_t>(h_ / 2) * 32);
+      lat32_.alloc(S * static_cast<size_t>(C_) * 4);
+    }
     cap_tokens_ = tokens;
   }
   // per-parity buffers: only the set written by this pass may be resized,
@@ -480,8 +491,9 @@ const void* Stage::forward_bf16(const StageInput& in) {
   bf16* cq = cq_.as<bf16>();
   bf16* hm = hmid_.as<bf16>();
   if (is_first()) {
-    launch_embed<float>(static_cast<const double*>(in.payload), static_cast<const double*>(w_in_),
-                        freq_.as<double>(), in.d_levels, in.d_frame_ids, S, C_, h_, tpf_, x, st);
+    launch_embed_fast(static_cast<const double*>(in.payload), w_in32_.as<float>(), freq_.as<double>(),
+                      ttab_.as<double>(), ftab_.as<double>(), in.d_levels, in.d_frame_ids, S, C_, h_, tpf_,
+                      lat32_.as<float>(), x, st);
   } else {
     BP_CUDA(cudaMemcpyAsync(x, in.payload, static_cast<size_t>(S * H) * 4, cudaMemcpyDeviceToDevice, st));
   }

@@ -120,6 +120,9 @@ class Stage {
   void* w_in_ = nullptr;   // fp64 [C, h]
   void* w_out_ = nullptr;  // T [h, C] (fp32 on the bf16 path)
   DevBuf freq_;            // fp64 [h/2] embedding frequencies
+  DevBuf w_in32_;          // fp32 [C, h] (bf16 path)
+  DevBuf ttab_;            // (sin, cos)(t * f_k), [tpf][h/2] double2 (bf16 path)
+  DevBuf ftab_, lat32_;    // per-pass frame terms / fp32 latents (bf16 path)
 
   // workspace
   int64_t cap_tokens_ = 0, cap_capture_ = 0;
