@@ -34,6 +34,12 @@ WORKLOADS = {
     1: dict(WAN13, blocks=3, frames=81, name="Wan2.1-1.3B-shape 81f 480p (BASELINE configs[1])"),
     "multi": dict(WAN13, blocks=9, frames=301, name="Wan2.1-1.3B-shape 301f 480p (BASELINE configs[2])"),
 }
+# BASELINE configs[4] (14B, 1025 frames 720p, 8 GPUs): the 8-stage layer split
+# on one GPU through the loopback transport, over a bounded sample of the
+# schedule (2 blocks x 2 denoising steps = 4 passes at full 720p width).
+WAN14 = dict(layers=40, hidden=5120, heads=40, ffn=13824, channels=64, height=45, width=80, context_len=512,
+             num_b=8, num_c=8, steps=2, blocks=2, frames=None, devices=8,
+             name="Wan2.1-14B-shape 720p, 8-stage split on 1 GPU (BASELINE configs[4] sample: 2 blocks x 2 steps)")
 
 
 def load_peaks():
@@ -176,6 +182,62 @@ def cpu_baseline(w, sched, threads=None, tokens_per_sample=16):
             "s_per_video_extrapolated": sec_video}
 
 
+def run_wan14b(args):
+    """Memory / feature-cache stress leg for configs[4]: all eight stages of
+    the 14B layer split (5 layers each) resident on one GPU, S = 43200 tokens,
+    Skv = 57600 on prefix passes. Reports seconds per pass, model TFLOP/s,
+    peak HBM, and the configs[4] video time this rate implies on 8 GPUs
+    (labelled a projection: schedule-aware makespan 1656 slots of one
+    5-layer stage)."""
+    import paper_2505_21070_b200 as bp
+    w = WAN14
+    cfg = bp.PipelineConfig(devices=w["devices"], precision="bf16", layers=w["layers"], hidden=w["hidden"],
+                            heads=w["heads"], ffn=w["ffn"], channels=w["channels"], height=w["height"],
+                            width=w["width"], context_len=w["context_len"], num_b=w["num_b"], num_c=w["num_c"],
+                            steps=w["steps"], blocks=w["blocks"], transport="loopback")
+    sched = bp.Schedule(cfg)
+    fl_sample, n_prefix = video_flops(w, sched)
+    t0 = time.perf_counter()
+    pipe = bp.Pipeline(cfg)
+    build_s = time.perf_counter() - t0
+    for _ in range(max(1, args.warmup)):
+        pipe.run_device()
+    ms = []
+    with ClockSampler(0) as clk:
+        for _ in range(max(1, args.steps)):
+            pipe.run_device()
+            ms.append(pipe.stats()["gpu_ms"])
+    st = pipe.stats()
+    s_sample = statistics.mean(ms) / 1e3
+    rate = fl_sample / s_sample
+    # configs[4]: 32 blocks x 50 steps = 1600 passes; 8 even stages; makespan
+    # T*B + N(N-1) = 1656 slots (SURVEY 8d), one slot = one stage pass
+    full = dict(w, steps=50, blocks=32)
+    tpf = w["height"] * w["width"]
+    S, P = (w["num_b"] + w["num_c"] // 2) * tpf, (w["num_c"] // 2) * tpf
+    f_pass = pass_flops(full, S, P)
+    slots = 50 * 32 + 8 * 7
+    proj = slots * (f_pass / 8) / rate
+    peaks, _ = load_peaks()
+    print(json.dumps({
+        "metric": "s per pass, Wan2.1-14B-shape 720p (configs[4] sample)", "value": s_sample / sched.npasses,
+        "unit": "s/pass", "higher_is_better": False, "n_gpus": 1, "steps": max(1, args.steps),
+        "warmup": max(1, args.warmup), "dtype": "bf16", "data": "synthetic (random-init 14B-shape weights)",
+        "config": {"workload": w["name"], "layers": w["layers"], "hidden": w["hidden"], "heads": w["heads"],
+                   "ffn": w["ffn"], "latent_grid": [w["height"], w["width"], w["channels"]],
+                   "tokens_per_pass": S, "prefix_tokens": P, "passes": sched.npasses, "prefix_passes": n_prefix,
+                   "stages": w["devices"]},
+        "s_per_sample": s_sample, "model_tflops": rate / 1e12,
+        "frac_of_sustained_peak": rate / 1e12 / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
+        "peak_hbm_gb": st["peak_bytes"] / 1e9,
+        "peak_hbm_note": "all eight 5-layer stages (weights, workspaces, KV caches) resident on this one GPU",
+        "build_s": build_s,
+        "projected_cfg4_8gpu_s_per_video": {"value": proj, "slots": slots, "flop_per_pass": f_pass,
+                                            "note": "projection from this measured rate: 1656 slots x one 5-layer "
+                                                    "stage pass; not a multi-GPU measurement"},
+        "gpu_launches": st["kernel_launches"], "clocks": clk.summary()}))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -183,7 +245,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="auto", choices=["auto", "wan14b"],
+                    help="auto: configs[1] at N=1, configs[2] at N>1; wan14b: the configs[4] sample leg")
     args = ap.parse_args()
+    if args.workload == "wan14b":
+        return run_wan14b(args)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -291,10 +357,19 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)  # busiest stage-boundary link
         link_bytes = float(t.item())
 
-    # e2e: the public API with host buffers (emitted latents copied to host
-    # and handed to the caller), wall clock per step
+    # e2e: the public API with host buffers. Rank 0 hands the engine the
+    # reference's noise pool from pinned host memory (bp_pipeline_set_pool;
+    # uploaded host->device inside every run) and receives every emitted
+    # block's latents back in host memory; wall clock per step, max over ranks.
+    pool = None
+    if rank == 0:
+        m = w["num_b"] + w["num_c"] // 2
+        pool = bp.pinned_empty((m, w["height"], w["width"], w["channels"]))
+        pool[...] = bp.build_pool(w["num_b"], w["num_c"], (w["height"], w["width"], w["channels"]),
+                                  bp.derive_seed(cfg.seed_noise, [0]), device=local)
+        pipe.set_pool(pool)
     e2e_vals = []
-    d2h = 0
+    h2d = d2h = 0
     for _ in range(max(1, min(args.steps, 2))):
         barrier()
         t0 = time.perf_counter()
@@ -307,7 +382,10 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
         e2e_vals.append(w["frames"] / dt)
-        d2h = sum(b["frames"].nbytes for b in blocks) if blocks and blocks[0]["frames"] is not None else 0
+        est = pipe.stats()
+        h2d, d2h = est["h2d_bytes"], est["d2h_bytes"]
+    if pool is not None:
+        pipe.set_pool(None)
 
     if rank != 0:
         return
@@ -343,8 +421,9 @@ def main():
                      "whole_step_frac": fl_video / s_video / 1e12 / peak},
         "cpu_baseline": cpu,
         "e2e": {"value": statistics.mean(e2e_vals), "unit": "frames/s",
-                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h,
-                "note": "noise is drawn on the device from seeds; the host input per step is the config only"},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "note": "wall clock per video through bp_pipeline_run: the noise pool uploaded from pinned host "
+                        "memory (bp_pipeline_set_pool) and every emitted block copied back to host"},
         # north_star: the slower of compute at peak and stage-boundary bytes over
         # NVLink (900 GB/s per direction) bounds the whole pipeline
         "pipeline_roofline": pipeline_roofline(fl_video, n, peak, link_bytes, s_video),

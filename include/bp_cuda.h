@@ -251,6 +251,8 @@ typedef struct {
   double attn_ms, gemm_ms;  /* per-class device time when profiling is enabled */
   double cross_ms;          /* cross-attention device time (profiling)             */
   int64_t attn_launches, gemm_launches, cross_launches;
+  int64_t h2d_bytes;        /* host->device bytes of the last run (host-supplied pool) */
+  int64_t d2h_bytes;        /* device->host bytes of the last run (emitted latents)   */
 } bp_pipeline_stats;
 BP_API bp_status bp_pipeline_get_stats(bp_pipeline* p, bp_pipeline_stats* out);
 /* Per-kernel-class timing with CUDA events on the launching stream (0/1). */
@@ -259,6 +261,16 @@ BP_API bp_status bp_pipeline_set_profiling(bp_pipeline* p, int32_t on);
 BP_API int64_t bp_pipeline_ntrace(bp_pipeline* p);
 BP_API bp_status bp_pipeline_trace(bp_pipeline* p, int64_t i, int64_t* round, int64_t* block_id,
                             int64_t* rows, int64_t* cols, double* eps /* may be NULL */);
+/* Host-supplied noise pool: replaces build_pool(seed_noise) (noise.cpp:26-48,
+ * engine.cpp:288-290) with M = num_b + num_c/2 caller entries of
+ * height*width*channels fp64 values in id order (the layout bp_noise_pool
+ * writes). The buffer is borrowed: it must stay valid for every later run,
+ * which uploads it host->device and applies the reference's pairwise
+ * collision check. NULL restores the seeded device pool. Rank 0 only. */
+BP_API bp_status bp_pipeline_set_pool(bp_pipeline* p, const double* host_pool, int64_t count);
+/* Page-locked host memory for pools and emission buffers (cudaMallocHost). */
+BP_API bp_status bp_host_alloc(int64_t bytes, void** out);
+BP_API bp_status bp_host_free(void* p);
 /* Device pointer + element count of emitted block i's latents (fp64). */
 BP_API bp_status bp_pipeline_block(bp_pipeline* p, int64_t i, const double** dev_data, int64_t* count);
 

@@ -74,7 +74,8 @@ class ChunkOut(C.Structure):
 class PipelineStats(C.Structure):
     _fields_ = [("gpu_ms", f64), ("passes", i64), ("kernel_launches", i64), ("peak_bytes", i64),
                 ("boundary_bytes", i64), ("attn_ms", f64), ("gemm_ms", f64), ("cross_ms", f64),
-                ("attn_launches", i64), ("gemm_launches", i64), ("cross_launches", i64)]
+                ("attn_launches", i64), ("gemm_launches", i64), ("cross_launches", i64),
+                ("h2d_bytes", i64), ("d2h_bytes", i64)]
 
 
 EMIT_FN = C.CFUNCTYPE(None, C.c_void_p, i64, i64, P(f64), P(i32), i32, P(i64))
@@ -122,6 +123,9 @@ _SIGS = {
     "bp_pipeline_ntrace": (i64, [C.c_void_p]),
     "bp_pipeline_trace": (i32, [C.c_void_p, i64, P(i64), P(i64), P(i64), P(i64), P(f64)]),
     "bp_pipeline_block": (i32, [C.c_void_p, i64, P(P(f64)), P(i64)]),
+    "bp_pipeline_set_pool": (i32, [C.c_void_p, P(f64), i64]),
+    "bp_host_alloc": (i32, [i64, P(C.c_void_p)]),
+    "bp_host_free": (i32, [C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

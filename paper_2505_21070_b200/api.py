@@ -252,6 +252,32 @@ def coordinated_noise_ids(num_b: int, num_c: int, appends: int, seed: int = 2) -
     return [b["noise_ids"] for b in s.blocks]
 
 
+class _Pinned:
+    def __init__(self, nbytes: int):
+        self.ptr = C.c_void_p()
+        check(lib.bp_host_alloc(nbytes, C.byref(self.ptr)))
+        self.nbytes = nbytes
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                lib.bp_host_free(self.ptr)
+        except Exception:
+            pass
+
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """A numpy array over page-locked host memory (cudaMallocHost); the
+    allocation lives as long as the array (its base buffer holds it)."""
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape))
+    nbytes = max(1, n * dt.itemsize)
+    mem = _Pinned(nbytes)
+    buf = (C.c_uint8 * nbytes).from_address(mem.ptr.value)
+    buf._bp_pinned = mem
+    return np.frombuffer(buf, dtype=dt, count=n).reshape(shape)
+
+
 # ---- engine.hpp: the pipeline ---------------------------------------------------------------
 class Pipeline:
     """run_pipeline (engine.cpp:255-497) on B200: build once, run many times."""
@@ -299,6 +325,21 @@ class Pipeline:
         cb = EMIT_FN(_cb)
         check(lib.bp_pipeline_run(self._h, cb, None))
         return blocks
+
+    def set_pool(self, pool: Optional[np.ndarray]) -> None:
+        """Host-supplied noise pool (replaces build_pool(seed_noise),
+        noise.cpp:26-48): M = num_b + num_c/2 entries in id order, fp64, the
+        layout build_pool returns. Each later run uploads it host->device
+        (pass a pinned_empty() array for a DMA-speed copy). None restores the
+        seeded device pool."""
+        if pool is None:
+            self._pool = None
+            check(lib.bp_pipeline_set_pool(self._h, C.cast(None, C.POINTER(f64)), 0))
+            return
+        if pool.dtype != np.float64 or not pool.flags["C_CONTIGUOUS"]:
+            raise TypeError("pool must be a C-contiguous float64 array")
+        self._pool = pool  # borrowed by the engine for every later run
+        check(lib.bp_pipeline_set_pool(self._h, _ptr(pool, f64), pool.size))
 
     def run_device(self) -> None:
         """One whole generation with the emitted latents left in HBM (no

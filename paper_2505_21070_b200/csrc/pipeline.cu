@@ -38,6 +38,7 @@ class Pipeline {
   std::vector<const double*> block_dev;    // emitted blocks' device latents (rank 0)
   std::vector<int64_t> block_count;
   bool profiling = false;
+  const double* host_pool = nullptr;       // borrowed caller pool (bp_pipeline_set_pool)
 
  private:
   void run_rank0_loopback(bp_emit_fn emit, void* user);
@@ -172,7 +173,12 @@ double* Pipeline::version_ptr(int64_t block, int version) const {
 void Pipeline::build_pool_and_check(cudaStream_t st) {
   const int M = d_.num_b + d_.num_c / 2;
   const uint64_t tag0 = 0;
-  launch_normal_fill(derive_seed(d_.seed_noise, &tag0, 1), M * hwc_, 1.0, pool_.as<double>(), st);
+  if (host_pool) {
+    BP_CUDA(cudaMemcpyAsync(pool_.p, host_pool, static_cast<size_t>(M * hwc_) * 8, cudaMemcpyHostToDevice, st));
+    stats.h2d_bytes += M * hwc_ * 8;
+  } else {
+    launch_normal_fill(derive_seed(d_.seed_noise, &tag0, 1), M * hwc_, 1.0, pool_.as<double>(), st);
+  }
   if (M > 1) {
     BP_CUDA(cudaMemsetAsync(flags_.p, 0, static_cast<size_t>(M) * M * 4, st));
     launch_pool_differs(pool_.as<double>(), M, hwc_, flags_.as<int>(), st);
@@ -243,8 +249,10 @@ void Pipeline::emit_block(const SchedBlock& b, cudaStream_t st, bool to_host) {
   const double* src = version_ptr(b.id, d_.steps);
   block_dev.push_back(src);
   block_count.push_back(b.frames * hwc_);
-  if (to_host)
+  if (to_host) {
     BP_CUDA(cudaMemcpyAsync(pinned_[k], src, static_cast<size_t>(b.frames * hwc_) * 8, cudaMemcpyDeviceToHost, st));
+    stats.d2h_bytes += b.frames * hwc_ * 8;
+  }
 }
 
 // DeviceWorker::process cache checks (engine.cpp:142-171) before the forward.
@@ -301,6 +309,7 @@ void Pipeline::run(bp_emit_fn emit, void* user) {
   block_count.clear();
   fault_pending_ = d_.fault_inject_ulp != 0;
   launches_at_start_ = g_launches.load();
+  stats.h2d_bytes = stats.d2h_bytes = 0;
   for (auto& s : stages_)
     if (s) s->set_profiling(profiling);
   if (d_.transport == BP_TRANSPORT_NCCL && d_.devices > 1) run_nccl(emit, user);
@@ -564,6 +573,30 @@ bp_status bp_pipeline_trace(bp_pipeline* p, int64_t i, int64_t* round, int64_t* 
     *cols = p->p->sched.desc.model.channels;
     if (eps) std::memcpy(eps, p->p->trace[static_cast<size_t>(i)].data(), p->p->trace[static_cast<size_t>(i)].size() * 8);
   });
+}
+
+bp_status bp_pipeline_set_pool(bp_pipeline* p, const double* host_pool, int64_t count) {
+  return bp::guarded([&] {
+    if (!p) bp::fail(BP_ERR_CONFIG, "null pipeline");
+    const bp_pipeline_desc& d = p->p->sched.desc;
+    const int64_t want = static_cast<int64_t>(d.num_b + d.num_c / 2) * d.model.height * d.model.width *
+                         d.model.channels;
+    if (host_pool && count != want)
+      bp::fail(BP_ERR_DIMENSION, "pool holds " + std::to_string(count) + " values, the queue needs " +
+                                     std::to_string(want) + " (M = num_b + num_c/2 entries)");
+    p->p->host_pool = host_pool;
+  });
+}
+
+bp_status bp_host_alloc(int64_t bytes, void** out) {
+  return bp::guarded([&] {
+    if (!out || bytes < 0) bp::fail(BP_ERR_CONFIG, "bad host allocation request");
+    BP_CUDA(cudaMallocHost(out, static_cast<size_t>(bytes > 0 ? bytes : 1)));
+  });
+}
+
+bp_status bp_host_free(void* ptr) {
+  return bp::guarded([&] { if (ptr) BP_CUDA(cudaFreeHost(ptr)); });
 }
 
 bp_status bp_pipeline_block(bp_pipeline* p, int64_t i, const double** dev_data, int64_t* count) {

@@ -293,12 +293,15 @@ void Stage::ensure_workspace(int64_t tokens, int64_t capture) {
     }
     cap_tokens_ = tokens;
   }
-  // per-parity buffers: only the set written by this pass may be resized,
-  // the other holds the resident cache of the previous pass
-  qkv_[parity_].reserve(nl * S * 3 * H * me);
-  if (capture > 0) {
-    recbuf_[parity_].reserve(nl * P * H * te);
-    capcopy_[parity_].reserve(nl * P * 2 * H * me);
+  qkv_.reserve(S * 3 * H * me);
+  // the recording is written before the previous one is read: per parity
+  if (capture > 0) recbuf_[parity_].reserve(nl * P * H * te);
+  // The KV cache of pass n is read by pass n+1's attention of layer l before
+  // that pass overwrites layer l's entry, so one buffer suffices; a growth
+  // keeps the old allocation alive until the next growth.
+  if (capture > 0 && nl * P * 2 * H * me > cap_.bytes) {
+    cap_old_ = std::move(cap_);
+    cap_.alloc(nl * P * 2 * H * me);
   }
   if (capture > cap_capture_ || rec_.tokens > cap_capture_ || cache_.tokens > cap_capture_) {
     const int64_t p = std::max({capture, rec_.tokens, cache_.tokens, cap_capture_});
@@ -306,6 +309,28 @@ void Stage::ensure_workspace(int64_t tokens, int64_t capture) {
     lnp_.alloc(static_cast<size_t>(p) * H * me);
     cap_capture_ = p;
   }
+}
+
+// take_rows(k|v, capture rows) into the layer's cache entry (model.cpp:302-318,
+// 321-322): after this layer's attention has read the previous entry, the
+// captured K|V rows are copied out of the QKV buffer into [capture][2h].
+// Runs of consecutive capture frames move with one launch.
+void Stage::capture_kv(const StageInput& in, int li, const void* qkv, size_t eb, Entry* nc) {
+  const int64_t H = h_, P = static_cast<int64_t>(in.capture_frames.size()) * tpf_;
+  char* dst = cap_.as<char>() + static_cast<int64_t>(li) * P * 2 * H * static_cast<int64_t>(eb);
+  const char* src = static_cast<const char*>(qkv);
+  const int64_t rs = 3 * H * static_cast<int64_t>(eb), rd = 2 * H * static_cast<int64_t>(eb);
+  size_t f = 0;
+  while (f < in.capture_frames.size()) {
+    size_t g = f + 1;
+    while (g < in.capture_frames.size() && in.capture_frames[g] == in.capture_frames[g - 1] + 1) ++g;
+    launch_copy_rows(src + static_cast<int64_t>(in.capture_frames[f]) * tpf_ * rs + H * static_cast<int64_t>(eb), rs,
+                     dst + static_cast<int64_t>(f) * tpf_ * rd, rd, static_cast<int64_t>(g - f) * tpf_, rd, stream_);
+    f = g;
+  }
+  nc->k.push_back(dst);
+  nc->v.push_back(dst + H * static_cast<int64_t>(eb));
+  nc->ld = 2 * H;
 }
 
 void Stage::kv_prefix_from_recording(int li, const void* rec_rows, int64_t rows, void* kv_out) {
@@ -370,17 +395,11 @@ const void* Stage::forward_simt(const StageInput& in) {
   } else {
     BP_CUDA(cudaMemcpyAsync(x, in.payload, static_cast<size_t>(S * H) * sizeof(T), cudaMemcpyDeviceToDevice, st));
   }
-  bool contiguous = true;
-  for (size_t i = 1; i < in.capture_frames.size(); ++i)
-    contiguous &= in.capture_frames[i] == in.capture_frames[i - 1] + 1;
-  const int64_t row0 = capturing ? static_cast<int64_t>(in.capture_frames[0]) * tpf_ : 0;
-
   Entry nc, nr;
-  T* qkv_set = qkv_[parity_].as<T>();
+  T* qkv = qkv_.as<T>();
   for (int li = 0; li < nl; ++li) {
     const LayerW& w = lw_[static_cast<size_t>(li)];
     const T* lnw = static_cast<const T*>(w.ln);
-    T* qkv = qkv_set + static_cast<int64_t>(li) * S * 3 * H;
     if (new_rec) {  // recorded->layer_inputs += take_rows(x, capture_rows) (model.cpp:295)
       T* dst = recbuf_[parity_].as<T>() + static_cast<int64_t>(li) * P * H;
       for (size_t f = 0; f < in.capture_frames.size(); ++f)
@@ -423,22 +442,7 @@ const void* Stage::forward_simt(const StageInput& in) {
     a.dh = dh_;
     a.scale = static_cast<T>(1.0 / std::sqrt(static_cast<double>(dh_)));
     launch_attention<T>(a, S, heads_, st);
-    if (new_cache) {  // captured K,V rows stay where this pass wrote them
-      if (contiguous) {
-        nc.k.push_back(qkv + row0 * 3 * H + H);
-        nc.v.push_back(qkv + row0 * 3 * H + 2 * H);
-        nc.ld = 3 * H;
-      } else {
-        T* dst = capcopy_[parity_].as<T>() + static_cast<int64_t>(li) * P * 2 * H;
-        for (size_t f = 0; f < in.capture_frames.size(); ++f)
-          launch_copy_rows(qkv + static_cast<int64_t>(in.capture_frames[f]) * tpf_ * 3 * H + H,
-                           3 * H * sizeof(T), dst + static_cast<int64_t>(f) * tpf_ * 2 * H,
-                           2 * H * sizeof(T), tpf_, 2 * H * sizeof(T), st);
-        nc.k.push_back(dst);
-        nc.v.push_back(dst + H);
-        nc.ld = 2 * H;
-      }
-    }
+    if (new_cache) capture_kv(in, li, qkv, sizeof(T), &nc);
     launch_matmul<T>(at, H, static_cast<const T*>(w.wo), H, static_cast<int>(S), h_, h_, x, H,
                      kEpiResidual, x, H, st);
     // cross-attention against the hoisted context K|V
@@ -497,18 +501,13 @@ const void* Stage::forward_bf16(const StageInput& in) {
   } else {
     BP_CUDA(cudaMemcpyAsync(x, in.payload, static_cast<size_t>(S * H) * 4, cudaMemcpyDeviceToDevice, st));
   }
-  bool contiguous = true;
-  for (size_t i = 1; i < in.capture_frames.size(); ++i)
-    contiguous &= in.capture_frames[i] == in.capture_frames[i - 1] + 1;
-  const int64_t row0 = capturing ? static_cast<int64_t>(in.capture_frames[0]) * tpf_ : 0;
   const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(dh_)));
 
   Entry nc, nr;
-  bf16* qkv_set = qkv_[parity_].as<bf16>();
+  bf16* qkv = qkv_.as<bf16>();
   for (int li = 0; li < nl; ++li) {
     const LayerW& w = lw_[static_cast<size_t>(li)];
     const float* lnw = static_cast<const float*>(w.ln);
-    bf16* qkv = qkv_set + static_cast<int64_t>(li) * S * 3 * H;
     if (new_rec) {
       float* dst = recbuf_[parity_].as<float>() + static_cast<int64_t>(li) * P * H;
       for (size_t f = 0; f < in.capture_frames.size(); ++f)
@@ -554,21 +553,7 @@ const void* Stage::forward_bf16(const StageInput& in) {
     prof_mark(0, true);
     launch_attn_bf16(a, S, st);
     prof_mark(0, false);
-    if (new_cache) {
-      if (contiguous) {
-        nc.k.push_back(qkv + row0 * 3 * H + H);
-        nc.v.push_back(qkv + row0 * 3 * H + 2 * H);
-        nc.ld = 3 * H;
-      } else {
-        bf16* dst = capcopy_[parity_].as<bf16>() + static_cast<int64_t>(li) * P * 2 * H;
-        for (size_t f = 0; f < in.capture_frames.size(); ++f)
-          launch_copy_rows(qkv + static_cast<int64_t>(in.capture_frames[f]) * tpf_ * 3 * H + H, 3 * H * 2,
-                           dst + static_cast<int64_t>(f) * tpf_ * 2 * H, 2 * H * 2, tpf_, 2 * H * 2, st);
-        nc.k.push_back(dst);
-        nc.v.push_back(dst + H);
-        nc.ld = 2 * H;
-      }
-    }
+    if (new_cache) capture_kv(in, li, qkv, 2, &nc);
     prof_mark(2, true);
     launch_gemm_bf16(at, H, static_cast<const bf16*>(w.wo), static_cast<int>(S), h_, h_, x, H,
                      kGemmResidualF32, st);

@@ -107,6 +107,7 @@ class Stage {
   int host_kind_ = 0;
   void ensure_workspace(int64_t tokens, int64_t capture_tokens);
   void kv_prefix_from_recording(int li, const void* rec_rows, int64_t rows, void* kv_out);
+  void capture_kv(const StageInput& in, int li, const void* qkv, size_t eb, Entry* nc);
 
   int device_, prec_;
   bp_model_desc m_;
@@ -127,9 +128,10 @@ class Stage {
   // workspace
   int64_t cap_tokens_ = 0, cap_capture_ = 0;
   DevBuf x_, ln_, attn_, cq_, hmid_, eps_, kvp_, lnp_;
-  DevBuf qkv_[2];          // [L_local][tokens][3h] per parity
-  DevBuf recbuf_[2];       // [L_local][capture][h] per parity
-  DevBuf capcopy_[2];      // [L_local][capture][2h] (non-contiguous captures)
+  DevBuf qkv_;             // [tokens][3h], reused by every layer
+  DevBuf recbuf_[2];       // [L_local][capture][h] per parity (written before the old one is read)
+  DevBuf cap_, cap_old_;   // KV feature cache [L_local][capture][2h]; cap_old_ keeps a
+                           // replaced allocation alive for the pass that still reads it
   DevBuf scratch_;         // audit
   int parity_ = 0;
   Entry cache_, rec_;

@@ -161,3 +161,78 @@ def test_scheduler_step_closed_form(bp):  # test_model.cpp:270-298
 def test_pool_720p_bit_exact(bp, ref):
     seed = bp.derive_seed(2, [0])
     assert np.array_equal(bp.build_pool(8, 8, (45, 80, 64), seed), ref.pool(8, 8, (45, 80, 64), seed))
+
+
+def test_host_supplied_pool(bp):
+    """bp_pipeline_set_pool: the reference's own pool handed in from pinned
+    host memory gives bitwise the seeded run; a wrong size is a
+    DimensionError and a pool with two equal entries fails build_pool's
+    collision check (noise.cpp:38-46) with a ConfigError."""
+    cfg = bp.PipelineConfig.from_dict(dict(G["mid"]["config"], precision="f64"))
+    want = bp.run_pipeline(cfg)
+    p = bp.Pipeline(cfg)
+    m = cfg.num_b + cfg.num_c // 2
+    pool = bp.pinned_empty((m, cfg.height, cfg.width, cfg.channels))
+    pool[...] = bp.build_pool(cfg.num_b, cfg.num_c, (cfg.height, cfg.width, cfg.channels),
+                              bp.derive_seed(cfg.seed_noise, [0]))
+    p.set_pool(pool)
+    got = p.run()
+    assert all(np.array_equal(x["frames"], y["frames"]) for x, y in zip(got, want["blocks"]))
+    st = p.stats()
+    assert st["h2d_bytes"] == pool.nbytes
+    assert st["d2h_bytes"] == sum(b["frames"].nbytes for b in got)
+    with pytest.raises(bp.DimensionError):
+        p.set_pool(np.zeros(7))
+    dup = pool.copy()
+    dup[1] = dup[0]
+    p.set_pool(dup)
+    with pytest.raises(bp.ConfigError):
+        p.run()
+    p.set_pool(None)
+    again = p.run()
+    assert all(np.array_equal(x["frames"], y["frames"]) for x, y in zip(again, want["blocks"]))
+
+
+def _two_passes(stage_or_ref, is_ref, x0, x1):
+    """A capture pass then a prefix pass (the cached-context route)."""
+    if is_ref:
+        a = stage_or_ref.forward(x0, [7, 7], [0, 1], capture=[1], mode="on")
+        b = stage_or_ref.forward(x1, [6, 6], [1, 2], mode="on", use_prev=1)
+        return a, b
+    a = stage_or_ref.forward_chunk(x0, [7, 7], [0, 1], capture_frames=[1], mode="on")["payload"]
+    b = stage_or_ref.forward_chunk(x1, [6, 6], [1, 2], mode="on", use_prev=1)["payload"]
+    return a, b
+
+
+def test_wan13_width_stage_vs_reference(bp, ref):
+    """One Wan2.1-1.3B-width layer (h 1536, 12 heads, dh 128, C 64, 4h FFN)
+    as a whole chunk (entry embedding + layer + head), a capture pass and a
+    cached-prefix pass, through bp_forward_chunk vs the reference library:
+    fp64 <= 1e-12, fp32 <= 1e-4, bf16 tensor-core path <= 2e-2."""
+    cfg = bp.PipelineConfig(layers=1, hidden=1536, heads=12, channels=64, height=2, width=4, context_len=64)
+    rng = np.random.default_rng(3)
+    x0, x1 = rng.standard_normal((16, 64)), rng.standard_normal((16, 64))
+    want = _two_passes(ref.RefChunk(cfg, 5, 0, 1, 6), True, x0, x1)
+    for prec, tol in (("f64", 1e-12), ("f32", 1e-4), ("bf16", 2e-2)):
+        got = _two_passes(bp.Stage(cfg, 5, 0, 1, 6, precision=prec), False, x0, x1)
+        for g, w_ in zip(got, want):
+            assert rel(g, w_) <= tol, (prec, rel(g, w_))
+
+
+def test_wan14b_width_stage(bp):
+    """Wan2.1-14B width (h 5120, 40 heads, FFN 13824) as two chunks of a
+    2-layer model: bf16 and fp32 vs the fp64 GPU path (itself pinned to the
+    reference at <= 1e-12), chunked == monolithic bitwise in bf16."""
+    cfg = bp.PipelineConfig(layers=2, hidden=5120, heads=40, ffn=13824, channels=64, height=2, width=4,
+                            context_len=64)
+    rng = np.random.default_rng(4)
+    x0, x1 = rng.standard_normal((16, 64)), rng.standard_normal((16, 64))
+    base = _two_passes(bp.Stage(cfg, 5, 0, 2, 6, precision="f64"), False, x0, x1)
+    for prec, tol in (("f32", 1e-4), ("bf16", 2e-2)):
+        got = _two_passes(bp.Stage(cfg, 5, 0, 2, 6, precision=prec), False, x0, x1)
+        for g, w_ in zip(got, base):
+            assert rel(g, w_) <= tol, (prec, rel(g, w_))
+    mono = bp.Stage(cfg, 5, 0, 2, 6, precision="bf16").forward_chunk(x0, [7, 7], [0, 1])["payload"]
+    mid = bp.Stage(cfg, 5, 0, 1, 6, precision="bf16").forward_chunk(x0, [7, 7], [0, 1])["payload"]
+    last = bp.Stage(cfg, 5, 1, 2, 6, precision="bf16").forward_chunk(mid, [7, 7], [0, 1])["payload"]
+    assert np.array_equal(mono, last)
