@@ -25,6 +25,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -369,6 +370,7 @@ __device__ __forceinline__ float max3f(float a, float b, float c) {
   return d;
 }
 
+template <int kPoly>
 __global__ void __launch_bounds__(PP_THREADS, 1)
     k_attn_pp(const __grid_constant__ AttnMapsPP maps, int64_t rows, int64_t n0, int64_t n1, float scale_log2,
               bf16* __restrict__ out, int64_t ldo) {
@@ -532,7 +534,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       for (int c = 0; c < 32; ++c) {
         const float2 xv = __ffma2_rn(make_float2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sc2,
                                      neg_m2);
-        const float2 p = (c & 3) == 3 ? ex2_poly2(xv) : make_float2(ex2(xv.x), ex2(xv.y));
+        const float2 p = (c & 3) >= 4 - kPoly ? ex2_poly2(xv) : make_float2(ex2(xv.x), ex2(xv.y));
         if (c & 1) ls_b = __fadd2_rn(ls_b, p);
         else ls_a = __fadd2_rn(ls_a, p);
         pk[c] = pack_bf16(p.x, p.y);
@@ -571,6 +573,294 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       tc::tmem_ld_wait();
       if (row < rows) {
         uint4* dst = reinterpret_cast<uint4*>(out + row * ldo + head * kDh + c * 32);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          dst[v] = make_uint4(pack_bf16(__uint_as_float(o[8 * v]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l),
+                              pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l),
+                              pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l),
+                              pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l));
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<512>(tmem);
+  }
+}
+
+// ============================================================================
+// Variant 3: two query tiles per CTA, 128-key tiles, one S buffer per tile,
+// each S row split across two softmax warps
+// ============================================================================
+// TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512). QK^T is an SS
+// MMA at N = 128, which runs at the tcgen05 floor (8 KB of smem per 64-cycle
+// step, tools/micro/mma_floor.cu); P_x(j) overwrites the first 64 columns of
+// S_x as packed bf16 and feeds PV as the TMEM A operand. The tensor core runs
+//   PV_A(j) QK_A(j+1) PV_B(j) QK_B(j+1) ...
+// so softmax A(j+1) overlaps PV_B(j) + QK_B(j+1) and vice versa; the commit
+// that publishes S_x(j+1) also covers PV_x(j), so an O rescale never waits.
+// The softmax of one tile is latency-bound with one warp per SM sub-partition,
+// so each row is split over two warps that share its TMEM lane quarter: half
+// h owns keys [64h, 64h+64) and O columns [64h, 64h+64); the halves swap
+// their row maxima through shared memory (one 64-thread named barrier per
+// tile, which also orders every S load of the tile before any P store).
+// 640 threads: warpgroup 0 = TMA warp, MMA warp, two idle warps (registers
+// released with setmaxnreg.dec); warpgroups 1-2 = tile A halves 0/1,
+// warpgroups 3-4 = tile B halves 0/1.
+constexpr int FA_BK = 128;
+constexpr int FA_KST = 2, FA_VST = 2;
+constexpr uint32_t FA_Q = 0;                          // Q_A, Q_B (32 KB each)
+constexpr uint32_t FA_K = FA_Q + 2 * TILE;
+constexpr uint32_t FA_V = FA_K + FA_KST * TILE;
+constexpr uint32_t FA_RED = FA_V + FA_VST * TILE;     // [parity][tile][half][128 rows] fp32
+constexpr uint32_t FA_BAR = FA_RED + 2 * 2 * 2 * 128 * 4;
+constexpr uint32_t FA_SMEM_BYTES = FA_BAR + 256 + 1024;
+constexpr int FA_THREADS = 640;
+static_assert(FA_SMEM_BYTES <= 232448, "variant-3 attention exceeds the 227 KB smem limit");
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+__global__ void __launch_bounds__(FA_THREADS, 1)
+    k_attn_fa(const __grid_constant__ AttnMaps maps, int64_t rows, int64_t n0, int64_t n1, float scale_log2,
+              bf16* __restrict__ out, int64_t ldo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + FA_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;              // [FA_KST]
+  uint64_t* k_empty = k_full + FA_KST;      // [FA_KST]
+  uint64_t* v_full = k_empty + FA_KST;      // [FA_VST]
+  uint64_t* v_empty = v_full + FA_VST;      // [FA_VST]
+  uint64_t* s_full = v_empty + FA_VST;      // [tile]
+  uint64_t* p_full = s_full + 2;            // [tile] (256 arrivals)
+  uint64_t* o_full = p_full + 2;            // [tile] final PV done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+  float* red = reinterpret_cast<float*>(smem + FA_RED);
+
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int qpair = blockIdx.x, head = blockIdx.y;
+  const int t0 = static_cast<int>((n0 + FA_BK - 1) / FA_BK);
+  const int t1 = static_cast<int>((n1 + FA_BK - 1) / FA_BK);
+  const int T = t0 + t1;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&maps.q);
+    tc::tma_prefetch(&maps.k1);
+    tc::tma_prefetch(&maps.v1);
+    tc::mbar_init(q_full, 1);
+    for (int s = 0; s < FA_KST; ++s) {
+      tc::mbar_init(&k_full[s], 1);
+      tc::mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < FA_VST; ++s) {
+      tc::mbar_init(&v_full[s], 1);
+      tc::mbar_init(&v_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&s_full[i], 1);
+      tc::mbar_init(&p_full[i], 256);
+      tc::mbar_init(&o_full[i], 1);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    tc::setmaxnreg_dec<32>();
+    if (warp == 0) {
+      // ---- TMA producer -----------------------------------------------------------------
+      tc::mbar_arrive_expect_tx_elect(q_full, 2 * TILE);
+      for (int x = 0; x < 2; ++x) {
+        const int qrow = qpair * 2 * BQ + x * BQ;
+        tc::tma_load_2d_elect(smem + FA_Q + x * TILE, &maps.q, q_full, head * kDh, qrow);
+        tc::tma_load_2d_elect(smem + FA_Q + x * TILE + HALF, &maps.q, q_full, head * kDh + 64, qrow);
+      }
+      for (int j = 0; j < T; ++j) {
+        const bool seg0 = j < t0;
+        const int row0 = (seg0 ? j : j - t0) * FA_BK;
+        const int ks = j % FA_KST, vs = j % FA_VST;
+        tc::mbar_wait(&k_empty[ks], ((j / FA_KST) & 1) ^ 1);
+        uint8_t* kd = smem + FA_K + ks * TILE;
+        const CUtensorMap* mk = seg0 ? &maps.k0 : &maps.k1;
+        tc::mbar_arrive_expect_tx_elect(&k_full[ks], TILE);
+        tc::tma_load_2d_elect(kd, mk, &k_full[ks], head * kDh, row0);
+        tc::tma_load_2d_elect(kd + HALF, mk, &k_full[ks], head * kDh + 64, row0);
+        tc::mbar_wait(&v_empty[vs], ((j / FA_VST) & 1) ^ 1);
+        uint8_t* vd = smem + FA_V + vs * TILE;
+        const CUtensorMap* mv = seg0 ? &maps.v0 : &maps.v1;
+        tc::mbar_arrive_expect_tx_elect(&v_full[vs], TILE);
+        tc::tma_load_2d_elect(vd, mv, &v_full[vs], head * kDh, row0);
+        tc::tma_load_2d_elect(vd + HALF, mv, &v_full[vs], head * kDh + 64, row0);
+      }
+    } else if (warp == 1) {
+      // ---- MMA issuer ---------------------------------------------------------------------
+      constexpr uint32_t idesc_s = tc::idesc_bf16(BQ, FA_BK, 0, 0);  // Q x K^T, both K-major smem
+      constexpr uint32_t idesc_o = tc::idesc_bf16(BQ, kDh, 0, 1);    // P (TMEM) x V (smem, MN-major)
+      const uint32_t q_base = tc::smem_u32(smem + FA_Q);
+      auto qk = [&](int x, int j) {
+        const uint32_t k_addr = tc::smem_u32(smem + FA_K + (j % FA_KST) * TILE);
+        tc::mma_ss_k128_elect<HALF / 16, HALF / 16>(tmem + static_cast<uint32_t>(x * FA_BK),
+                                                    tc::desc_sw128(q_base + x * TILE, 1024, 16),
+                                                    tc::desc_sw128(k_addr, 1024, 16), idesc_s, 0u);
+      };
+      auto pv = [&](int x, int j) {
+        const uint32_t v_addr = tc::smem_u32(smem + FA_V + (j % FA_VST) * TILE);
+        const uint32_t o = tmem + 256u + static_cast<uint32_t>(x * kDh);
+        const uint32_t p = tmem + static_cast<uint32_t>(x * FA_BK);
+        // keys [0,64) then [64,128): 64 rows x 128 B = 8 KB further into each d-half
+        tc::mma_ts_k64_elect<2048 / 16>(o, p, tc::desc_sw128(v_addr, 1024, HALF), idesc_o, j > 0 ? 1u : 0u);
+        tc::mma_ts_k64_elect<2048 / 16>(o, p + 32, tc::desc_sw128(v_addr + 8192, 1024, HALF), idesc_o, 1u);
+      };
+      tc::mbar_wait(q_full, 0);
+      if (T > 0) {
+        tc::mbar_wait(&k_full[0], 0);
+        tc::fence_after_sync();
+        qk(0, 0);
+        tc::mma_commit_elect(&s_full[0]);
+        qk(1, 0);
+        tc::mma_commit_elect(&s_full[1]);
+        tc::mma_commit_elect(&k_empty[0]);
+      }
+      for (int j = 0; j < T; ++j) {
+        const bool more = j + 1 < T;
+        tc::mbar_wait(&v_full[j % FA_VST], (j / FA_VST) & 1);
+        tc::mbar_wait(&p_full[0], j & 1);
+        tc::fence_after_sync();
+        pv(0, j);
+        if (more) {
+          tc::mbar_wait(&k_full[(j + 1) % FA_KST], ((j + 1) / FA_KST) & 1);
+          tc::fence_after_sync();
+          qk(0, j + 1);  // in-order after PV_A(j), which reads P_A(j) from the same columns
+          tc::mma_commit_elect(&s_full[0]);
+        } else {
+          tc::mma_commit_elect(&o_full[0]);
+        }
+        tc::mbar_wait(&p_full[1], j & 1);
+        tc::fence_after_sync();
+        pv(1, j);
+        tc::mma_commit_elect(&v_empty[j % FA_VST]);
+        if (more) {
+          qk(1, j + 1);
+          tc::mma_commit_elect(&s_full[1]);
+          tc::mma_commit_elect(&k_empty[(j + 1) % FA_KST]);
+        } else {
+          tc::mma_commit_elect(&o_full[1]);
+        }
+      }
+    }
+  } else {
+    tc::setmaxnreg_inc<112>();  // pool = 640 x 96 at launch: 32 + 4 x 112 = 480
+    // ---- softmax + epilogue: tile x, key half hf, row r (TMEM lane) ---------------------------
+    const int x = (warp - 4) >> 3;
+    const int hf = ((warp - 4) >> 2) & 1;
+    const int qq = warp & 3;
+    const int r = qq * 32 + lane;
+    const int bar_id = 1 + x * 4 + qq;  // the two warps of this tile and lane quarter
+    const uint32_t lane_off = static_cast<uint32_t>(qq * 32) << 16;
+    const uint32_t tm_s = tmem + lane_off + static_cast<uint32_t>(x * FA_BK);
+    const uint32_t tm_o = tmem + lane_off + 256u + static_cast<uint32_t>(x * kDh + hf * 64);
+    const float2 sc2 = make_float2(scale_log2, scale_log2);
+    float m_used = -INFINITY;
+    float2 l2 = make_float2(0.f, 0.f);
+    const int n0i = static_cast<int>(n0), n1i = static_cast<int>(n1);
+    for (int j = 0; j < T; ++j) {
+      const bool seg0 = j < t0;
+      const int row0 = (seg0 ? j : j - t0) * FA_BK;
+      const int rem = (seg0 ? n0i : n1i) - row0 - hf * 64;  // valid keys in this half
+      tc::mbar_wait(&s_full[x], j & 1);
+      tc::fence_after_sync();
+      uint32_t sr[64];
+      tc::tmem_ld32(tm_s + static_cast<uint32_t>(hf * 64), *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tc::tmem_ld32(tm_s + static_cast<uint32_t>(hf * 64 + 32), *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tc::tmem_ld_wait();
+      if (rem < 64) {  // keys past the segment end (a segment's last tile)
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+          if (c >= rem) sr[c] = __float_as_uint(-INFINITY);
+      }
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 64; c += 8) {
+        m4[0] = max3f(m4[0], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+        m4[1] = max3f(m4[1], __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
+        m4[2] = max3f(m4[2], __uint_as_float(sr[c + 4]), __uint_as_float(sr[c + 5]));
+        m4[3] = max3f(m4[3], __uint_as_float(sr[c + 6]), __uint_as_float(sr[c + 7]));
+      }
+      // swap half-row maxima; the barrier also orders both halves' S loads
+      // before either half's P store (P of half 1 lands in S columns of half 0)
+      float* slot = red + ((j & 1) * 2 + x) * 256;
+      slot[hf * 128 + r] = max3f(m4[0], m4[1], fmaxf(m4[2], m4[3]));
+      tc::fence_before_sync();
+      named_bar_sync(bar_id, 64);
+      tc::fence_after_sync();
+      const float mx = fmaxf(slot[r], slot[128 + r]) * scale_log2;  // scale > 0
+      const bool need = mx > m_used + kRescaleThreshold;
+      const float m_new = need ? mx : m_used;
+      const float corr = need ? ex2(m_used - m_new) : 1.f;  // 0 on the first tile
+      const float2 neg_m2 = make_float2(-m_new, -m_new);
+      float2 ls_a = make_float2(0.f, 0.f), ls_b = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int k = ch * 16 + c;
+          const float2 xv = __ffma2_rn(make_float2(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sc2,
+                                       neg_m2);
+          const float2 p = (c & 3) == 3 ? ex2_poly2(xv) : make_float2(ex2(xv.x), ex2(xv.y));
+          if (c & 1) ls_b = __fadd2_rn(ls_b, p);
+          else ls_a = __fadd2_rn(ls_a, p);
+          pk[c] = pack_bf16(p.x, p.y);
+        }
+        tc::tmem_st16(tm_s + static_cast<uint32_t>(hf * 32 + ch * 16), pk);
+      }
+      l2 = __ffma2_rn(l2, make_float2(corr, corr), __fadd2_rn(ls_a, ls_b));
+      m_used = m_new;
+      // O holds PV_x(j-1): the commit that published S_x(j) covers it
+      if (j >= 1 && __any_sync(0xffffffffu, need)) {
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t o[32];
+          const uint32_t ta = tm_o + static_cast<uint32_t>(c * 32);
+          tc::tmem_ld32(ta, o);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+          tc::tmem_st32(ta, o);
+        }
+      }
+      tc::tmem_st_wait();
+      tc::fence_before_sync();
+      tc::mbar_arrive(&p_full[x]);
+    }
+    // row sum over both halves, through the parity slot tile T-1 did not use
+    // (its last readers passed the barrier of tile T-1 before anyone gets here)
+    float* ls = red + (((T & 1) * 2) + x) * 256;
+    ls[hf * 128 + r] = l2.x + l2.y;
+    named_bar_sync(bar_id, 64);
+    const float l = ls[r] + ls[128 + r];
+    if (T >= 1) {
+      tc::mbar_wait(&o_full[x], 0);
+      tc::fence_after_sync();
+    }
+    const int64_t row = static_cast<int64_t>(qpair) * 2 * BQ + x * BQ + r;
+    const float inv_l = 1.f / l;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t o[32];
+      tc::tmem_ld32(tm_o + static_cast<uint32_t>(c * 32), o);
+      tc::tmem_ld_wait();
+      if (row < rows) {
+        uint4* dst = reinterpret_cast<uint4*>(out + row * ldo + head * kDh + hf * 64 + c * 32);
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           dst[v] = make_uint4(pack_bf16(__uint_as_float(o[8 * v]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l),
@@ -630,7 +920,10 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
   static bool configured = false;
   if (!configured) {
     BP_CUDA(cudaFuncSetAttribute(k_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    BP_CUDA(cudaFuncSetAttribute(k_attn_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_attn_pp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_attn_pp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_attn_pp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_attn_fa, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM_BYTES));
     configured = true;
   }
   AttnMaps maps;
@@ -645,7 +938,10 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     maps.v0 = maps.v1;
   }
   const float scale_log2 = a.scale * 1.4426950408889634f;
-  if (variant == 2) {  // ping-pong: 256 query rows per CTA, 64-key tiles
+  if (variant == 3) {  // two Q tiles per CTA, 128-key tiles, one S buffer per tile
+    dim3 grid(static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(a.heads));
+    k_attn_fa<<<grid, FA_THREADS, FA_SMEM_BYTES, st>>>(maps, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
+  } else if (variant == 2) {  // ping-pong: 256 query rows per CTA, 64-key tiles
     AttnMapsPP pm;
     pm.q = maps.q;
     pm.k1 = map_for(a.k1, a.n1, H, a.ldk1, PBK);
@@ -658,7 +954,14 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
       pm.v0 = pm.v1;
     }
     dim3 grid(static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(a.heads));
-    k_attn_pp<<<grid, PP_THREADS, PP_SMEM_BYTES, st>>>(pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
+    // pairs of exp2 (out of 4) evaluated on the FMA pipe; BP_ATTN_POLY overrides (A/B runs)
+    static const int poly = [] {
+      const char* e = std::getenv("BP_ATTN_POLY");
+      return e ? std::atoi(e) : 1;
+    }();
+    if (poly == 0) k_attn_pp<0><<<grid, PP_THREADS, PP_SMEM_BYTES, st>>>(pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
+    else if (poly == 2) k_attn_pp<2><<<grid, PP_THREADS, PP_SMEM_BYTES, st>>>(pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
+    else k_attn_pp<1><<<grid, PP_THREADS, PP_SMEM_BYTES, st>>>(pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
   } else {
     dim3 grid(static_cast<unsigned>((rows + BQ - 1) / BQ), static_cast<unsigned>(a.heads));
     k_attn_tc<<<grid, kThreads, SMEM_BYTES, st>>>(maps, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);

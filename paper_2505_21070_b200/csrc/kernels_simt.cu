@@ -320,9 +320,29 @@ __global__ void k_copy_rows(const uint32_t* __restrict__ src, int64_t src_ld, ui
   }
 }
 
+// 16-byte rows: a warp-strided row walk, one uint4 per thread per step
+// (the KV-cache capture moves [P, 2h] bf16 out of the [S, 3h] QKV buffer).
+__global__ void k_copy_rows16(const uint4* __restrict__ src, int64_t src_ld, uint4* __restrict__ dst, int64_t dst_ld,
+                              int rows, int vecs) {
+  for (int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < rows; r += gridDim.x * (blockDim.x / 32)) {
+    const uint4* s = src + static_cast<int64_t>(r) * src_ld;
+    uint4* d = dst + static_cast<int64_t>(r) * dst_ld;
+    for (int c = threadIdx.x & 31; c < vecs; c += 32) d[c] = __ldg(s + c);
+  }
+}
+
 void launch_copy_rows(const void* src, int64_t src_ld_bytes, void* dst, int64_t dst_ld_bytes,
                       int64_t rows, int64_t row_bytes, cudaStream_t st) {
   if (rows <= 0 || row_bytes <= 0) return;
+  if (((row_bytes | src_ld_bytes | dst_ld_bytes | reinterpret_cast<uintptr_t>(src) |
+        reinterpret_cast<uintptr_t>(dst)) & 15) == 0 && rows < (1LL << 31)) {
+    const int64_t want = (rows + 7) / 8;
+    k_copy_rows16<<<static_cast<int>(want < kNumSms * 16 ? want : kNumSms * 16), 256, 0, st>>>(
+        static_cast<const uint4*>(src), src_ld_bytes / 16, static_cast<uint4*>(dst), dst_ld_bytes / 16,
+        static_cast<int>(rows), static_cast<int>(row_bytes / 16));
+    count_launch();
+    return;
+  }
   if ((row_bytes | src_ld_bytes | dst_ld_bytes) & 3) fail(BP_ERR_INTERNAL, "copy_rows needs 4-byte rows");
   const int64_t words = row_bytes / 4, total = rows * words;
   const int64_t want = (total + 255) / 256;
