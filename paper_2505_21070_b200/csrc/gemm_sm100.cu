@@ -289,13 +289,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     };
     int acc = 0;
     uint32_t acc_phase = 0;
+    // Residual chunks are fetched two chunks ahead (the first two before the
+    // accumulator is ready): 8 KB in flight per warp keeps HBM busy while
+    // TMEM reads, the smem transpose and the stores of earlier chunks proceed.
+    float4 nA[8], nB[8];
+    auto load_res = [&](float4 (&dst)[8], int row0, int col0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {  // 4 rows x 128 bytes per instruction
+        const int rr = 4 * i + (lane >> 3), gcol = col0 + (lane & 7) * 4;
+        if (row0 + rr < M && gcol < N)
+          dst[i] = *reinterpret_cast<const float4*>(static_cast<float*>(Cv) + static_cast<int64_t>(row0 + rr) * ldc + gcol);
+      }
+    };
     for (int pair = cluster; pair < total; pair += nclusters) {
       const int m_blk = (pair / n_tiles) * 2 + rank, n_blk = pair % n_tiles;
       const int row0 = m_blk * BM + q * 32;  // this warp's 32 rows
-      tc::mbar_wait(&tfull[acc], acc_phase);
-      tc::fence_after_sync();
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      auto chunk = [&](int c, const float4 (&old)[8]) {
         uint32_t r[32];
         tc::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c), r);
         tc::tmem_ld_wait();
@@ -326,16 +335,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int u = 0; u < 8; ++u)
             tc::st_shared_v4(slab_addr(lane, u), r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]);
           __syncwarp();
-          float4 old[8];
-          if (EPI == kGemmResidualF32) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {  // 4 rows x 128 bytes per instruction
-              const int rr = 4 * i + (lane >> 3), gcol = col0 + (lane & 7) * 4;
-              if (row0 + rr < M && gcol < N)
-                old[i] = *reinterpret_cast<const float4*>(static_cast<float*>(Cv) + static_cast<int64_t>(row0 + rr) * ldc +
-                                                          gcol);
-            }
-          }
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int rr = 4 * i + (lane >> 3), u = lane & 7;
@@ -351,6 +350,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         __syncwarp();  // the slab is rewritten by the next chunk
+      };
+      if (EPI == kGemmResidualF32) {
+        load_res(nA, row0, n_blk * BN);
+        load_res(nB, row0, n_blk * BN + 32);
+      }
+      tc::mbar_wait(&tfull[acc], acc_phase);
+      tc::fence_after_sync();
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 64) {
+        float4 old[8];
+        if (EPI == kGemmResidualF32) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) old[i] = nA[i];
+          if (c + 64 < BN) load_res(nA, row0, n_blk * BN + c + 64);
+        }
+        chunk(c, old);
+        if (EPI == kGemmResidualF32) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) old[i] = nB[i];
+          if (c + 96 < BN) load_res(nB, row0, n_blk * BN + c + 96);
+        }
+        chunk(c + 32, old);
       }
       tc::fence_before_sync();
       tc::mbar_arrive(&tempty[acc]);
