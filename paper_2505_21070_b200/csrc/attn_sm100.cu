@@ -592,6 +592,263 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
 }
 
 // ============================================================================
+// Variant 4: k_attn_pp on a CTA pair (cta_group::2)
+// ============================================================================
+// Two CTAs of a (2,1,1) cluster on one TPC run the ping-pong schedule of
+// k_attn_pp on two adjacent query pairs of the same head as ONE M = 256 MMA
+// per step: QK^T (M256 N64) takes its A rows from each CTA's own Q tile and
+// splits the 64-key B tile by N, so each CTA stages only 32 keys of K (8 KB)
+// and reads 5 KB of shared memory per K=16 step instead of 6 KB (the SS step
+// that bounds k_attn_pp is smem-bound); PV (M256 N128) splits V by head-dim
+// columns, so each CTA stages a [64 keys][64 d] half. K/V bytes per CTA halve.
+// The leader CTA issues every MMA; both CTAs' TMA loads complete on the
+// leader's full barriers, every commit is multicast to both CTAs, and each
+// softmax warp reports P-ready to the leader with one remote arrive.
+// TMEM layout and softmax are k_attn_pp's.
+constexpr uint32_t P2_KH = 32 * 64 * 2;             // [32 keys][64 d] box, 4 KB
+constexpr uint32_t P2_KT = 2 * P2_KH;               // this CTA's K half-tile, 8 KB
+constexpr uint32_t P2_VT = PBK * 64 * 2;            // [64 keys][64 d] V half, 8 KB
+constexpr int P2_KST = 6, P2_VST = 6;
+constexpr uint32_t P2_Q = 0;
+constexpr uint32_t P2_K = P2_Q + 2 * TILE;
+constexpr uint32_t P2_V = P2_K + P2_KST * P2_KT;
+constexpr uint32_t P2_BAR = P2_V + P2_VST * P2_VT;
+constexpr uint32_t P2_SMEM_BYTES = P2_BAR + 256 + 1024;
+static_assert(P2_SMEM_BYTES <= 232448, "pair attention exceeds the 227 KB smem limit");
+
+struct AttnMapsP2 {
+  CUtensorMap q, k0, v0, k1, v1;  // q: 128-row boxes; k: 32-row boxes; v: 64-row boxes
+};
+
+template <int kPoly>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
+    k_attn_pp2(const __grid_constant__ AttnMapsP2 maps, int64_t rows, int64_t n0, int64_t n1, float scale_log2,
+               bf16* __restrict__ out, int64_t ldo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P2_BAR);
+  uint64_t* q_full = bars + 0;              // leader: both CTAs' Q
+  uint64_t* k_full = bars + 1;              // [P2_KST] leader: both K halves
+  uint64_t* k_empty = k_full + P2_KST;      // [P2_KST] each CTA (multicast commit)
+  uint64_t* v_full = k_empty + P2_KST;      // [P2_VST] leader
+  uint64_t* v_empty = v_full + P2_VST;      // [P2_VST] each CTA
+  uint64_t* s_full = v_empty + P2_VST;      // [tile][buffer] each CTA
+  uint64_t* p_full = s_full + 4;            // [tile][buffer] leader, 8 warp arrivals
+  uint64_t* pv_done = p_full + 4;           // [tile] each CTA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_ctarank();
+  const int qpair = blockIdx.x, head = blockIdx.y;
+  const int t0 = static_cast<int>((n0 + PBK - 1) / PBK);
+  const int t1 = static_cast<int>((n1 + PBK - 1) / PBK);
+  const int T = t0 + t1;
+  constexpr uint16_t kBoth = 0x3;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&maps.q);
+    tc::tma_prefetch(&maps.k1);
+    tc::tma_prefetch(&maps.v1);
+    tc::mbar_init(q_full, 1);
+    for (int s = 0; s < P2_KST; ++s) {
+      tc::mbar_init(&k_full[s], 1);
+      tc::mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < P2_VST; ++s) {
+      tc::mbar_init(&v_full[s], 1);
+      tc::mbar_init(&v_empty[s], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      tc::mbar_init(&s_full[i], 1);
+      tc::mbar_init(&p_full[i], 8);
+    }
+    tc::mbar_init(&pv_done[0], 1);
+    tc::mbar_init(&pv_done[1], 1);
+    tc::fence_mbarrier_init_cluster();
+  }
+  if (warp == 1) tc::tmem_alloc_cg2<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();  // barrier inits of both CTAs visible before any remote arrive / TMA
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- TMA producer (both CTAs): own Q tiles, own K / V halves -> leader's barriers ----
+    const uint32_t lq = tc::mapa_shared(tc::smem_u32(q_full), 0);
+    if (rank == 0) tc::mbar_arrive_expect_tx_elect(q_full, 4 * TILE);
+    for (int x = 0; x < 2; ++x) {
+      const int qrow = qpair * 2 * BQ + x * BQ;
+      tc::tma_load_2d_cg2_elect(smem + P2_Q + x * TILE, &maps.q, lq, head * kDh, qrow);
+      tc::tma_load_2d_cg2_elect(smem + P2_Q + x * TILE + HALF, &maps.q, lq, head * kDh + 64, qrow);
+    }
+    for (int j = 0; j < T; ++j) {
+      const bool seg0 = j < t0;
+      const int row0 = (seg0 ? j : j - t0) * PBK;
+      const int ks = j % P2_KST, vs = j % P2_VST;
+      tc::mbar_wait_cluster(&k_empty[ks], ((j / P2_KST) & 1) ^ 1);
+      uint8_t* kd = smem + P2_K + ks * P2_KT;
+      const CUtensorMap* mk = seg0 ? &maps.k0 : &maps.k1;
+      const uint32_t lk = tc::mapa_shared(tc::smem_u32(&k_full[ks]), 0);
+      if (rank == 0) tc::mbar_arrive_expect_tx_elect(&k_full[ks], 2 * P2_KT);
+      tc::tma_load_2d_cg2_elect(kd, mk, lk, head * kDh, row0 + static_cast<int>(rank) * 32);
+      tc::tma_load_2d_cg2_elect(kd + P2_KH, mk, lk, head * kDh + 64, row0 + static_cast<int>(rank) * 32);
+      tc::mbar_wait_cluster(&v_empty[vs], ((j / P2_VST) & 1) ^ 1);
+      uint8_t* vd = smem + P2_V + vs * P2_VT;
+      const CUtensorMap* mv = seg0 ? &maps.v0 : &maps.v1;
+      const uint32_t lv = tc::mapa_shared(tc::smem_u32(&v_full[vs]), 0);
+      if (rank == 0) tc::mbar_arrive_expect_tx_elect(&v_full[vs], 2 * P2_VT);
+      tc::tma_load_2d_cg2_elect(vd, mv, lv, head * kDh + static_cast<int>(rank) * 64, row0);
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      // ---- MMA issuer (leader) ---------------------------------------------------------------
+      constexpr uint32_t idesc_s = tc::idesc_bf16(2 * BQ, PBK, 0, 0);  // Q x K^T, M256 N64
+      constexpr uint32_t idesc_o = tc::idesc_bf16(2 * BQ, kDh, 0, 1);  // P (TMEM) x V, M256 N128
+      const uint32_t q_base = tc::smem_u32(smem + P2_Q);
+      auto qk = [&](int x, int j) {
+        const uint32_t k_addr = tc::smem_u32(smem + P2_K + (j % P2_KST) * P2_KT);
+        const uint32_t d = tmem + static_cast<uint32_t>(x * 2 * PBK + (j & 1) * PBK);
+        tc::mma_ss_k128_cg2_elect<HALF / 16, P2_KH / 16>(d, tc::desc_sw128(q_base + x * TILE, 1024, 16),
+                                                         tc::desc_sw128(k_addr, 1024, 16), idesc_s, 0u);
+        tc::mma_commit_cg2_multicast_elect(&s_full[x * 2 + (j & 1)], kBoth);
+      };
+      auto pv = [&](int x, int j) {
+        const uint32_t v_addr = tc::smem_u32(smem + P2_V + (j % P2_VST) * P2_VT);
+        const uint32_t p_tm = tmem + static_cast<uint32_t>(x * 2 * PBK + (j & 1) * PBK);
+        tc::mma_ts_k64_cg2_elect<2048 / 16>(tmem + 256 + x * kDh, p_tm, tc::desc_sw128(v_addr, 1024, P2_VT),
+                                            idesc_o, j > 0 ? 1u : 0u);
+        tc::mma_commit_cg2_multicast_elect(&pv_done[x], kBoth);
+      };
+      auto qk_pair = [&](int j) {
+        tc::mbar_wait_cluster(&k_full[j % P2_KST], (j / P2_KST) & 1);
+        tc::fence_after_sync();
+        qk(0, j);
+        qk(1, j);
+        tc::mma_commit_cg2_multicast_elect(&k_empty[j % P2_KST], kBoth);
+      };
+      tc::mbar_wait_cluster(q_full, 0);
+      if (T > 0) qk_pair(0);
+      if (T > 1) qk_pair(1);
+      for (int j = 0; j < T; ++j) {
+        tc::mbar_wait_cluster(&v_full[j % P2_VST], (j / P2_VST) & 1);
+        for (int x = 0; x < 2; ++x) {
+          tc::mbar_wait_cluster(&p_full[x * 2 + (j & 1)], (j >> 1) & 1);
+          tc::fence_after_sync();
+          pv(x, j);
+        }
+        tc::mma_commit_cg2_multicast_elect(&v_empty[j % P2_VST], kBoth);
+        if (j + 2 < T) qk_pair(j + 2);  // S buffer j & 1 is free once PV(j) is issued (in-order)
+      }
+    }
+  } else {
+    // ---- softmax + epilogue of tile x (each CTA, its own rows) ------------------------------
+    const int x = (warp - 2) >> 2;
+    const int qq = warp & 3;
+    const int r = qq * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(qq * 32) << 16;
+    const uint32_t tm_o = tmem + lane_off + 256u + static_cast<uint32_t>(x * kDh);
+    const float2 sc2 = make_float2(scale_log2, scale_log2);
+    float m_used = -INFINITY;
+    float2 l2 = make_float2(0.f, 0.f);
+    const int n0i = static_cast<int>(n0), n1i = static_cast<int>(n1);
+    const uint32_t p_full_leader = tc::mapa_shared(tc::smem_u32(&p_full[x * 2]), 0);
+    for (int j = 0; j < T; ++j) {
+      const int b = j & 1;
+      const bool seg0 = j < t0;
+      const int row0 = (seg0 ? j : j - t0) * PBK;
+      const int rem = (seg0 ? n0i : n1i) - row0;
+      const uint32_t tm_s = tmem + lane_off + static_cast<uint32_t>(x * 2 * PBK + b * PBK);
+      tc::mbar_wait_cluster(&s_full[x * 2 + b], (j >> 1) & 1);
+      tc::fence_after_sync();
+      uint32_t sr[64];
+      tc::tmem_ld32(tm_s, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tc::tmem_ld32(tm_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tc::tmem_ld_wait();
+      if (rem < PBK) {  // keys past the segment end (a segment's last tile)
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+          if (c >= rem) sr[c] = __float_as_uint(-INFINITY);
+      }
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 64; c += 8) {
+        m4[0] = max3f(m4[0], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+        m4[1] = max3f(m4[1], __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
+        m4[2] = max3f(m4[2], __uint_as_float(sr[c + 4]), __uint_as_float(sr[c + 5]));
+        m4[3] = max3f(m4[3], __uint_as_float(sr[c + 6]), __uint_as_float(sr[c + 7]));
+      }
+      const float mx = max3f(m4[0], m4[1], fmaxf(m4[2], m4[3])) * scale_log2;  // scale > 0
+      const bool need = mx > m_used + kRescaleThreshold;
+      const float m_new = need ? mx : m_used;
+      const float corr = need ? ex2(m_used - m_new) : 1.f;  // 0 on the first tile
+      const float2 neg_m2 = make_float2(-m_new, -m_new);
+      uint32_t pk[32];
+      float2 ls_a = make_float2(0.f, 0.f), ls_b = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const float2 xv = __ffma2_rn(make_float2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sc2,
+                                     neg_m2);
+        const float2 p = (c & 3) >= 4 - kPoly ? ex2_poly2(xv) : make_float2(ex2(xv.x), ex2(xv.y));
+        if (c & 1) ls_b = __fadd2_rn(ls_b, p);
+        else ls_a = __fadd2_rn(ls_a, p);
+        pk[c] = pack_bf16(p.x, p.y);
+      }
+      l2 = __ffma2_rn(l2, make_float2(corr, corr), __fadd2_rn(ls_a, ls_b));
+      m_used = m_new;
+      if (j >= 1 && __any_sync(0xffffffffu, need)) {  // O must hold PV(j-1) before it is rescaled
+        tc::mbar_wait_cluster(&pv_done[x], (j - 1) & 1);
+        tc::fence_after_sync();
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          const uint32_t ta = tm_o + static_cast<uint32_t>(c * 32);
+          tc::tmem_ld32(ta, o);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+          tc::tmem_st32(ta, o);
+        }
+      }
+      tc::tmem_st32(tm_s, pk);
+      tc::tmem_st_wait();
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(p_full_leader + static_cast<uint32_t>(b * 8));
+    }
+    if (T >= 1) {
+      tc::mbar_wait_cluster(&pv_done[x], (T - 1) & 1);
+      tc::fence_after_sync();
+    }
+    const int64_t row = static_cast<int64_t>(qpair) * 2 * BQ + x * BQ + r;
+    const float inv_l = 1.f / (l2.x + l2.y);
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      tc::tmem_ld32(tm_o + static_cast<uint32_t>(c * 32), o);
+      tc::tmem_ld_wait();
+      if (row < rows) {
+        uint4* dst = reinterpret_cast<uint4*>(out + row * ldo + head * kDh + c * 32);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          dst[v] = make_uint4(pack_bf16(__uint_as_float(o[8 * v]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l),
+                              pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l),
+                              pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l),
+                              pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l));
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();  // the peer's MMAs / arrivals / TMA into this CTA are done
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc_cg2<512>(tmem);
+  }
+}
+
+// ============================================================================
 // Variant 3: two query tiles per CTA, 128-key tiles, one S buffer per tile,
 // each S row split across two softmax warps
 // ============================================================================
@@ -924,6 +1181,7 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     BP_CUDA(cudaFuncSetAttribute(k_attn_pp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
     BP_CUDA(cudaFuncSetAttribute(k_attn_pp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
     BP_CUDA(cudaFuncSetAttribute(k_attn_fa, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
     configured = true;
   }
   AttnMaps maps;
@@ -938,7 +1196,22 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     maps.v0 = maps.v1;
   }
   const float scale_log2 = a.scale * 1.4426950408889634f;
-  if (variant == 3) {  // two Q tiles per CTA, 128-key tiles, one S buffer per tile
+  if (variant == 4) {  // k_attn_pp on a CTA pair (cta_group::2)
+    AttnMapsP2 pm;
+    pm.q = maps.q;
+    pm.k1 = map_for(a.k1, a.n1, H, a.ldk1, 32);
+    pm.v1 = map_for(a.v1, a.n1, H, a.ldv1, PBK);
+    if (a.n0 > 0) {
+      pm.k0 = map_for(a.k0, a.n0, H, a.ldk0, 32);
+      pm.v0 = map_for(a.v0, a.n0, H, a.ldv0, PBK);
+    } else {
+      pm.k0 = pm.k1;
+      pm.v0 = pm.v1;
+    }
+    const unsigned pairs = static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ));
+    dim3 grid(pairs + (pairs & 1u), static_cast<unsigned>(a.heads));
+    k_attn_pp2<1><<<grid, PP_THREADS, P2_SMEM_BYTES, st>>>(pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
+  } else if (variant == 3) {  // two Q tiles per CTA, 128-key tiles, one S buffer per tile
     dim3 grid(static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(a.heads));
     k_attn_fa<<<grid, FA_THREADS, FA_SMEM_BYTES, st>>>(maps, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
   } else if (variant == 2) {  // ping-pong: 256 query rows per CTA, 64-key tiles

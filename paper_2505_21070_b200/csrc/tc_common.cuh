@@ -133,6 +133,126 @@ __device__ __forceinline__ void tma_load_2d_multicast_elect(void* dst, const CUt
       : "memory");
 }
 
+// ---- CTA pair (cta_group::2) ------------------------------------------------------------
+// Address of the same shared variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// Arrive on an mbarrier given by its shared::cluster address (possibly the peer's).
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Wait with cluster-scope acquire (arrivals came from the peer CTA).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait_cluster(addr, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (!mbar_try_wait_cluster(addr, parity)) {
+    if (globaltimer_ns() - t0 > 5000000000ULL) __trap();
+  }
+}
+// 2-D TMA load into this CTA's shared memory whose complete_tx lands on the
+// mbarrier at shared::cluster address `bar_cluster` (the leader CTA's).
+__device__ __forceinline__ void tma_load_2d_cg2_elect(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                      int c1) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n"
+      "}\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+template <int kCols>
+__device__ __forceinline__ void tmem_alloc_cg2(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(kCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <int kCols>
+__device__ __forceinline__ void tmem_dealloc_cg2(uint32_t base) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(kCols) : "memory");
+}
+// Arrives on the mbarrier at the offset of `bar` in every CTA of cta_mask once
+// all previously issued cta_group::2 MMAs of this thread complete.
+__device__ __forceinline__ void mma_commit_cg2_multicast_elect(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
+}
+// K=128 chain of cta_group::2 SS MMAs (see mma_ss_k128_elect).
+template <uint32_t AH, uint32_t BH>
+__device__ __forceinline__ void mma_ss_k128_cg2_elect(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                                      uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t;\n"
+      ".reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.b32 t, 0, 0;\n"
+      "add.s64 a1, %1, 2;  add.s64 b1, %2, 2;\n"
+      "add.s64 a2, %1, 4;  add.s64 b2, %2, 4;\n"
+      "add.s64 a3, %1, 6;  add.s64 b3, %2, 6;\n"
+      "add.s64 a4, %1, %5; add.s64 b4, %2, %6;\n"
+      "add.s64 a5, a4, 2;  add.s64 b5, b4, 2;\n"
+      "add.s64 a6, a4, 4;  add.s64 b6, b4, 4;\n"
+      "add.s64 a7, a4, 6;  add.s64 b7, b4, 6;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a4, b4, %3, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a5, b5, %3, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a6, b6, %3, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a7, b7, %3, t;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "n"(static_cast<uint64_t>(AH)), "n"(static_cast<uint64_t>(BH)));
+}
+// K=64 chain of cta_group::2 TS MMAs (see mma_ts_k64_elect).
+template <uint32_t BSTEP>
+__device__ __forceinline__ void mma_ts_k64_cg2_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                                     uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t;\n"
+      ".reg .b32 x1, x2, x3;\n"
+      ".reg .b64 b1, b2, b3;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.b32 t, 0, 0;\n"
+      "add.u32 x1, %1, 8;  add.u32 x2, %1, 16; add.u32 x3, %1, 24;\n"
+      "add.s64 b1, %2, %5; add.s64 b2, b1, %5; add.s64 b3, b2, %5;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [x1], b1, %3, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [x2], b2, %3, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [x3], b3, %3, t;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate), "n"(static_cast<uint64_t>(BSTEP)));
+}
+
 // ---- tcgen05 ---------------------------------------------------------------------------
 // Shared-memory matrix descriptor: K-major operand tile stored by TMA with
 // 128-byte swizzling (rows of 64 bf16, 8-row / 1024-byte swizzle atoms).
