@@ -65,7 +65,13 @@ typedef enum {
   BP_PREC_F32 = 1,   /* fp32 verification mode (rel-L2 <= 1e-4)                  */
   BP_PREC_BF16 = 2   /* tcgen05 bf16 tensor-core path, fp32 residual (<= 2e-2)  */
 } bp_precision;
-typedef enum { BP_TRANSPORT_LOOPBACK = 0, BP_TRANSPORT_NCCL = 1 } bp_transport;
+/* LOOPBACK: every stage on one GPU in one process. NCCL: one process per GPU,
+ * ncclSend/ncclRecv between consecutive stages. IPC: one process per GPU (or
+ * several processes on one GPU), each stage writes the next stage's receive
+ * ring directly through CUDA IPC memory (peer copies over NVLink between
+ * GPUs) and signals through counters in the receiver's and sender's memory,
+ * written and polled by one-warp stream-ordered kernels. */
+typedef enum { BP_TRANSPORT_LOOPBACK = 0, BP_TRANSPORT_NCCL = 1, BP_TRANSPORT_IPC = 2 } bp_transport;
 
 /* ModelConfig (model.hpp:21-32) + the defaulted FFN width extension. */
 typedef struct {
@@ -232,6 +238,14 @@ BP_API bp_status bp_nccl_unique_id(uint8_t out[128]);
 BP_API bp_status bp_pipeline_create(const bp_pipeline_desc* desc, int32_t rank, int32_t world,
                              int32_t device, const uint8_t* nccl_ids, bp_pipeline** out);
 BP_API bp_status bp_pipeline_destroy(bp_pipeline* p);
+/* IPC transport handshake: each rank exports the handle of its receive block
+ * (64 bytes), the caller all-gathers them in rank order, then every rank
+ * connects before its first run. */
+BP_API bp_status bp_ipc_handle(bp_pipeline* p, uint8_t out[64]);
+BP_API bp_status bp_ipc_connect(bp_pipeline* p, const uint8_t* handles /* world x 64 bytes */);
+/* Diagnostic: this rank's ring counters (delivered hidden, delivered eps,
+ * consumed hidden-out, consumed eps-out). */
+BP_API bp_status bp_ipc_counters(bp_pipeline* p, uint32_t out[4]);
 
 /* EmittedBlock (engine.hpp:73-78) callback, rank 0 only, emission order. */
 typedef void (*bp_emit_fn)(void* user, int64_t block_id, int64_t frames, const double* data,

@@ -117,6 +117,9 @@ _SIGS = {
     "bp_nccl_unique_id": (i32, [P(C.c_uint8)]),
     "bp_pipeline_create": (i32, [P(PipelineDesc), i32, i32, i32, P(C.c_uint8), P(C.c_void_p)]),
     "bp_pipeline_destroy": (i32, [C.c_void_p]),
+    "bp_ipc_handle": (i32, [C.c_void_p, P(C.c_uint8)]),
+    "bp_ipc_connect": (i32, [C.c_void_p, P(C.c_uint8)]),
+    "bp_ipc_counters": (i32, [C.c_void_p, P(C.c_uint32)]),
     "bp_pipeline_run": (i32, [C.c_void_p, EMIT_FN, C.c_void_p]),
     "bp_pipeline_get_stats": (i32, [C.c_void_p, P(PipelineStats)]),
     "bp_pipeline_set_profiling": (i32, [C.c_void_p, i32]),

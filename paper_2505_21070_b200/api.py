@@ -283,7 +283,11 @@ class Pipeline:
     """run_pipeline (engine.cpp:255-497) on B200: build once, run many times."""
 
     def __init__(self, config: ConfigLike, rank: int = 0, world: int = 1, device: int = 0,
-                 nccl_ids: Optional[bytes] = None):
+                 nccl_ids: Optional[bytes] = None,
+                 ipc_exchange: Optional[Callable[[bytes], Sequence[bytes]]] = None):
+        """nccl_ids: world x 128-byte NCCL unique ids (transport "nccl").
+        ipc_exchange: all-gathers this rank's 64-byte IPC handle and returns
+        every rank's handle in rank order (transport "ipc", world > 1)."""
         self.cfg = _cfg(config)
         self._h = C.c_void_p()
         desc = self.cfg.to_desc()
@@ -292,6 +296,16 @@ class Pipeline:
             buf = (C.c_uint8 * len(nccl_ids)).from_buffer_copy(nccl_ids)
             ids = C.cast(buf, C.POINTER(C.c_uint8))
         check(lib.bp_pipeline_create(C.byref(desc), rank, world, device, ids, C.byref(self._h)))
+        if self.cfg.transport == "ipc" and world > 1:
+            if ipc_exchange is None:
+                raise errors.ConfigError("transport 'ipc' needs ipc_exchange to share the ranks' handles")
+            mine = (C.c_uint8 * 64)()
+            check(lib.bp_ipc_handle(self._h, mine))
+            allh = b"".join(bytes(h) for h in ipc_exchange(bytes(mine)))
+            if len(allh) != 64 * world:
+                raise errors.ConfigError("ipc_exchange must return one 64-byte handle per rank")
+            hb = (C.c_uint8 * len(allh)).from_buffer_copy(allh)
+            check(lib.bp_ipc_connect(self._h, hb))
         self.schedule = Schedule(self.cfg)
 
     def close(self):

@@ -14,7 +14,7 @@ ORDERS = {"reverse": 0, "sequential": 1}
 CACHE = {"off": 0, "on": 1, "recompute": 2}
 STRATEGIES = {"coordinated": 0, "complete-shuffle": 1, "subset": 2, "fresh": 3, "repeat": 4}
 PRECISIONS = {"f64": 0, "f32": 1, "bf16": 2}
-TRANSPORTS = {"loopback": 0, "nccl": 1}
+TRANSPORTS = {"loopback": 0, "nccl": 1, "ipc": 2}
 
 
 @dataclasses.dataclass

@@ -4,10 +4,13 @@
 // per GPU) or all stages share one GPU (loopback). Hidden states move
 // between stages with ncclSend/ncclRecv on dedicated streams, double-buffered
 // and event-chained to compute, so transfers overlap the next pass.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include "nccl_dl.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -69,17 +72,98 @@ class Pipeline {
   ncclComm_t comm_prev_ = nullptr, comm_next_ = nullptr, comm_eps_ = nullptr;
   cudaStream_t s_recv_ = nullptr, s_send_ = nullptr, s_eps_ = nullptr;
   DevBuf rbuf_[2], ebuf_[2];
+
+ public:
+  // IPC transport: this rank's exported block = [hidden ring: 2 slots]
+  // [eps ring: 2 slots][counters]; the same layout on every rank.
+  //   cnt[0] hidden passes delivered into my ring (written by rank - 1)
+  //   cnt[1] eps passes delivered into my eps ring (rank 0; written by N - 1)
+  //   cnt[2] my outgoing hidden passes consumed (written by rank + 1)
+  //   cnt[3] my outgoing eps passes consumed (rank N - 1; written by rank 0)
+  // Counters grow monotonically across runs (ipc_epoch_ passes per run).
+  void ipc_handle(uint8_t out[64]);
+  void ipc_connect(const uint8_t* handles);
+  void ipc_counters(uint32_t out[4]);
+
+ private:
+  bool multi() const { return d_.transport != BP_TRANSPORT_LOOPBACK && d_.devices > 1; }
+  bool ipc() const { return d_.transport == BP_TRANSPORT_IPC && d_.devices > 1; }
+  char* ipc_slot(char* block, int which, int64_t i) const {
+    return block + (which == 0 ? 0 : 2 * ipc_hid_) + (i & 1) * (which == 0 ? ipc_hid_ : ipc_eps_);
+  }
+  uint32_t* ipc_cnt(char* block, int k) const {
+    return reinterpret_cast<uint32_t*>(block + 2 * ipc_hid_ + 2 * ipc_eps_) + k;
+  }
+  void ipc_send(char* peer, int which, int64_t i, const void* src, size_t bytes, cudaStream_t s);
+  void ipc_wait_delivered(int which, int64_t i, cudaStream_t s);
+  void ipc_release(char* peer, int which, int64_t i, cudaStream_t s);
+  DevBuf ipc_block_;
+  size_t ipc_hid_ = 0, ipc_eps_ = 0;
+  char* peer_next_ = nullptr;  // rank + 1's block (my hidden sends land there)
+  char* peer_prev_ = nullptr;  // rank - 1's block (I release its hidden sends)
+  char* peer_eps_ = nullptr;   // rank 0 <-> rank N - 1 (eps return)
+  std::vector<char*> opened_;
+  bool ipc_ready_ = false;
+  uint32_t ipc_epoch_ = 0;
 };
+
+__device__ __forceinline__ uint64_t tc_globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Stream-ordered wait until *addr >= v (wrap-safe). A one-warp polling kernel
+// rather than cuStreamWaitValue32: a channel parked in a semaphore acquire is
+// not switched out under time-slicing, so two processes sharing one GPU
+// deadlock on each other's counters (observed on B200), while a polling
+// kernel is preempted like any other. Traps after 20 s instead of hanging.
+__device__ unsigned long long g_ipc_timeouts[4];  // diagnostics: count, last addr, last wanted, last seen
+__global__ void k_wait_geq(const uint32_t* addr, uint32_t v, int soft) {
+  if (threadIdx.x != 0) return;
+  const uint64_t t0 = tc_globaltimer();
+  for (;;) {
+    uint32_t cur;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(cur) : "l"(addr) : "memory");
+    if (static_cast<int32_t>(cur - v) >= 0) break;
+    __nanosleep(256);
+    if (tc_globaltimer() - t0 > (soft ? 3000000000ULL : 20000000000ULL)) {
+      if (!soft) __trap();
+      atomicAdd(&g_ipc_timeouts[0], 1ULL);
+      g_ipc_timeouts[1] = reinterpret_cast<unsigned long long>(addr);
+      g_ipc_timeouts[2] = v;
+      g_ipc_timeouts[3] = cur;
+      break;
+    }
+  }
+}
+static const bool g_ipc_soft = std::getenv("BP_IPC_SOFT") != nullptr;
+void stream_wait_geq(cudaStream_t s, const uint32_t* addr, uint32_t v) {
+  k_wait_geq<<<1, 32, 0, s>>>(addr, v, g_ipc_soft ? 1 : 0);
+  BP_CUDA(cudaGetLastError());
+}
+// Stream-ordered release store of a counter (possibly in a peer process's
+// memory): everything the stream did before is visible before the value.
+__global__ void k_write_release(uint32_t* addr, uint32_t v) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+  }
+}
+void stream_write(cudaStream_t s, uint32_t* addr, uint32_t v) {
+  k_write_release<<<1, 32, 0, s>>>(addr, v);
+  BP_CUDA(cudaGetLastError());
+}
 
 extern std::atomic<int64_t> g_launches;
 
 Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, const uint8_t* ids)
     : sched(build_schedule(d)), d_(d), rank_(rank), world_(world), device_(device) {
   const int N = d.devices;
-  if (d.transport == BP_TRANSPORT_NCCL) {
-    if (world != N) fail(BP_ERR_CONFIG, "NCCL transport needs world == devices (one stage per GPU)");
+  if (d.transport == BP_TRANSPORT_NCCL || d.transport == BP_TRANSPORT_IPC) {
+    if (world != N) fail(BP_ERR_CONFIG, "multi-process transports need world == devices (one stage per process)");
     if (rank < 0 || rank >= world) fail(BP_ERR_CONFIG, "bad rank");
-    if (N > 1 && ids == nullptr) fail(BP_ERR_CONFIG, "NCCL transport needs unique ids");
+    if (d.transport == BP_TRANSPORT_NCCL && N > 1 && ids == nullptr) fail(BP_ERR_CONFIG, "NCCL transport needs unique ids");
   } else {
     if (world != 1 || rank != 0) fail(BP_ERR_CONFIG, "loopback runs as a single process");
   }
@@ -90,7 +174,7 @@ Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, c
   hwc_ = tpf_ * C_;
   stages_.resize(static_cast<size_t>(N));
   for (int j = 0; j < N; ++j) {
-    const bool local = d.transport != BP_TRANSPORT_NCCL || j == rank;
+    const bool local = d.transport == BP_TRANSPORT_LOOPBACK || j == rank;
     if (!local) continue;
     stages_[static_cast<size_t>(j)] = std::make_unique<Stage>(
         device_, d.model, d.seed_model, d.seed_context, sched.begins[static_cast<size_t>(j)],
@@ -147,12 +231,24 @@ Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, c
     if (rank_ > 0) { rbuf_[0].alloc(hid); rbuf_[1].alloc(hid); }
     if (rank_ == 0) { ebuf_[0].alloc(eps); ebuf_[1].alloc(eps); }
   }
+  if (d.transport == BP_TRANSPORT_IPC && N > 1) {
+    BP_CUDA(cudaStreamCreateWithFlags(&s_recv_, cudaStreamNonBlocking));
+    BP_CUDA(cudaStreamCreateWithFlags(&s_send_, cudaStreamNonBlocking));
+    BP_CUDA(cudaStreamCreateWithFlags(&s_eps_, cudaStreamNonBlocking));
+    const Stage& s = *stages_[static_cast<size_t>(rank_)];
+    auto align256 = [](size_t n) { return (n + 255) & ~static_cast<size_t>(255); };
+    ipc_hid_ = align256(static_cast<size_t>(sched.max_tokens) * d.model.hidden * s.act_bytes());
+    ipc_eps_ = align256(static_cast<size_t>(sched.max_tokens) * C_ * s.eps_bytes());
+    ipc_block_.alloc(2 * ipc_hid_ + 2 * ipc_eps_ + 256);
+    BP_CUDA(cudaMemset(ipc_cnt(ipc_block_.as<char>(), 0), 0, 256));
+  }
   BP_CUDA(cudaDeviceSynchronize());
 }
 
 Pipeline::~Pipeline() {
   cudaSetDevice(device_);
   cudaDeviceSynchronize();
+  for (char* q : opened_) cudaIpcCloseMemHandle(q);
   for (double* h : pinned_) cudaFreeHost(h);
   if (comm_prev_) bp::nccl().CommDestroy(comm_prev_);
   if (comm_next_) bp::nccl().CommDestroy(comm_next_);
@@ -301,6 +397,75 @@ void Pipeline::after_stage(const SchedPass& p, int j, Stage& s) {
   }
 }
 
+void Pipeline::ipc_handle(uint8_t out[64]) {
+  if (!ipc()) fail(BP_ERR_CONFIG, "pipeline does not use the IPC transport");
+  cudaIpcMemHandle_t h;
+  BP_CUDA(cudaIpcGetMemHandle(&h, ipc_block_.p));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+  std::memcpy(out, &h, 64);
+}
+
+void Pipeline::ipc_connect(const uint8_t* handles) {
+  if (!ipc()) fail(BP_ERR_CONFIG, "pipeline does not use the IPC transport");
+  if (ipc_ready_) fail(BP_ERR_CONFIG, "IPC transport already connected");
+  BP_CUDA(cudaSetDevice(device_));
+  const int N = d_.devices;
+  std::vector<char*> mapped(static_cast<size_t>(N), nullptr);
+  auto open = [&](int r) {
+    if (r == rank_) fail(BP_ERR_INTERNAL, "IPC: a rank does not map its own block");
+    if (!mapped[static_cast<size_t>(r)]) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + 64 * r, 64);
+      void* q = nullptr;
+      BP_CUDA(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+      mapped[static_cast<size_t>(r)] = static_cast<char*>(q);
+      opened_.push_back(static_cast<char*>(q));
+    }
+    return mapped[static_cast<size_t>(r)];
+  };
+  if (rank_ + 1 < N) peer_next_ = open(rank_ + 1);
+  if (rank_ > 0) peer_prev_ = open(rank_ - 1);
+  if (rank_ == 0) peer_eps_ = open(N - 1);
+  if (rank_ == N - 1) peer_eps_ = open(0);
+  ipc_ready_ = true;
+}
+
+// Diagnostic: this rank's four counters, read on a private stream (works
+// while the pipeline's streams are blocked in stream waits).
+void Pipeline::ipc_counters(uint32_t out[4]) {
+  if (!ipc()) fail(BP_ERR_CONFIG, "pipeline does not use the IPC transport");
+  cudaStream_t s;
+  BP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  BP_CUDA(cudaMemcpyAsync(out, ipc_cnt(ipc_block_.as<char>(), 0), 16, cudaMemcpyDeviceToHost, s));
+  BP_CUDA(cudaStreamSynchronize(s));
+  cudaStreamDestroy(s);
+}
+
+// Sender side of one ring: wait until the receiver consumed pass i - 2 (its
+// slot i & 1 is free), copy into the receiver's slot, publish delivery.
+static const bool g_ipc_trace = std::getenv("BP_IPC_TRACE") != nullptr;
+static_assert(sizeof(long long) == 8, "");
+void Pipeline::ipc_send(char* peer, int which, int64_t i, const void* src, size_t bytes, cudaStream_t s) {
+  if (g_ipc_trace) std::fprintf(stderr, "[rank %d] send ch%d pass %lld (%zu B)\n", rank_, which, static_cast<long long>(i), bytes);
+  // slot i & 1 is free once pass i - 2 is released; the first two passes of a
+  // run wait until every pass of the previous run is released (the receiver
+  // may still be finishing it when this rank starts the next run)
+  const uint32_t base = ipc_epoch_;
+  stream_wait_geq(s, ipc_cnt(ipc_block_.as<char>(), which == 0 ? 2 : 3),
+                  i >= 2 ? base + static_cast<uint32_t>(i - 1) : base);
+  BP_CUDA(cudaMemcpyAsync(ipc_slot(peer, which, i), src, bytes, cudaMemcpyDeviceToDevice, s));
+  stream_write(s, ipc_cnt(peer, which == 0 ? 0 : 1), base + static_cast<uint32_t>(i + 1));
+}
+// Receiver side: pass i has landed in my slot i & 1.
+void Pipeline::ipc_wait_delivered(int which, int64_t i, cudaStream_t s) {
+  if (g_ipc_trace) std::fprintf(stderr, "[rank %d] recv ch%d pass %lld\n", rank_, which, static_cast<long long>(i));
+  stream_wait_geq(s, ipc_cnt(ipc_block_.as<char>(), which == 0 ? 0 : 1), ipc_epoch_ + static_cast<uint32_t>(i + 1));
+}
+// Receiver side: slot i & 1 has been consumed (stream-ordered after its use).
+void Pipeline::ipc_release(char* peer, int which, int64_t i, cudaStream_t s) {
+  stream_write(s, ipc_cnt(peer, which == 0 ? 2 : 3), ipc_epoch_ + static_cast<uint32_t>(i + 1));
+}
+
 void Pipeline::run(bp_emit_fn emit, void* user) {
   BP_CUDA(cudaSetDevice(device_));
   trace.clear();
@@ -312,7 +477,8 @@ void Pipeline::run(bp_emit_fn emit, void* user) {
   stats.h2d_bytes = stats.d2h_bytes = 0;
   for (auto& s : stages_)
     if (s) s->set_profiling(profiling);
-  if (d_.transport == BP_TRANSPORT_NCCL && d_.devices > 1) run_nccl(emit, user);
+  if (ipc() && !ipc_ready_) fail(BP_ERR_CONFIG, "IPC transport: bp_ipc_connect has not been called");
+  if (multi()) run_nccl(emit, user);
   else run_rank0_loopback(emit, user);
   stats.attn_ms = stats.gemm_ms = stats.cross_ms = 0.0;
   stats.attn_launches = stats.gemm_launches = stats.cross_launches = 0;
@@ -425,11 +591,25 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
     BP_CUDA(cudaEventRecord(ev_fwd[i], st_));
     return out_ring[i & 1].p;
   };
+  const bool use_ipc = ipc();
+  // channel 0: hidden state j -> j+1; channel 1: eps N-1 -> 0
   auto send_to = [&](ncclComm_t comm, cudaStream_t ss, const SchedPass& p, const void* buf, int peer,
                      size_t count, ncclDataType_t dt) {
     BP_CUDA(cudaStreamWaitEvent(ss, ev_fwd[p.index], 0));
-    BP_NCCL(bp::nccl().Send(buf, count, dt, peer, comm, ss));
+    if (use_ipc) {
+      const bool eps_ch = peer < 0;
+      ipc_send(eps_ch ? peer_eps_ : peer_next_, eps_ch ? 1 : 0, p.index, buf,
+               count * (dt == ncclFloat64 ? 8 : 4), ss);
+    } else {
+      BP_NCCL(bp::nccl().Send(buf, count, dt, peer, comm, ss));
+    }
     BP_CUDA(cudaEventRecord(ev_sent[p.index], ss));
+  };
+  auto eps_buf = [&](int64_t i) -> void* {
+    return use_ipc ? static_cast<void*>(ipc_slot(ipc_block_.as<char>(), 1, i)) : ebuf_[i & 1].p;
+  };
+  auto hid_buf = [&](int64_t i) -> void* {
+    return use_ipc ? static_cast<void*>(ipc_slot(ipc_block_.as<char>(), 0, i)) : rbuf_[i & 1].p;
   };
 
   if (j == 0) {
@@ -442,8 +622,16 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
     auto post_eps_recv = [&](int64_t i) {
       if (i >= P) return;
       const SchedPass& p = sched.passes[static_cast<size_t>(i)];
-      if (i >= 2) BP_CUDA(cudaStreamWaitEvent(s_eps_, ev_used[i - 2], 0));
-      BP_NCCL(bp::nccl().Recv(ebuf_[i & 1].p, static_cast<size_t>(p.tokens) * C_, edt, 0, comm_eps_, s_eps_));
+      if (use_ipc) {
+        if (i >= 2) {  // give slot i & 1 back once STEP(i - 2) has read it
+          BP_CUDA(cudaStreamWaitEvent(s_eps_, ev_used[i - 2], 0));
+          ipc_release(peer_eps_, 1, i - 2, s_eps_);
+        }
+        ipc_wait_delivered(1, i, s_eps_);
+      } else {
+        if (i >= 2) BP_CUDA(cudaStreamWaitEvent(s_eps_, ev_used[i - 2], 0));
+        BP_NCCL(bp::nccl().Recv(ebuf_[i & 1].p, static_cast<size_t>(p.tokens) * C_, edt, 0, comm_eps_, s_eps_));
+      }
       BP_CUDA(cudaEventRecord(ev_recv[i], s_eps_));
     };
     post_eps_recv(0);
@@ -460,7 +648,7 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
         boundary += p.tokens * H * static_cast<int64_t>(abytes);
       } else {
         BP_CUDA(cudaStreamWaitEvent(st_, ev_recv[p.index], 0));
-        step(p, ebuf_[p.index & 1].p, st_);
+        step(p, eps_buf(p.index), st_);
         BP_CUDA(cudaEventRecord(ev_used[p.index], st_));
         post_eps_recv(p.index + 2);
         if (p.finishes_block) emit_block(sched.blocks[static_cast<size_t>(p.block - 1)], st_, emit != nullptr);
@@ -470,8 +658,16 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
     auto post_recv = [&](int64_t i) {
       if (i >= P) return;
       const SchedPass& p = sched.passes[static_cast<size_t>(i)];
-      if (i >= 2) BP_CUDA(cudaStreamWaitEvent(s_recv_, ev_used[i - 2], 0));
-      BP_NCCL(bp::nccl().Recv(rbuf_[i & 1].p, static_cast<size_t>(p.tokens) * H, adt, 0, comm_prev_, s_recv_));
+      if (use_ipc) {
+        if (i >= 2) {  // give slot i & 1 back once forward(i - 2) has copied it in
+          BP_CUDA(cudaStreamWaitEvent(s_recv_, ev_used[i - 2], 0));
+          ipc_release(peer_prev_, 0, i - 2, s_recv_);
+        }
+        ipc_wait_delivered(0, i, s_recv_);
+      } else {
+        if (i >= 2) BP_CUDA(cudaStreamWaitEvent(s_recv_, ev_used[i - 2], 0));
+        BP_NCCL(bp::nccl().Recv(rbuf_[i & 1].p, static_cast<size_t>(p.tokens) * H, adt, 0, comm_prev_, s_recv_));
+      }
       BP_CUDA(cudaEventRecord(ev_recv[i], s_recv_));
     };
     post_recv(0);
@@ -479,20 +675,41 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
     for (int64_t i = 0; i < P; ++i) {
       const SchedPass& p = sched.passes[static_cast<size_t>(i)];
       BP_CUDA(cudaStreamWaitEvent(st_, ev_recv[i], 0));
-      const void* out = forward_pass(p, rbuf_[i & 1].p);
+      const void* out = forward_pass(p, hid_buf(i));
       BP_CUDA(cudaEventRecord(ev_used[i], st_));  // input copied into the stage's residual stream
       post_recv(i + 2);
       if (j + 1 < N) {
         send_to(comm_next_, s_send_, p, out, 1, static_cast<size_t>(p.tokens) * H, adt);
         boundary += p.tokens * H * static_cast<int64_t>(abytes);
       } else {
-        send_to(comm_eps_, s_send_, p, out, 1, static_cast<size_t>(p.tokens) * C_, edt);
+        send_to(comm_eps_, s_send_, p, out, use_ipc ? -1 : 1, static_cast<size_t>(p.tokens) * C_, edt);
+      }
+    }
+  }
+  if (use_ipc) {  // release the last two slots so the counters line up for the next run
+    for (int64_t i = std::max<int64_t>(0, P - 2); i < P; ++i) {
+      if (j == 0) {
+        BP_CUDA(cudaStreamWaitEvent(s_eps_, ev_used[i], 0));
+        ipc_release(peer_eps_, 1, i, s_eps_);
+      } else {
+        BP_CUDA(cudaStreamWaitEvent(s_recv_, ev_used[i], 0));
+        ipc_release(peer_prev_, 0, i, s_recv_);
       }
     }
   }
   BP_CUDA(cudaStreamSynchronize(s_send_));
   if (s_eps_) BP_CUDA(cudaStreamSynchronize(s_eps_));
   BP_CUDA(cudaStreamSynchronize(s_recv_));
+  if (use_ipc) ipc_epoch_ += static_cast<uint32_t>(P);
+  if (use_ipc && g_ipc_soft) {
+    unsigned long long t[4];
+    BP_CUDA(cudaMemcpyFromSymbol(t, g_ipc_timeouts, sizeof t));
+    uint32_t c[4];
+    BP_CUDA(cudaMemcpy(c, ipc_cnt(ipc_block_.as<char>(), 0), 16, cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[rank %d] ipc timeouts %llu (addr off %lld want %llu seen %llu) counters %u %u %u %u epoch %u\n",
+                 rank_, t[0], static_cast<long long>(t[1]) - reinterpret_cast<long long>(ipc_block_.p), t[2], t[3],
+                 c[0], c[1], c[2], c[3], ipc_epoch_);
+  }
   BP_CUDA(cudaEventRecord(e1, st_));
   BP_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;
@@ -541,6 +758,24 @@ bp_status bp_pipeline_create(const bp_pipeline_desc* desc, int32_t rank, int32_t
     auto h = std::make_unique<bp_pipeline>();
     h->p = std::make_unique<bp::Pipeline>(*desc, rank, world, device, nccl_ids);
     *out = h.release();
+  });
+}
+
+bp_status bp_ipc_handle(bp_pipeline* p, uint8_t out[64]) {
+  return bp::guarded([&] {
+    if (!p || !out) bp::fail(BP_ERR_CONFIG, "null argument");
+    p->p->ipc_handle(out);
+  });
+}
+
+bp_status bp_ipc_counters(bp_pipeline* p, uint32_t out[4]) {
+  return bp::guarded([&] { p->p->ipc_counters(out); });
+}
+
+bp_status bp_ipc_connect(bp_pipeline* p, const uint8_t* handles) {
+  return bp::guarded([&] {
+    if (!p || !handles) bp::fail(BP_ERR_CONFIG, "null argument");
+    p->p->ipc_connect(handles);
   });
 }
 

@@ -1,0 +1,58 @@
+"""Row (e) on one GPU: the multi-process layer pipeline (one process per
+stage, static per-rank programs, send/recv rings on side streams, rank 0 owning
+latents and Euler updates) with the CUDA-IPC transport, several processes
+sharing device 0. The latents must equal the single-process serial oracle
+bitwise (test_engine.cpp:66-78: N-invariance), across repeated runs of the
+same pipeline (ring counters carry over between runs)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+G = json.load(open(os.path.join(ROOT, "tests", "golden", "goldens.json")))
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def run_ranks(cfg, n, tmp_path, runs=2):
+    out = str(tmp_path / "mp.npz")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "tests", "mp_worker.py"), json.dumps(cfg), out, str(runs)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return np.load(out)
+
+
+@pytest.mark.parametrize("prec,n", [("f64", 2), ("bf16", 2), ("f64", 4)])
+def test_ipc_pipeline_equals_serial_bitwise(bp, tmp_path, prec, n):
+    base = dict(G["mid"]["config"], precision=prec)
+    if n > 2:  # four processes time-slice one GPU: a shorter schedule
+        base.update(steps=3, blocks=2)
+    want = bp.serial_oracle(base)
+    ref = np.concatenate([b["frames"].ravel() for b in want["blocks"]])
+    got = run_ranks(dict(base, devices=n, transport="ipc"), n, tmp_path)
+    for r in range(2):
+        assert np.array_equal(got[f"run{r}"], ref), (prec, n, r)
+        assert list(got[f"ids{r}"]) == [b["block_id"] for b in want["blocks"]]
+    assert int(got["boundary_bytes"]) > 0
+
+
+def test_ipc_pipeline_sequential_order_uneven(bp, tmp_path):
+    """Sequential order, cache off, an uneven 3-way split of 4 layers."""
+    base = dict(G["mid"]["config"], precision="f64", order="sequential", cache="off")
+    want = bp.serial_oracle(base)
+    ref = np.concatenate([b["frames"].ravel() for b in want["blocks"]])
+    got = run_ranks(dict(base, devices=3, transport="ipc", uneven_split=True), 3, tmp_path, runs=1)
+    assert np.array_equal(got["run0"], ref)
