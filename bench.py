@@ -245,6 +245,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
+                    help="N > 1 stage-boundary transport: NCCL send/recv or CUDA-IPC peer copies")
     ap.add_argument("--workload", default="auto", choices=["auto", "wan14b"],
                     help="auto: configs[1] at N=1, configs[2] at N>1; wan14b: the configs[4] sample leg")
     args = ap.parse_args()
@@ -263,14 +265,14 @@ def main():
                             ffn=w["ffn"], channels=w["channels"], height=w["height"], width=w["width"],
                             context_len=w["context_len"], num_b=w["num_b"], num_c=w["num_c"], steps=w["steps"],
                             blocks=w["blocks"], uneven_split=True,
-                            transport="nccl" if n > 1 else "loopback")
+                            transport=args.transport if n > 1 else "loopback")
     sched = bp.Schedule(cfg)
     fl_video, n_prefix = video_flops(w, sched)
     config = {"workload": w["name"], "layers": w["layers"], "hidden": w["hidden"], "heads": w["heads"],
               "ffn": w["ffn"], "latent_grid": [w["height"], w["width"], w["channels"]], "context_len": w["context_len"],
               "num_b": w["num_b"], "num_c": w["num_c"], "steps": w["steps"], "blocks": w["blocks"],
               "frames": w["frames"], "passes": sched.npasses, "prefix_passes": n_prefix,
-              "parallelism": f"layer-pipeline x{n}", "l2": "inputs larger than L2 (18720x1536 activations per pass)"}
+              "parallelism": f"layer-pipeline x{n}" + (f" ({args.transport})" if n > 1 else ""), "l2": "inputs larger than L2 (18720x1536 activations per pass)"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -299,26 +301,34 @@ def main():
 
     dist = None
     ids = None
+    exchange = None
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
-        obj = [None]
-        if rank == 0:
-            from paper_2505_21070_b200._lib import lib
-            import ctypes
-            buf = bytearray()
-            for _ in range(n):
-                b = (ctypes.c_uint8 * 128)()
-                assert lib.bp_nccl_unique_id(b) == 0
-                buf += bytes(b)
-            obj = [bytes(buf)]
-        dist.broadcast_object_list(obj, src=0)
-        ids = obj[0]
+
+        def exchange(h):  # IPC transport: every rank's 64-byte handle, rank order
+            got = [None] * world
+            dist.all_gather_object(got, h)
+            return got
+
+        if args.transport == "nccl":
+            obj = [None]
+            if rank == 0:
+                from paper_2505_21070_b200._lib import lib
+                import ctypes
+                buf = bytearray()
+                for _ in range(n):
+                    b = (ctypes.c_uint8 * 128)()
+                    assert lib.bp_nccl_unique_id(b) == 0
+                    buf += bytes(b)
+                obj = [bytes(buf)]
+            dist.broadcast_object_list(obj, src=0)
+            ids = obj[0]
 
     t_build = time.perf_counter()
-    pipe = bp.Pipeline(cfg, rank=rank, world=world, device=local, nccl_ids=ids)
+    pipe = bp.Pipeline(cfg, rank=rank, world=world, device=local, nccl_ids=ids, ipc_exchange=exchange)
     build_s = time.perf_counter() - t_build
 
     def barrier():
