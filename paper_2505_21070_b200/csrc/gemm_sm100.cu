@@ -194,13 +194,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 // pieces: the L1 work per tile drops 8x, which is what bounded the K = 1536
 // residual GEMMs.
 constexpr uint32_t B_HALF = B_BYTES / 2;
-constexpr uint32_t PAIR_STAGING = STAGES * (A_BYTES + B_BYTES) + 256;  // after the ring + mbarriers
-constexpr uint32_t PAIR_SMEM_BYTES = PAIR_STAGING + 4 * 4096 + 1024;
+constexpr uint32_t PAIR_STAGING = (STAGES * (A_BYTES + B_BYTES) + 256 + 1023) & ~1023u;  // after ring + mbarriers
+constexpr uint32_t PAIR_SMEM_BYTES = PAIR_STAGING + 2 * 4 * 4096 + 1024;  // two 4 KB slabs per epilogue warp
+static_assert(PAIR_SMEM_BYTES <= 232448, "pair GEMM exceeds the 227 KB smem limit");
 
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bh, int M, int N,
-                int K, void* __restrict__ Cv, int64_t ldc) {
+                int K, void* __restrict__ Cv, int64_t ldc, const __grid_constant__ CUtensorMap map_c) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
@@ -210,7 +211,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* staging = smem + PAIR_STAGING;  // 4 epilogue warps x 4 KB
+  uint8_t* staging = smem + PAIR_STAGING;  // 4 epilogue warps x 2 x 4 KB (1024-aligned: TMA swizzle atoms)
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int rank = static_cast<int>(tc::cluster_ctarank());
@@ -283,24 +284,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else {
     // ---- epilogue (warps 2..5 -> TMEM lane quarters 2,3,0,1), transposed through smem ----
     const int q = warp & 3;
-    const uint32_t slab = tc::smem_u32(staging + (warp - 2) * 4096);
+    const uint32_t slab = tc::smem_u32(staging + (warp - 2) * 8192);
     auto slab_addr = [&](int row, int unit) {
       return slab + static_cast<uint32_t>(row * 128 + ((unit ^ (row & 7)) << 4));
     };
+    int red_buf = 0;  // residual epilogue: which of the warp's two slabs the next chunk uses
     int acc = 0;
     uint32_t acc_phase = 0;
-    // Residual chunks are fetched two chunks ahead (the first two before the
-    // accumulator is ready): 8 KB in flight per warp keeps HBM busy while
-    // TMEM reads, the smem transpose and the stores of earlier chunks proceed.
-    float4 nA[8], nB[8];
-    auto load_res = [&](float4 (&dst)[8], int row0, int col0) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {  // 4 rows x 128 bytes per instruction
-        const int rr = 4 * i + (lane >> 3), gcol = col0 + (lane & 7) * 4;
-        if (row0 + rr < M && gcol < N)
-          dst[i] = *reinterpret_cast<const float4*>(static_cast<float*>(Cv) + static_cast<int64_t>(row0 + rr) * ldc + gcol);
-      }
-    };
     for (int pair = cluster; pair < total; pair += nclusters) {
       const int m_blk = (pair / n_tiles) * 2 + rank, n_blk = pair % n_tiles;
       const int row0 = m_blk * BM + q * 32;  // this warp's 32 rows
@@ -309,6 +299,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c), r);
         tc::tmem_ld_wait();
         const int col0 = n_blk * BN + c;
+        if (EPI == kGemmResidualF32) {
+          // x += acc through a TMA reduce-add: the 32x32 fp32 chunk goes to a
+          // 128B-swizzled slab (the tensor map's layout) and L2 performs the
+          // read-modify-write, so the epilogue never waits on residual loads.
+          const uint32_t sl = slab + static_cast<uint32_t>(red_buf * 4096);
+          tc::bulk_wait_group_read<1>();  // the slab's previous reduce has read it
+          __syncwarp();
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            tc::st_shared_v4(sl + static_cast<uint32_t>(lane * 128 + ((u ^ (lane & 7)) << 4)), r[4 * u],
+                             r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]);
+          tc::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tc::tma_reduce_add_2d(&map_c, staging + (warp - 2) * 8192 + red_buf * 4096, col0, row0);
+            tc::bulk_commit_group();
+          }
+          red_buf ^= 1;
+          (void)old;
+          return;
+        }
         if (EPI == kGemmStoreBf16 || EPI == kGemmGeluBf16) {
           uint32_t pk[16];
 #pragma unroll
@@ -351,26 +362,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         __syncwarp();  // the slab is rewritten by the next chunk
       };
-      if (EPI == kGemmResidualF32) {
-        load_res(nA, row0, n_blk * BN);
-        load_res(nB, row0, n_blk * BN + 32);
-      }
+
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::fence_after_sync();
 #pragma unroll 1
       for (int c = 0; c < BN; c += 64) {
         float4 old[8];
-        if (EPI == kGemmResidualF32) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) old[i] = nA[i];
-          if (c + 64 < BN) load_res(nA, row0, n_blk * BN + c + 64);
-        }
         chunk(c, old);
-        if (EPI == kGemmResidualF32) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) old[i] = nB[i];
-          if (c + 96 < BN) load_res(nB, row0, n_blk * BN + c + 96);
-        }
         chunk(c + 32, old);
       }
       tc::fence_before_sync();
@@ -378,6 +376,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (EPI == kGemmResidualF32) tc::bulk_wait_group<0>();  // this lane's reduce-adds are complete
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -411,7 +410,7 @@ std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
 template <int EPI>
 void launch_pair(const CUtensorMap& ma, const CUtensorMap& mbh, int M, int N, int K, void* C, int64_t ldc,
-                 cudaStream_t st) {
+                 const CUtensorMap& mc, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     BP_CUDA(cudaFuncSetAttribute(k_gemm_pair<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM_BYTES));
@@ -419,7 +418,7 @@ void launch_pair(const CUtensorMap& ma, const CUtensorMap& mbh, int M, int N, in
   }
   const int pairs = (((M + BM - 1) / BM + 1) / 2) * ((N + BN - 1) / BN);
   const int clusters = pairs < kNumSms / 2 ? pairs : kNumSms / 2;
-  k_gemm_pair<EPI><<<2 * clusters, kThreads, PAIR_SMEM_BYTES, st>>>(ma, mbh, M, N, K, C, ldc);
+  k_gemm_pair<EPI><<<2 * clusters, kThreads, PAIR_SMEM_BYTES, st>>>(ma, mbh, M, N, K, C, ldc, mc);
 }
 
 template <int EPI>
@@ -437,8 +436,7 @@ void launch_epi(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int 
 
 }  // namespace
 
-void make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
-                       uint32_t box_rows, uint32_t box_cols) {
+static void load_encode() {
   if (!g_encode) {
     cudaDriverEntryPointQueryResult q{};
     void* fn = nullptr;
@@ -446,6 +444,24 @@ void make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64
     if (!fn || q != cudaDriverEntryPointSuccess) fail(BP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
+}
+
+void make_tmap_2d_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                      uint32_t box_rows, uint32_t box_cols) {
+  load_encode();
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 4};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(BP_ERR_CUDA, "cuTensorMapEncodeTiled (f32) failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+void make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                       uint32_t box_rows, uint32_t box_cols) {
+  load_encode();
   const cuuint64_t dims[2] = {cols, rows};
   const cuuint64_t strides[1] = {ld * 2};
   const cuuint32_t box[2] = {box_cols, box_rows};
@@ -468,6 +484,18 @@ static const CUtensorMap& cached_map(const void* p, uint64_t rows, uint64_t cols
   return g_maps.emplace(k, m).first->second;
 }
 
+static const CUtensorMap& cached_map_f32(const void* p, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t br,
+                                         uint32_t bc) {
+  std::lock_guard<std::mutex> lock(g_map_mu);
+  const MapKey k{p, rows, cols, ld | (1ull << 62), br, bc};  // tagged: fp32 maps never alias bf16 ones
+  auto it = g_maps.find(k);
+  if (it != g_maps.end()) return it->second;
+  if (g_maps.size() > 4096) g_maps.clear();
+  CUtensorMap m;
+  make_tmap_2d_f32(&m, p, rows, cols, ld, br, bc);
+  return g_maps.emplace(k, m).first->second;
+}
+
 void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C, int64_t ldc, int epi,
                     cudaStream_t st, int variant) {
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15)
@@ -478,11 +506,16 @@ void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int
   if (variant == 2) {  // cluster pair sharing the weight tile (128-row weight boxes)
     const CUtensorMap mbh =
         cached_map(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(K), BN / 2, BK);
+    CUtensorMap mc = mbh;  // unused except by the residual epilogue
+    if (epi == kGemmResidualF32) {
+      if ((reinterpret_cast<uintptr_t>(C) & 15) || (ldc * 4) % 16) fail(BP_ERR_INTERNAL, "residual C must be 16-byte aligned");
+      mc = cached_map_f32(C, static_cast<uint64_t>(M), static_cast<uint64_t>(N), static_cast<uint64_t>(ldc), 32, 32);
+    }
     switch (epi) {
-      case kGemmStoreBf16: launch_pair<kGemmStoreBf16>(ma, mbh, M, N, K, C, ldc, st); break;
-      case kGemmGeluBf16: launch_pair<kGemmGeluBf16>(ma, mbh, M, N, K, C, ldc, st); break;
-      case kGemmResidualF32: launch_pair<kGemmResidualF32>(ma, mbh, M, N, K, C, ldc, st); break;
-      default: launch_pair<kGemmStoreF32>(ma, mbh, M, N, K, C, ldc, st); break;
+      case kGemmStoreBf16: launch_pair<kGemmStoreBf16>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+      case kGemmGeluBf16: launch_pair<kGemmGeluBf16>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+      case kGemmResidualF32: launch_pair<kGemmResidualF32>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+      default: launch_pair<kGemmStoreF32>(ma, mbh, M, N, K, C, ldc, mc, st); break;
     }
     count_launch();
     return;

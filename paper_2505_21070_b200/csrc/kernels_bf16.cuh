@@ -19,6 +19,10 @@ void launch_embed_table(const double* freq, int h, int tpf, double* ttab, cudaSt
 void launch_embed_fast(const double* lat, const float* w_in32, const double* freq, const double* ttab,
                        double* ftab, const int32_t* levels, const int64_t* frame_ids, int64_t tokens, int C, int h,
                        int tpf, float* lat32, float* x, cudaStream_t st);
+// fp32 C[M,N] (+)= A[M,K] B[K,N] for the path's fp32 side GEMMs (embedding,
+// head); falls back to the generic SIMT GEMM for shapes the tile kernel skips.
+void launch_gemm_f32_tile(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K, float* C,
+                          int64_t ldc, bool residual, cudaStream_t st);
 void launch_ln_bf16(const float* x, int64_t ldx, const float* g, const float* b, int64_t rows,
                     int n, bf16* y, cudaStream_t st);
 

@@ -591,8 +591,8 @@ const void* Stage::forward_bf16(const StageInput& in) {
   if (new_rec) { nr.valid = true; nr.tokens = P; rec_ = std::move(nr); }
   parity_ ^= 1;
   if (is_last()) {
-    launch_matmul<float>(x, H, static_cast<const float*>(w_out_), C_, static_cast<int>(S), C_, h_,
-                         eps_.as<float>(), C_, kEpiNone, nullptr, 0, st);
+    launch_gemm_f32_tile(x, H, static_cast<const float*>(w_out_), C_, static_cast<int>(S), C_, h_, eps_.as<float>(),
+                         C_, false, st);
     return eps_.p;
   }
   return x_.p;

@@ -236,3 +236,20 @@ def test_wan14b_width_stage(bp):
     mid = bp.Stage(cfg, 5, 0, 1, 6, precision="bf16").forward_chunk(x0, [7, 7], [0, 1])["payload"]
     last = bp.Stage(cfg, 5, 1, 2, 6, precision="bf16").forward_chunk(mid, [7, 7], [0, 1])["payload"]
     assert np.array_equal(mono, last)
+
+
+def test_wan_size_invariants(bp):
+    """Size-independent properties at the production shape (Wan2.1-1.3B width,
+    480p latent grid, S = 18720, cached prefix 6240; 2 blocks x 2 steps so
+    both prefix and tail passes run): the 2-stage loopback pipeline equals the
+    single stage bitwise, cached == recompute bitwise, every latent finite."""
+    base = dict(layers=30, hidden=1536, heads=12, ffn=8960, channels=64, height=30, width=52,
+                context_len=512, num_b=8, num_c=8, steps=2, blocks=2, precision="bf16")
+    one = bp.run_pipeline(dict(base, devices=1))
+    two = bp.run_pipeline(dict(base, devices=2))
+    rec = bp.run_pipeline(dict(base, devices=1, cache="recompute"))
+    a, b, c = latents(one), latents(two), latents(rec)
+    assert a.size == (12 + 8) * 30 * 52 * 64
+    assert np.isfinite(a).all()
+    assert np.array_equal(a, b)
+    assert np.array_equal(a, c)
