@@ -350,7 +350,8 @@ def main():
     barrier()
     lib_launch = []
     gpu_ms = []
-    prof = {"attn_ms": 0.0, "gemm_ms": 0.0, "cross_ms": 0.0, "attn_launches": 0, "gemm_launches": 0}
+    prof = {"attn_ms": 0.0, "gemm_ms": 0.0, "cross_ms": 0.0, "ln_ms": 0.0, "attn_launches": 0, "gemm_launches": 0,
+            "ln_launches": 0}
     from paper_2505_21070_b200._lib import lib
     lib.bp_pipeline_set_profiling(pipe._h, 1)
     with ClockSampler(local) as clk:
@@ -422,6 +423,7 @@ def main():
         pass
     cpu = None if args.no_cpu_baseline else cpu_baseline(w, sched)
     s_video = ms / 1e3
+    tokens_per_pass = (w["num_b"] + w["num_c"] // 2) * w["height"] * w["width"]
     out = {
         "metric": METRIC, "value": w["frames"] / s_video, "unit": "frames/s", "n_gpus": n, "steps": args.steps,
         "warmup": n_warm, "ms_per_step": ms, "higher_is_better": True,
@@ -439,6 +441,17 @@ def main():
                      "gemm_tflops": None if prof["gemm_ms"] <= 0 else
                      (fl_video - self_attn_flops(w, sched)) * args.steps / (prof["gemm_ms"] / 1e3) / 1e12,
                      "whole_step_frac": fl_video / s_video / 1e12 / peak},
+        # north_star: the elementwise path against HBM bandwidth -- the
+        # LayerNorm kernel (fp32 residual row in, bf16 operand row out: 6 B per
+        # element algorithmic), device time from CUDA events in the timed steps
+        "elementwise_roofline": None if prof["ln_ms"] <= 0 else {
+            "bound": "hbm", "kernel": "k_ln_bf16_reg (LayerNorm + affine, fp32 -> bf16)",
+            "achieved": prof["ln_launches"] * tokens_per_pass * w["hidden"] * 6 / (prof["ln_ms"] / 1e3) / 1e9,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": prof["ln_launches"] * tokens_per_pass * w["hidden"] * 6 / (prof["ln_ms"] / 1e3) / 1e9 / peaks["hbm_gbs"],
+            "bytes_per_launch": tokens_per_pass * w["hidden"] * 6, "share_of_step": prof["ln_ms"] / 1e3 / (args.steps * s_video),
+            "note": "event windows around each launch include the launch gap; ncu kernel time is lower "
+                    "(profiles/r01b_summary.md)"},
         "cpu_baseline": cpu,
         "e2e": {"value": statistics.mean(e2e_vals), "unit": "frames/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -265,6 +265,8 @@ typedef struct {
   double attn_ms, gemm_ms;  /* per-class device time when profiling is enabled */
   double cross_ms;          /* cross-attention device time (profiling)             */
   int64_t attn_launches, gemm_launches, cross_launches;
+  double ln_ms;             /* LayerNorm device time (profiling)                   */
+  int64_t ln_launches;
   int64_t h2d_bytes;        /* host->device bytes of the last run (host-supplied pool) */
   int64_t d2h_bytes;        /* device->host bytes of the last run (emitted latents)   */
 } bp_pipeline_stats;

@@ -480,15 +480,16 @@ void Pipeline::run(bp_emit_fn emit, void* user) {
   if (ipc() && !ipc_ready_) fail(BP_ERR_CONFIG, "IPC transport: bp_ipc_connect has not been called");
   if (multi()) run_nccl(emit, user);
   else run_rank0_loopback(emit, user);
-  stats.attn_ms = stats.gemm_ms = stats.cross_ms = 0.0;
-  stats.attn_launches = stats.gemm_launches = stats.cross_launches = 0;
+  stats.attn_ms = stats.gemm_ms = stats.cross_ms = stats.ln_ms = 0.0;
+  stats.attn_launches = stats.gemm_launches = stats.cross_launches = stats.ln_launches = 0;
   for (auto& s : stages_) {
     if (!s) continue;
-    double ms[3];
-    int64_t n[3];
+    double ms[4];
+    int64_t n[4];
     s->prof_collect(ms, n);
-    stats.attn_ms += ms[0]; stats.cross_ms += ms[1]; stats.gemm_ms += ms[2];
+    stats.attn_ms += ms[0]; stats.cross_ms += ms[1]; stats.gemm_ms += ms[2]; stats.ln_ms += ms[3];
     stats.attn_launches += n[0]; stats.cross_launches += n[1]; stats.gemm_launches += n[2];
+    stats.ln_launches += n[3];
   }
   stats.passes = static_cast<int64_t>(sched.passes.size());
   stats.kernel_launches = g_launches.load() - launches_at_start_;

@@ -515,7 +515,9 @@ const void* Stage::forward_bf16(const StageInput& in) {
                          dst + static_cast<int64_t>(f) * tpf_ * H, H * 4, tpf_, H * 4, st);
       nr.rec.push_back(dst);
     }
+    prof_mark(3, true);
     launch_ln_bf16(x, H, lnw, lnw + H, S, h_, ln, st);
+    prof_mark(3, false);
     AttnBf16Args a{};
     if (in.use_prev == 1) {
       a.k0 = static_cast<const bf16*>(cache_.k[static_cast<size_t>(li)]);
@@ -558,7 +560,9 @@ const void* Stage::forward_bf16(const StageInput& in) {
     launch_gemm_bf16(at, H, static_cast<const bf16*>(w.wo), static_cast<int>(S), h_, h_, x, H,
                      kGemmResidualF32, st);
     prof_mark(2, false);
+    prof_mark(3, true);
     launch_ln_bf16(x, H, lnw + 2 * H, lnw + 3 * H, S, h_, ln, st);
+    prof_mark(3, false);
     prof_mark(2, true);
     launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.cq), static_cast<int>(S), h_, h_, cq, H,
                      kGemmStoreBf16, st);
@@ -577,7 +581,9 @@ const void* Stage::forward_bf16(const StageInput& in) {
     launch_gemm_bf16(at, H, static_cast<const bf16*>(w.co), static_cast<int>(S), h_, h_, x, H,
                      kGemmResidualF32, st);
     prof_mark(2, false);
+    prof_mark(3, true);
     launch_ln_bf16(x, H, lnw + 4 * H, lnw + 5 * H, S, h_, ln, st);
+    prof_mark(3, false);
     prof_mark(2, true);
     launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.w1), static_cast<int>(S), F_, h_, hm, F_,
                      kGemmGeluBf16, st);
@@ -704,8 +710,8 @@ void Stage::prof_mark(int cls, bool begin) {
   }
 }
 
-void Stage::prof_collect(double ms[3], int64_t launches[3]) {
-  for (int i = 0; i < 3; ++i) { ms[i] = 0.0; launches[i] = 0; }
+void Stage::prof_collect(double ms[4], int64_t launches[4]) {
+  for (int i = 0; i < 4; ++i) { ms[i] = 0.0; launches[i] = 0; }
   if (!prof_marks_.empty()) BP_CUDA(cudaEventSynchronize(prof_marks_.back().second.second));
   for (const auto& m : prof_marks_) {
     float t = 0.f;

@@ -66,9 +66,9 @@ class Stage {
   int64_t rec_tokens() const { return rec_.tokens; }
 
   // Per-kernel-class device timing with CUDA events on this stage's stream:
-  // class 0 self-attention, 1 cross-attention, 2 GEMMs.
+  // class 0 self-attention, 1 cross-attention, 2 GEMMs, 3 LayerNorm.
   void set_profiling(bool on) { prof_on_ = on; }
-  void prof_collect(double ms[3], int64_t launches[3]);
+  void prof_collect(double ms[4], int64_t launches[4]);
 
  private:
   void prof_mark(int cls, bool begin);
