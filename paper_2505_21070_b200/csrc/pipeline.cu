@@ -230,6 +230,31 @@ Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, c
     const size_t eps = static_cast<size_t>(sched.max_tokens) * C_ * s.eps_bytes();
     if (rank_ > 0) { rbuf_[0].alloc(hid); rbuf_[1].alloc(hid); }
     if (rank_ == 0) { ebuf_[0].alloc(eps); ebuf_[1].alloc(eps); }
+    // Connect every channel now, in an order with no cycle. NCCL connects a
+    // point-to-point pair lazily at its first operation and blocks until the
+    // peer takes part; the run's first operations are receives on BOTH ends
+    // of the ring (rank 0 posts its eps receives before its first send, the
+    // last rank posts its hidden receive before its first eps send), which
+    // would wait on each other forever. Here each stage first receives from
+    // its predecessor, then sends to its successor; the eps return goes last.
+    DevBuf tiny;
+    tiny.alloc(256);
+    if (rank_ > 0) {
+      BP_NCCL(bp::nccl().Recv(tiny.p, 1, ncclFloat32, 0, comm_prev_, s_recv_));
+      BP_CUDA(cudaStreamSynchronize(s_recv_));
+    }
+    if (rank_ + 1 < N) {
+      BP_NCCL(bp::nccl().Send(tiny.p, 1, ncclFloat32, 1, comm_next_, s_send_));
+      BP_CUDA(cudaStreamSynchronize(s_send_));
+    }
+    if (rank_ == N - 1) {
+      BP_NCCL(bp::nccl().Send(tiny.p, 1, ncclFloat32, 1, comm_eps_, s_send_));
+      BP_CUDA(cudaStreamSynchronize(s_send_));
+    }
+    if (rank_ == 0) {
+      BP_NCCL(bp::nccl().Recv(tiny.p, 1, ncclFloat32, 0, comm_eps_, s_eps_));
+      BP_CUDA(cudaStreamSynchronize(s_eps_));
+    }
   }
   if (d.transport == BP_TRANSPORT_IPC && N > 1) {
     BP_CUDA(cudaStreamCreateWithFlags(&s_recv_, cudaStreamNonBlocking));

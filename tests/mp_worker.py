@@ -34,7 +34,16 @@ def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist.init_process_group("gloo")
-    device = 0 if cfg.transport == "ipc" else local
+    one_gpu = cfg.transport == "ipc" or os.environ.get("BP_MP_ONE_GPU") == "1"
+    device = 0 if one_gpu else local
+    if cfg.transport == "nccl" and one_gpu:
+        # NCCL refuses two ranks on one GPU of one host (duplicate bus id); a
+        # distinct host id per rank makes it treat the ranks as separate hosts
+        # and use its socket transport over loopback, which exercises the
+        # NCCL executor path on a single device
+        os.environ["NCCL_HOSTID"] = f"blockpipe-rank-{rank}"
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+        os.environ.setdefault("NCCL_IB_DISABLE", "1")
 
     def exchange(h):
         got = [None] * world

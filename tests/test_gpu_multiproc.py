@@ -1,9 +1,12 @@
 """Row (e) on one GPU: the multi-process layer pipeline (one process per
 stage, static per-rank programs, send/recv rings on side streams, rank 0 owning
-latents and Euler updates) with the CUDA-IPC transport, several processes
-sharing device 0. The latents must equal the single-process serial oracle
-bitwise (test_engine.cpp:66-78: N-invariance), across repeated runs of the
-same pipeline (ring counters carry over between runs)."""
+latents and Euler updates), several processes sharing device 0, with both
+transports: CUDA IPC, and NCCL (each rank given its own NCCL host id, so NCCL
+treats the ranks as separate hosts and uses its socket transport; the
+executor's NCCL calls, channel connection order and stream/event logic are
+the ones an 8-GPU run uses). The latents must equal the single-process serial
+oracle bitwise (test_engine.cpp:66-78: N-invariance), across repeated runs of
+the same pipeline."""
 import json
 import os
 import socket
@@ -27,10 +30,11 @@ def free_port():
 
 def run_ranks(cfg, n, tmp_path, runs=2):
     out = str(tmp_path / "mp.npz")
+    env = dict(os.environ, BP_MP_ONE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            os.path.join(ROOT, "tests", "mp_worker.py"), json.dumps(cfg), out, str(runs)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return np.load(out)
 
@@ -56,3 +60,16 @@ def test_ipc_pipeline_sequential_order_uneven(bp, tmp_path):
     ref = np.concatenate([b["frames"].ravel() for b in want["blocks"]])
     got = run_ranks(dict(base, devices=3, transport="ipc", uneven_split=True), 3, tmp_path, runs=1)
     assert np.array_equal(got["run0"], ref)
+
+
+@pytest.mark.parametrize("prec,n", [("f64", 2), ("bf16", 3)])
+def test_nccl_pipeline_equals_serial_bitwise(bp, tmp_path, prec, n):
+    """The NCCL transport, including the deadlock-free channel connection
+    order (pipeline.cu: every stage receives from its predecessor before it
+    sends; NCCL connects a pair lazily and blocks until both ends take part)."""
+    base = dict(G["mid"]["config"], precision=prec, steps=3, blocks=2)
+    want = bp.serial_oracle(base)
+    ref = np.concatenate([b["frames"].ravel() for b in want["blocks"]])
+    got = run_ranks(dict(base, devices=n, transport="nccl", uneven_split=n == 3), n, tmp_path)
+    for r in range(2):
+        assert np.array_equal(got[f"run{r}"], ref), (prec, n, r)
