@@ -33,6 +33,9 @@ WAN13 = dict(layers=30, hidden=1536, heads=12, ffn=8960, channels=64, height=30,
 WORKLOADS = {
     1: dict(WAN13, blocks=3, frames=81, name="Wan2.1-1.3B-shape 81f 480p (BASELINE configs[1])"),
     "multi": dict(WAN13, blocks=9, frames=301, name="Wan2.1-1.3B-shape 301f 480p (BASELINE configs[2])"),
+    # wiring checks only (the mid parity config: 4 layers, h 256, 3 blocks x 6 steps)
+    "tiny": dict(layers=4, hidden=256, heads=2, ffn=1024, channels=64, height=4, width=6, context_len=16,
+                 num_b=8, num_c=8, steps=6, blocks=3, frames=41, name="mid parity config (wiring check only)"),
     # the paper's headline video length (BASELINE configs[3] names 8 GPUs);
     # selectable at any N, e.g. N = 1 for the single-GPU reference point
     "wan13-1025": dict(WAN13, blocks=32, frames=1025, name="Wan2.1-1.3B-shape 1025f 480p (BASELINE configs[3] video)"),
@@ -250,7 +253,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
                     help="N > 1 stage-boundary transport: NCCL send/recv or CUDA-IPC peer copies")
-    ap.add_argument("--workload", default="auto", choices=["auto", "wan14b", "wan13-301", "wan13-1025"],
+    ap.add_argument("--workload", default="auto", choices=["auto", "wan14b", "wan13-301", "wan13-1025", "tiny"],
                     help="auto: configs[1] at N=1, configs[2] at N>1; wan13-301 / wan13-1025: those videos at "
                          "any N; wan14b: the configs[4] sample leg")
     args = ap.parse_args()
@@ -260,11 +263,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("BP_BENCH_ONE_GPU") == "1" and world > 1:
+        # wiring check of the N > 1 path on a single GPU: every rank on device
+        # 0, NCCL told the ranks are separate hosts (socket transport); the
+        # numbers are time-sliced and mean nothing
+        local = 0
+        os.environ["NCCL_HOSTID"] = f"blockpipe-bench-rank-{rank}"
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+        os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
     n = max(args.gpus, world)
     if args.workload == "wan13-301":
         w = WORKLOADS["multi"]
-    elif args.workload == "wan13-1025":
-        w = WORKLOADS["wan13-1025"]
+    elif args.workload in ("wan13-1025", "tiny"):
+        w = WORKLOADS[args.workload]
     else:
         w = WORKLOADS[1] if n == 1 else WORKLOADS["multi"]
 
