@@ -56,17 +56,28 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
-def pipeline_roofline(flops_video, n, peak_tflops, link_bytes_video, s_video):
+def pipeline_roofline(flops_video, n, peak_tflops, link_bytes_video, s_video, sched=None, layers=None):
     """Whole-pipeline roofline of one video: compute at the sustained bf16
     peak on N GPUs vs the busiest stage boundary's bytes over one NVLink
-    direction (900 GB/s); frac = that ideal time / the measured time."""
+    direction (900 GB/s); frac = that ideal time / the measured time. With
+    the schedule, also the schedule-aware bound: the makespan in
+    slots (EventLog) x one slot of the largest stage at peak."""
     compute_s = flops_video / (n * peak_tflops * 1e12)
     nvlink_s = link_bytes_video / 900e9 if n > 1 else 0.0
     ideal = max(compute_s, nvlink_s)
-    return {"bound": "tensor" if compute_s >= nvlink_s else "nvlink", "compute_s": compute_s, "nvlink_s": nvlink_s,
-            "ideal_s": ideal, "measured_s": s_video, "frac": ideal / s_video if s_video > 0 else None,
-            "link_bytes_per_video": link_bytes_video, "peak_tflops": peak_tflops, "nvlink_gbs": 900.0,
-            "note": "N = 1 has no stage boundary; the loopback transport keeps every stage on one GPU"}
+    out = {"bound": "tensor" if compute_s >= nvlink_s else "nvlink", "compute_s": compute_s, "nvlink_s": nvlink_s,
+           "ideal_s": ideal, "measured_s": s_video, "frac": ideal / s_video if s_video > 0 else None,
+           "link_bytes_per_video": link_bytes_video, "peak_tflops": peak_tflops, "nvlink_gbs": 900.0}
+    if sched is not None and layers:
+        slots = int(sched.events[:, 0].max() - sched.events[:, 0].min()) + 1 if len(sched.events) else 0
+        largest = max(e - b for b, e in sched.partition)
+        slot_s = flops_video / sched.npasses * (largest / layers) / (peak_tflops * 1e12)
+        out.update({"makespan_slots": slots, "largest_stage_layers": largest,
+                    "schedule_aware_s": slots * slot_s,
+                    "schedule_aware_frac": slots * slot_s / s_video if s_video > 0 else None})
+    out["note"] = ("N = 1: no stage boundary, every stage on one GPU" if n == 1 else
+                   f"N = {n}: busiest stage boundary over one NVLink direction")
+    return out
 
 
 def pass_flops(w, tokens, prefix, reference_algorithm=False):
@@ -470,7 +481,7 @@ def main():
                         "memory (bp_pipeline_set_pool) and every emitted block copied back to host"},
         # north_star: the slower of compute at peak and stage-boundary bytes over
         # NVLink (900 GB/s per direction) bounds the whole pipeline
-        "pipeline_roofline": pipeline_roofline(fl_video, n, peak, link_bytes, s_video),
+        "pipeline_roofline": pipeline_roofline(fl_video, n, peak, link_bytes, s_video, sched, w["layers"]),
         "gpu_launches": int(statistics.mean(lib_launch)),
         "clocks": clk.summary(),
         "build_s": build_s,
