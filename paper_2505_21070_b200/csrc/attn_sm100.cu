@@ -421,6 +421,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
+  tc::pdl_wait();  // Q/K/V were produced by the previous kernel
 
   if (warp == 0) {
     // ---- TMA producer -------------------------------------------------------------------
@@ -1232,9 +1233,8 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
       const char* e = std::getenv("BP_ATTN_POLY");
       return e ? std::atoi(e) : 1;
     }();
-    if (poly == 0) k_attn_pp<0><<<grid, PP_THREADS, PP_SMEM_BYTES, st>>>(pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
-    else if (poly == 2) k_attn_pp<2><<<grid, PP_THREADS, PP_SMEM_BYTES, st>>>(pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
-    else k_attn_pp<1><<<grid, PP_THREADS, PP_SMEM_BYTES, st>>>(pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
+    auto kern = poly == 0 ? k_attn_pp<0> : (poly == 2 ? k_attn_pp<2> : k_attn_pp<1>);
+    launch_pdl(kern, grid, dim3(PP_THREADS), PP_SMEM_BYTES, st, pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
   } else {
     dim3 grid(static_cast<unsigned>((rows + BQ - 1) / BQ), static_cast<unsigned>(a.heads));
     k_attn_tc<<<grid, kThreads, SMEM_BYTES, st>>>(maps, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);

@@ -241,6 +241,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc::cluster_sync();  // barrier inits visible to the peer before any remote arrive / multicast
   tc::fence_after_sync();
   const uint32_t tmem_base = *tmem_slot;
+  tc::pdl_wait();  // A and the residual were produced by the previous kernel
 
   if (warp == 0) {
     // ---- TMA producer: own A tile + own half of the shared weight tile (multicast) ----
@@ -418,7 +419,8 @@ void launch_pair(const CUtensorMap& ma, const CUtensorMap& mbh, int M, int N, in
   }
   const int pairs = (((M + BM - 1) / BM + 1) / 2) * ((N + BN - 1) / BN);
   const int clusters = pairs < kNumSms / 2 ? pairs : kNumSms / 2;
-  k_gemm_pair<EPI><<<2 * clusters, kThreads, PAIR_SMEM_BYTES, st>>>(ma, mbh, M, N, K, C, ldc, mc);
+  launch_pdl(k_gemm_pair<EPI>, dim3(2 * clusters), dim3(kThreads), PAIR_SMEM_BYTES, st, ma, mbh, M, N, K, C, ldc,
+                 mc);
 }
 
 template <int EPI>

@@ -10,6 +10,7 @@
 #include "device.cuh"
 #include "kernels_bf16.cuh"
 #include "kernels_simt.cuh"
+#include "tc_common.cuh"
 
 namespace bp {
 
@@ -60,6 +61,9 @@ template <int NV>
 __global__ void __launch_bounds__(256) k_ln_bf16_reg(const float* __restrict__ x, int64_t ldx,
                                                      const float* __restrict__ g, const float* __restrict__ b,
                                                      int64_t rows, int n, bf16* __restrict__ y) {
+  // launched as a programmatic dependent of the residual GEMM: the CTAs are
+  // resident before it ends and start reading x as soon as its writes land
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= rows) return;
@@ -101,12 +105,15 @@ void launch_ln_bf16(const float* x, int64_t ldx, const float* g, const float* b,
   if (rows <= 0) return;
   if (n % 4 != 0 || ldx % 4 != 0) fail(BP_ERR_CONFIG, "bf16 path needs hidden % 4 == 0");
   const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
+  auto pdl = [&](auto kern) {  // programmatic dependent launch (overlaps the launch with the producer's tail)
+    launch_pdl(kern, dim3(blocks), dim3(256), 0, st, x, ldx, g, b, rows, n, y);
+  };
   switch (n) {  // register-resident rows for the hidden sizes in use (Wan 1.3B / 14B, test models)
-    case 128: k_ln_bf16_reg<1><<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
-    case 256: k_ln_bf16_reg<2><<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
-    case 512: k_ln_bf16_reg<4><<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
-    case 1536: k_ln_bf16_reg<12><<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
-    case 5120: k_ln_bf16_reg<40><<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
+    case 128: pdl(k_ln_bf16_reg<1>); break;
+    case 256: pdl(k_ln_bf16_reg<2>); break;
+    case 512: pdl(k_ln_bf16_reg<4>); break;
+    case 1536: pdl(k_ln_bf16_reg<12>); break;
+    case 5120: pdl(k_ln_bf16_reg<40>); break;
     default: k_ln_bf16<<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
   }
   count_launch();

@@ -8,6 +8,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <string>
+#include <utility>
 
 namespace bp {
 namespace tc {
@@ -122,6 +125,12 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_group() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
+
+// ---- programmatic dependent launch ----------------------------------------------------
+// Kernels launched with launch_pdl may start while the previous kernel in the
+// stream is still running; they do their setup (barriers, TMEM, descriptor
+// prefetch) and then wait here before touching anything it produced.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // ---- thread-block clusters --------------------------------------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -550,6 +559,24 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 }  // namespace tc
+
+// Host: launch with programmatic stream serialization (see pdl_wait).
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  static const bool off = std::getenv("BP_NO_PDL") != nullptr;  // A/B switch: plain stream order
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = off ? 0 : 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (e != cudaSuccess) fail(BP_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
+}
 
 // Host: TMA descriptor for a row-major bf16 matrix [rows, cols] (row stride ld
 // elements), box [box_rows, box_cols], 128-byte swizzle. Zero-fills OOB.
