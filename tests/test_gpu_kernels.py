@@ -85,7 +85,8 @@ def test_gemm_bench(lib):
 @pytest.mark.parametrize("impl", [1, 2, 3, 4])
 @pytest.mark.parametrize("rows,n0,n1,heads", [(128, 0, 128, 1), (300, 0, 300, 2), (300, 200, 300, 2),
                                               (257, 256, 129, 2), (96, 0, 512, 3), (1000, 640, 1000, 1),
-                                              (513, 65, 63, 2), (256, 0, 1, 1), (40, 7, 100, 2)])
+                                              (513, 65, 63, 2), (256, 0, 1, 1), (40, 7, 100, 2),
+                                              (512, 0, 1024, 2), (256, 512, 1024, 1), (300, 0, 512, 1)])
 def test_attention_tcgen05(lib, rows, n0, n1, heads, impl):
     """impl 1: one 128-row Q tile per CTA; impl 2: ping-pong over two Q tiles, 64-key tiles;
     impl 3: two Q tiles, 128-key tiles, one S buffer per tile; impl 4: impl 2 on a CTA pair."""
