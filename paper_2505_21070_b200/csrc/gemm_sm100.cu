@@ -193,25 +193,40 @@ __global__ void __launch_bounds__(kThreads, 1)
 // 128-byte rows (4 rows fp32, 8 rows bf16) instead of 32 scattered 16-byte
 // pieces: the L1 work per tile drops 8x, which is what bounded the K = 1536
 // residual GEMMs.
+//
+// kCg2 (variant 3): the pair runs ONE cta_group::2 MMA per k-step, M = 256
+// (each CTA's 128 A rows) x N = 256 (each CTA stages its 128-row half of the
+// weight tile, no multicast): a stage is 32 KB instead of 48 KB, so the ring
+// holds 6 stages; the leader CTA issues every MMA, both CTAs' TMA loads
+// complete on the leader's full barriers, and each CTA's epilogue drains its
+// own 128 accumulator rows and reports to the leader's tempty barrier.
 constexpr uint32_t B_HALF = B_BYTES / 2;
-constexpr uint32_t PAIR_STAGING = (STAGES * (A_BYTES + B_BYTES) + 256 + 1023) & ~1023u;  // after ring + mbarriers
-constexpr uint32_t PAIR_SMEM_BYTES = PAIR_STAGING + 2 * 4 * 4096 + 1024;  // two 4 KB slabs per epilogue warp
-static_assert(PAIR_SMEM_BYTES <= 232448, "pair GEMM exceeds the 227 KB smem limit");
+template <bool kCg2>
+struct PairLayout {
+  static constexpr int kStages = kCg2 ? 6 : STAGES;
+  static constexpr uint32_t kStageB = kCg2 ? B_HALF : B_BYTES;
+  static constexpr uint32_t kStaging = (kStages * (A_BYTES + kStageB) + 256 + 1023) & ~1023u;  // after ring + mbarriers
+  static constexpr uint32_t kSmem = kStaging + 2 * 4 * 4096 + 1024;  // two 4 KB slabs per epilogue warp
+  static_assert(kSmem <= 232448, "pair GEMM exceeds the 227 KB smem limit");
+};
+constexpr uint32_t PAIR_SMEM_BYTES = PairLayout<false>::kSmem;
 
-template <int EPI>
+template <int EPI, bool kCg2 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bh, int M, int N,
                 int K, void* __restrict__ Cv, int64_t ldc, const __grid_constant__ CUtensorMap map_c) {
+  using L = PairLayout<kCg2>;
+  constexpr int kSt = L::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
-  uint8_t* sb = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sb + STAGES * B_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sb = smem + kSt * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + kSt * L::kStageB);
+  uint64_t* empty = full + kSt;
+  uint64_t* tfull = empty + kSt;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* staging = smem + PAIR_STAGING;  // 4 epilogue warps x 2 x 4 KB (1024-aligned: TMA swizzle atoms)
+  uint8_t* staging = smem + L::kStaging;  // 4 epilogue warps x 2 x 4 KB (1024-aligned: TMA swizzle atoms)
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int rank = static_cast<int>(tc::cluster_ctarank());
@@ -225,17 +240,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&map_a);
     tc::tma_prefetch(&map_bh);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < kSt; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 2);  // both CTAs' MMAs
+      tc::mbar_init(&empty[s], kCg2 ? 1 : 2);  // the leader's MMA / both CTAs' MMAs
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], 128);
+      tc::mbar_init(&tempty[a], kCg2 ? 8 : 128);  // cg2: one lane per epilogue warp of both CTAs
     }
     tc::fence_mbarrier_init_cluster();
   }
-  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  if (warp == 1) {
+    if (kCg2) tc::tmem_alloc_cg2<512>(tmem_slot);
+    else tc::tmem_alloc<512>(tmem_slot);
+  }
   tc::fence_before_sync();
   __syncthreads();
   tc::cluster_sync();  // barrier inits visible to the peer before any remote arrive / multicast
@@ -251,36 +269,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int m_blk = (pair / n_tiles) * 2 + rank, n_blk = pair % n_tiles;
       for (int kb = 0; kb < num_k; ++kb) {
         tc::mbar_wait(&empty[stage], phase ^ 1);
-        tc::mbar_arrive_expect_tx_elect(&full[stage], A_BYTES + B_BYTES);
-        tc::tma_load_2d_elect(sa + stage * A_BYTES, &map_a, &full[stage], kb * BK, m_blk * BM);
-        tc::tma_load_2d_multicast_elect(sb + stage * B_BYTES + rank * B_HALF, &map_bh, &full[stage], kb * BK,
-                                        n_blk * BN + rank * (BN / 2), kBoth);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (kCg2) {  // own A rows + own weight half, both completing on the leader's barrier
+          const uint32_t lf = tc::mapa_shared(tc::smem_u32(&full[stage]), 0);
+          if (rank == 0) tc::mbar_arrive_expect_tx_elect(&full[stage], 2 * (A_BYTES + B_HALF));
+          tc::tma_load_2d_cg2_elect(sa + stage * A_BYTES, &map_a, lf, kb * BK, m_blk * BM);
+          tc::tma_load_2d_cg2_elect(sb + stage * L::kStageB, &map_bh, lf, kb * BK, n_blk * BN + rank * (BN / 2));
+        } else {
+          tc::mbar_arrive_expect_tx_elect(&full[stage], A_BYTES + B_BYTES);
+          tc::tma_load_2d_elect(sa + stage * A_BYTES, &map_a, &full[stage], kb * BK, m_blk * BM);
+          tc::tma_load_2d_multicast_elect(sb + stage * B_BYTES + rank * B_HALF, &map_bh, &full[stage], kb * BK,
+                                          n_blk * BN + rank * (BN / 2), kBoth);
+        }
+        if (++stage == kSt) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer ---------------------------------------------------------------------
-    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int pair = cluster; pair < total; pair += nclusters) {
-      tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc::fence_after_sync();
-      const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
-      for (int kb = 0; kb < num_k; ++kb) {
-        tc::mbar_wait(&full[stage], phase);
+    // ---- MMA issuer (cg2: the leader only) --------------------------------------------------
+    if (!kCg2 || rank == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(kCg2 ? 2 * BM : BM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int pair = cluster; pair < total; pair += nclusters) {
+        tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc::fence_after_sync();
-        const uint32_t a0 = tc::smem_u32(sa + stage * A_BYTES);
-        const uint32_t b0 = tc::smem_u32(sb + stage * B_BYTES);
-        tc::mma_ss_k64_elect(d, tc::desc_sw128(a0, 1024, 16), tc::desc_sw128(b0, 1024, 16), idesc, kb ? 1u : 0u);
-        tc::mma_commit_multicast_elect(&empty[stage], kBoth);  // frees the stage in both CTAs
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < num_k; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::fence_after_sync();
+          const uint32_t a0 = tc::smem_u32(sa + stage * A_BYTES);
+          const uint32_t b0 = tc::smem_u32(sb + stage * L::kStageB);
+          if (kCg2) {
+            tc::mma_ss_k64_cg2_elect(d, tc::desc_sw128(a0, 1024, 16), tc::desc_sw128(b0, 1024, 16), idesc,
+                                     kb ? 1u : 0u);
+            tc::mma_commit_cg2_multicast_elect(&empty[stage], kBoth);
+          } else {
+            tc::mma_ss_k64_elect(d, tc::desc_sw128(a0, 1024, 16), tc::desc_sw128(b0, 1024, 16), idesc, kb ? 1u : 0u);
+            tc::mma_commit_multicast_elect(&empty[stage], kBoth);  // frees the stage in both CTAs
+          }
+          if (++stage == kSt) { stage = 0; phase ^= 1; }
+        }
+        if (kCg2) tc::mma_commit_cg2_multicast_elect(&tfull[acc], kBoth);
+        else tc::mma_commit_elect(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
       }
-      tc::mma_commit_elect(&tfull[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
     }
   } else {
     // ---- epilogue (warps 2..5 -> TMEM lane quarters 2,3,0,1), transposed through smem ----
@@ -373,7 +407,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         chunk(c + 32, old);
       }
       tc::fence_before_sync();
-      tc::mbar_arrive(&tempty[acc]);
+      if (kCg2) {  // the leader's MMA reuses the accumulator once both CTAs drained it
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster(tc::mapa_shared(tc::smem_u32(&tempty[acc]), 0));
+      } else {
+        tc::mbar_arrive(&tempty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -384,7 +423,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc::cluster_sync();  // the peer may still multicast into / arrive on this CTA's shared memory until here
   if (warp == 1) {
     tc::fence_after_sync();
-    tc::tmem_dealloc<512>(tmem_base);
+    if (kCg2) tc::tmem_dealloc_cg2<512>(tmem_base);
+    else tc::tmem_dealloc<512>(tmem_base);
   }
 }
 
@@ -409,18 +449,19 @@ struct MapKeyHash {
 };
 std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
-template <int EPI>
+template <int EPI, bool kCg2 = false>
 void launch_pair(const CUtensorMap& ma, const CUtensorMap& mbh, int M, int N, int K, void* C, int64_t ldc,
                  const CUtensorMap& mc, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    BP_CUDA(cudaFuncSetAttribute(k_gemm_pair<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_gemm_pair<EPI, kCg2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 PairLayout<kCg2>::kSmem));
     configured = true;
   }
   const int pairs = (((M + BM - 1) / BM + 1) / 2) * ((N + BN - 1) / BN);
   const int clusters = pairs < kNumSms / 2 ? pairs : kNumSms / 2;
-  launch_pdl(k_gemm_pair<EPI>, dim3(2 * clusters), dim3(kThreads), PAIR_SMEM_BYTES, st, ma, mbh, M, N, K, C, ldc,
-                 mc);
+  launch_pdl(k_gemm_pair<EPI, kCg2>, dim3(2 * clusters), dim3(kThreads), PairLayout<kCg2>::kSmem, st, ma, mbh, M, N, K,
+             C, ldc, mc);
 }
 
 template <int EPI>
@@ -505,7 +546,7 @@ void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int
   if ((lda * 2) % 16 || (K * 2) % 16 || N % 32 || ldc % 8)
     fail(BP_ERR_INTERNAL, "GEMM strides must be 16-byte multiples and N % 32 == 0");
   const CUtensorMap ma = cached_map(A, static_cast<uint64_t>(M), static_cast<uint64_t>(K), static_cast<uint64_t>(lda), BM, BK);
-  if (variant == 2) {  // cluster pair sharing the weight tile (128-row weight boxes)
+  if (variant == 2 || variant == 3) {  // cluster pair sharing the weight tile (128-row weight boxes)
     const CUtensorMap mbh =
         cached_map(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(K), BN / 2, BK);
     CUtensorMap mc = mbh;  // unused except by the residual epilogue
@@ -513,11 +554,20 @@ void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int
       if ((reinterpret_cast<uintptr_t>(C) & 15) || (ldc * 4) % 16) fail(BP_ERR_INTERNAL, "residual C must be 16-byte aligned");
       mc = cached_map_f32(C, static_cast<uint64_t>(M), static_cast<uint64_t>(N), static_cast<uint64_t>(ldc), 32, 32);
     }
-    switch (epi) {
-      case kGemmStoreBf16: launch_pair<kGemmStoreBf16>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-      case kGemmGeluBf16: launch_pair<kGemmGeluBf16>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-      case kGemmResidualF32: launch_pair<kGemmResidualF32>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-      default: launch_pair<kGemmStoreF32>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+    if (variant == 3) {  // one cta_group::2 MMA (M = 256) per k-step
+      switch (epi) {
+        case kGemmStoreBf16: launch_pair<kGemmStoreBf16, true>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+        case kGemmGeluBf16: launch_pair<kGemmGeluBf16, true>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+        case kGemmResidualF32: launch_pair<kGemmResidualF32, true>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+        default: launch_pair<kGemmStoreF32, true>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+      }
+    } else {
+      switch (epi) {
+        case kGemmStoreBf16: launch_pair<kGemmStoreBf16>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+        case kGemmGeluBf16: launch_pair<kGemmGeluBf16>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+        case kGemmResidualF32: launch_pair<kGemmResidualF32>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+        default: launch_pair<kGemmStoreF32>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+      }
     }
     count_launch();
     return;

@@ -400,10 +400,11 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
 
 namespace {
 // GEMM: 0 = SIMT check path, 1 = tcgen05 one CTA per tile, 2 = tcgen05 cluster
-// pair sharing the weight tile. BP_GEMM_IMPL overrides the default.
+// pair sharing the weight tile, 3 = cta_group::2 pair (M = 256 MMAs). BP_GEMM_IMPL
+// overrides the default.
 int default_gemm_impl() {
   const char* e = std::getenv("BP_GEMM_IMPL");
-  return e ? std::atoi(e) : 2;
+  return e ? std::atoi(e) : 3;
 }
 int g_gemm_impl = default_gemm_impl();
 // 0 = SIMT check path, 1 = tcgen05 one Q tile/CTA, 2 = tcgen05 ping-pong.

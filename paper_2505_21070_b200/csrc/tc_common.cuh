@@ -260,6 +260,26 @@ __device__ __forceinline__ void mma_ss_k128_cg2_elect(uint32_t tmem_d, uint64_t 
       "}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "n"(static_cast<uint64_t>(AH)), "n"(static_cast<uint64_t>(BH)));
 }
+// K=64 chain (4 x K=16) of cta_group::2 SS MMAs inside one 128-byte swizzle atom.
+__device__ __forceinline__ void mma_ss_k64_cg2_elect(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                                     uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t;\n"
+      ".reg .b64 a1, a2, a3, b1, b2, b3;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "setp.eq.b32 t, 0, 0;\n"
+      "add.s64 a1, %1, 2; add.s64 b1, %2, 2;\n"
+      "add.s64 a2, %1, 4; add.s64 b2, %2, 4;\n"
+      "add.s64 a3, %1, 6; add.s64 b3, %2, 6;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, t;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
 // K=64 chain of cta_group::2 TS MMAs (see mma_ts_k64_elect).
 template <uint32_t BSTEP>
 __device__ __forceinline__ void mma_ts_k64_cg2_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,

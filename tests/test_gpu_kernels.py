@@ -17,7 +17,7 @@ def lib(bp):
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 512, 128), (1000, 1536, 1536), (257, 4608, 256),
                                    (64, 96, 64), (130, 8960, 128)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
-@pytest.mark.parametrize("impl", [1, 2])
+@pytest.mark.parametrize("impl", [1, 2, 3])
 def test_gemm_tcgen05(lib, M, N, K, epi, impl):
     """impl 1: one CTA per 128x256 tile; impl 2: 2-CTA cluster sharing the weight tile (multicast)."""
     rng = np.random.default_rng(M * 7 + N + K + epi)
@@ -45,7 +45,7 @@ def test_gemm_tcgen05(lib, M, N, K, epi, impl):
     assert np.linalg.norm(g - c) / np.linalg.norm(c) < (5e-3 if epi in (0, 1) else 1e-5)
 
 
-@pytest.mark.parametrize("impl", [1, 2])
+@pytest.mark.parametrize("impl", [1, 2, 3])
 def test_gemm_row_position_invariance(lib, impl):
     """A row's result does not depend on its M position (cached == recompute),
     nor on which GEMM implementation or cluster CTA computed it."""
