@@ -462,7 +462,7 @@ def main():
         "s_per_video": s_video, "latent_frames_per_s": sum(b["frames"] for b in sched.blocks) / s_video,
         "peak_hbm_gb": stats["peak_bytes"] / 1e9,
         "model_tflops": fl_video / s_video / 1e12,
-        "roofline": {"bound": "tensor", "kernel": "k_attn_pp (self-attention, tcgen05 ping-pong)",
+        "roofline": {"bound": "tensor", "kernel": "k_attn_pp2 (self-attention, tcgen05 ping-pong on a cta_group::2 pair)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_kind": f"{peak_kind} sustained (kernel timed inside a long step)",

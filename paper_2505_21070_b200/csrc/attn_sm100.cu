@@ -673,6 +673,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
   tc::cluster_sync();  // barrier inits of both CTAs visible before any remote arrive / TMA
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
+  tc::pdl_wait();  // Q/K/V were produced by the previous kernel
 
   if (warp == 0) {
     // ---- TMA producer (both CTAs): own Q tiles, own K / V halves -> leader's barriers ----
@@ -1211,7 +1212,7 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     }
     const unsigned pairs = static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ));
     dim3 grid(pairs + (pairs & 1u), static_cast<unsigned>(a.heads));
-    k_attn_pp2<1><<<grid, PP_THREADS, P2_SMEM_BYTES, st>>>(pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
+    launch_pdl(k_attn_pp2<1>, grid, dim3(PP_THREADS), P2_SMEM_BYTES, st, pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
   } else if (variant == 3) {  // two Q tiles per CTA, 128-key tiles, one S buffer per tile
     dim3 grid(static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(a.heads));
     k_attn_fa<<<grid, FA_THREADS, FA_SMEM_BYTES, st>>>(maps, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);

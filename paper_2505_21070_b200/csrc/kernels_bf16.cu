@@ -407,11 +407,12 @@ int default_gemm_impl() {
   return e ? std::atoi(e) : 3;
 }
 int g_gemm_impl = default_gemm_impl();
-// 0 = SIMT check path, 1 = tcgen05 one Q tile/CTA, 2 = tcgen05 ping-pong.
+// 0 = SIMT check path, 1 = tcgen05 one Q tile/CTA, 2 = tcgen05 ping-pong, 3 = 128-key
+// tiles with one S buffer per tile, 4 = the ping-pong on a cta_group::2 pair.
 // BP_ATTN_IMPL overrides the default (A/B runs of the whole suite).
 int default_attn_impl() {
   const char* e = std::getenv("BP_ATTN_IMPL");
-  return e ? std::atoi(e) : 2;
+  return e ? std::atoi(e) : 4;
 }
 int g_attn_impl = default_attn_impl();
 }  // namespace

@@ -52,5 +52,5 @@ def ref_attn(q, k, v, heads, dh, scale):
 
 
 # the library's default attention implementation (kernels_bf16.cu), restored after A/B tests
-DEFAULT_ATTN_IMPL = int(os.environ.get("BP_ATTN_IMPL", "2"))
+DEFAULT_ATTN_IMPL = int(os.environ.get("BP_ATTN_IMPL", "4"))
 DEFAULT_GEMM_IMPL = int(os.environ.get("BP_GEMM_IMPL", "3"))

@@ -14,7 +14,7 @@ what = sys.argv[1] if len(sys.argv) > 1 else "attn"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 only = sys.argv[3] if len(sys.argv) > 3 else ""  # substring filter on the case tag
 ms = ctypes.c_double()
-impl = os.environ.get("BP_ATTN_IMPL", "2")
+impl = os.environ.get("BP_ATTN_IMPL", "4")
 if what in ("attn", "all"):
     # (rows, heads, dh, prefix n0, block n1): prefix pass, plain pass, cross-attention
     for rows, n0, n1, tag in ((18720, 6240, 18720, "self+prefix"), (18720, 0, 18720, "self"),
