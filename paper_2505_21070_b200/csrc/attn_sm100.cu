@@ -1184,6 +1184,7 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     BP_CUDA(cudaFuncSetAttribute(k_attn_pp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
     BP_CUDA(cudaFuncSetAttribute(k_attn_fa, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM_BYTES));
     BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
     configured = true;
   }
   AttnMaps maps;
@@ -1212,7 +1213,14 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     }
     const unsigned pairs = static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ));
     dim3 grid(pairs + (pairs & 1u), static_cast<unsigned>(a.heads));
-    launch_pdl(k_attn_pp2<1>, grid, dim3(PP_THREADS), P2_SMEM_BYTES, st, pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
+    // every exp2 on MUFU by default here: the pair leaves the MUFU pipe headroom
+    // and the FMA-pipe polynomial costs issue slots (15.64 vs 16.22 s per video)
+    static const int poly2 = [] {
+      const char* e = std::getenv("BP_ATTN_POLY");
+      return e ? std::atoi(e) : 0;
+    }();
+    launch_pdl(poly2 == 0 ? k_attn_pp2<0> : k_attn_pp2<1>, grid, dim3(PP_THREADS), P2_SMEM_BYTES, st, pm, rows, a.n0,
+               a.n1, scale_log2, a.out, a.ldo);
   } else if (variant == 3) {  // two Q tiles per CTA, 128-key tiles, one S buffer per tile
     dim3 grid(static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(a.heads));
     k_attn_fa<<<grid, FA_THREADS, FA_SMEM_BYTES, st>>>(maps, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
