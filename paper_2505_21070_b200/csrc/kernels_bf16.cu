@@ -431,15 +431,21 @@ void launch_gemm_bf16(const bf16* A, int64_t lda, const bf16* W, int M, int N, i
 
 void launch_attn_bf16(const AttnBf16Args& a, int64_t rows, cudaStream_t st) {
   if (rows <= 0) return;
-  // short key ranges (cross-attention over the 512-token context, 8 key tiles)
-  // run the single-CTA ping-pong (variant 2): the pair's cluster setup does not
-  // pay off there (0.48 vs 0.51 s of cross-attention per video). BP_CROSS_IMPL
-  // overrides (-1: same as self-attention).
+  if (g_attn_impl >= 1) launch_attn_tc(a, rows, st, g_attn_impl);
+  else launch_attn_simt(a, rows, st);
+}
+
+void launch_attn_bf16_cross(const AttnBf16Args& a, int64_t rows, cudaStream_t st) {
+  if (rows <= 0) return;
+  // cross-attention over the 512-token context (8 key tiles) runs the
+  // single-CTA ping-pong (variant 2): the pair's cluster setup does not pay
+  // off there (0.48 vs 0.51 s of cross-attention per video). BP_CROSS_IMPL
+  // overrides (-1: the self-attention variant).
   static const int cross_impl = [] {
     const char* e = std::getenv("BP_CROSS_IMPL");
     return e ? std::atoi(e) : 2;
   }();
-  const int impl = (cross_impl >= 0 && g_attn_impl >= 1 && a.n0 + a.n1 <= 1024) ? cross_impl : g_attn_impl;
+  const int impl = (cross_impl >= 0 && g_attn_impl >= 1) ? cross_impl : g_attn_impl;
   if (impl >= 1) launch_attn_tc(a, rows, st, impl);
   else launch_attn_simt(a, rows, st);
 }

@@ -50,6 +50,8 @@ struct AttnBf16Args {
 // Non-causal multi-head attention (model.cpp:47-72) of q rows against
 // [prefix ++ current] keys; softmax in fp32.
 void launch_attn_bf16(const AttnBf16Args& a, int64_t rows, cudaStream_t st);
+// The cross-attention call (short key range; see kernels_bf16.cu).
+void launch_attn_bf16_cross(const AttnBf16Args& a, int64_t rows, cudaStream_t st);
 void set_attn_impl(int impl);
 int attn_impl();
 

@@ -575,7 +575,7 @@ const void* Stage::forward_bf16(const StageInput& in) {
     c.out = at; c.ldo = H;
     c.heads = heads_; c.dh = dh_; c.scale = scale;
     prof_mark(1, true);
-    launch_attn_bf16(c, S, st);
+    launch_attn_bf16_cross(c, S, st);
     prof_mark(1, false);
     prof_mark(2, true);
     launch_gemm_bf16(at, H, static_cast<const bf16*>(w.co), static_cast<int>(S), h_, h_, x, H,
