@@ -34,8 +34,8 @@ WORKLOADS = {
     1: dict(WAN13, blocks=3, frames=81, name="Wan2.1-1.3B-shape 81f 480p (BASELINE configs[1])"),
     "multi": dict(WAN13, blocks=9, frames=301, name="Wan2.1-1.3B-shape 301f 480p (BASELINE configs[2])"),
     # wiring checks only (the mid parity config: 4 layers, h 256, 3 blocks x 6 steps)
-    "tiny": dict(layers=4, hidden=256, heads=2, ffn=1024, channels=64, height=4, width=6, context_len=16,
-                 num_b=8, num_c=8, steps=6, blocks=3, frames=41, name="mid parity config (wiring check only)"),
+    "tiny": dict(layers=8, hidden=256, heads=2, ffn=1024, channels=64, height=4, width=6, context_len=16,
+                 num_b=8, num_c=8, steps=6, blocks=3, frames=41, name="8-layer mid parity shape (wiring check only)"),
     # the paper's headline video length (BASELINE configs[3] names 8 GPUs);
     # selectable at any N, e.g. N = 1 for the single-GPU reference point
     "wan13-1025": dict(WAN13, blocks=32, frames=1025, name="Wan2.1-1.3B-shape 1025f 480p (BASELINE configs[3] video)"),
