@@ -347,6 +347,7 @@ static_assert(PP_SMEM_BYTES <= 232448, "ping-pong attention exceeds the 227 KB s
 
 struct AttnMapsPP {
   CUtensorMap q, k0, v0, k1, v1;  // q: 128-row boxes; k/v: 64-row boxes
+  CUtensorMap o;                  // output, 128-row boxes (epilogue TMA stores)
 };
 
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
@@ -565,24 +566,40 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       tc::mbar_wait(&pv_done[x], (T - 1) & 1);
       tc::fence_after_sync();
     }
-    const int64_t row = static_cast<int64_t>(qpair) * 2 * BQ + x * BQ + r;
+    // epilogue: O / l as bf16 into the idle K ring (every QK^T of both tiles
+    // completed before this tile's last PV) in the output map's 128B-swizzled
+    // [128 rows][64 cols] layout, then two TMA stores: whole rows per
+    // transaction instead of 16-byte pieces from 32 rows per instruction
     const float inv_l = 1.f / (l2.x + l2.y);
+    uint8_t* stage_o = smem + PP_K + x * TILE;
+    const uint32_t so = tc::smem_u32(stage_o);
 #pragma unroll 1
     for (int c = 0; c < 4; ++c) {
       uint32_t o[32];
       tc::tmem_ld32(tm_o + static_cast<uint32_t>(c * 32), o);
       tc::tmem_ld_wait();
-      if (row < rows) {
-        uint4* dst = reinterpret_cast<uint4*>(out + row * ldo + head * kDh + c * 32);
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          dst[v] = make_uint4(pack_bf16(__uint_as_float(o[8 * v]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l),
-                              pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l),
-                              pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l),
-                              pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l));
-        }
+      for (int v = 0; v < 4; ++v) {
+        const uint32_t unit = static_cast<uint32_t>((c & 1) * 4 + v);
+        tc::st_shared_v4(so + static_cast<uint32_t>((c >> 1) * HALF + r * 128) + ((unit ^ static_cast<uint32_t>(r & 7)) << 4),
+                         pack_bf16(__uint_as_float(o[8 * v]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l),
+                         pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l),
+                         pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l),
+                         pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l));
       }
     }
+    tc::fence_proxy_async_smem();
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + x) : "memory");  // this tile's 128 softmax threads
+    if (qq == 0 && lane == 0) {
+      const int qrow = qpair * 2 * BQ + x * BQ;
+      tc::tma_store_2d(&maps.o, stage_o, head * kDh, qrow);
+      tc::tma_store_2d(&maps.o, stage_o + HALF, head * kDh + 64, qrow);
+      tc::bulk_commit_group();
+      tc::bulk_wait_group_read<0>();  // smem read out; the global writes drain on their own
+    }
+    (void)out;
+    (void)ldo;
+    (void)rows;
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -619,9 +636,10 @@ static_assert(P2_SMEM_BYTES <= 232448, "pair attention exceeds the 227 KB smem l
 
 struct AttnMapsP2 {
   CUtensorMap q, k0, v0, k1, v1;  // q: 128-row boxes; k: 32-row boxes; v: 64-row boxes
+  CUtensorMap o;                  // output, 128-row boxes (epilogue TMA stores)
 };
 
-template <int kPoly>
+template <int kPoly, bool kTmaEpi = true>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     k_attn_pp2(const __grid_constant__ AttnMapsP2 maps, int64_t rows, int64_t n0, int64_t n1, float scale_log2,
                bf16* __restrict__ out, int64_t ldo) {
@@ -824,6 +842,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     }
     const int64_t row = static_cast<int64_t>(qpair) * 2 * BQ + x * BQ + r;
     const float inv_l = 1.f / (l2.x + l2.y);
+    if (kTmaEpi) {
+      // O / l as bf16 into this tile's Q buffer (every QK^T completed before its
+      // last PV) in the output map's swizzled [128][64] layout, then TMA stores
+      uint8_t* stage_o = smem + P2_Q + x * TILE;
+      const uint32_t so = tc::smem_u32(stage_o);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t o[32];
+        tc::tmem_ld32(tm_o + static_cast<uint32_t>(c * 32), o);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const uint32_t unit = static_cast<uint32_t>((c & 1) * 4 + v);
+          tc::st_shared_v4(so + static_cast<uint32_t>((c >> 1) * HALF + r * 128) + ((unit ^ static_cast<uint32_t>(r & 7)) << 4),
+                           pack_bf16(__uint_as_float(o[8 * v]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l),
+                           pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l),
+                           pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l),
+                           pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l));
+        }
+      }
+      tc::fence_proxy_async_smem();
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + x) : "memory");  // this tile's 128 softmax threads
+      if (qq == 0 && lane == 0) {
+        const int qrow = qpair * 2 * BQ + x * BQ;
+        tc::tma_store_2d(&maps.o, stage_o, head * kDh, qrow);
+        tc::tma_store_2d(&maps.o, stage_o + HALF, head * kDh + 64, qrow);
+        tc::bulk_commit_group();
+        tc::bulk_wait_group_read<0>();
+      }
+    } else
 #pragma unroll 1
     for (int c = 0; c < 4; ++c) {
       uint32_t o[32];
@@ -1185,6 +1233,8 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     BP_CUDA(cudaFuncSetAttribute(k_attn_fa, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM_BYTES));
     BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
     BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
     configured = true;
   }
   AttnMaps maps;
@@ -1219,8 +1269,20 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
       const char* e = std::getenv("BP_ATTN_POLY");
       return e ? std::atoi(e) : 0;
     }();
-    launch_pdl(poly2 == 0 ? k_attn_pp2<0> : k_attn_pp2<1>, grid, dim3(PP_THREADS), P2_SMEM_BYTES, st, pm, rows, a.n0,
-               a.n1, scale_log2, a.out, a.ldo);
+    // epilogue: direct 16-byte stores (default) or smem + TMA stores
+    // (BP_ATTN_TMA_EPI=1): equal in the step (15.64-15.65 s either way), the
+    // direct stores 2-3% faster in isolation. The single-CTA kernel, which runs
+    // the short cross-attention, always stages through smem (0.48 -> 0.40 s).
+    static const bool tma_epi = [] {
+      const char* e = std::getenv("BP_ATTN_TMA_EPI");
+      return e && std::atoi(e) != 0;
+    }();
+    if ((reinterpret_cast<uintptr_t>(a.out) | static_cast<uintptr_t>(a.ldo * 2)) % 16)
+      fail(BP_ERR_INTERNAL, "attention output must be 16-byte aligned");
+    pm.o = map_for(a.out, rows, H, a.ldo);
+    auto kern = tma_epi ? (poly2 == 0 ? k_attn_pp2<0, true> : k_attn_pp2<1, true>)
+                        : (poly2 == 0 ? k_attn_pp2<0, false> : k_attn_pp2<1, false>);
+    launch_pdl(kern, grid, dim3(PP_THREADS), P2_SMEM_BYTES, st, pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
   } else if (variant == 3) {  // two Q tiles per CTA, 128-key tiles, one S buffer per tile
     dim3 grid(static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(a.heads));
     k_attn_fa<<<grid, FA_THREADS, FA_SMEM_BYTES, st>>>(maps, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
@@ -1236,6 +1298,9 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
       pm.k0 = pm.k1;
       pm.v0 = pm.v1;
     }
+    if ((reinterpret_cast<uintptr_t>(a.out) | static_cast<uintptr_t>(a.ldo * 2)) % 16)
+      fail(BP_ERR_INTERNAL, "attention output must be 16-byte aligned");
+    pm.o = map_for(a.out, rows, H, a.ldo);
     dim3 grid(static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(a.heads));
     // pairs of exp2 (out of 4) evaluated on the FMA pipe; BP_ATTN_POLY overrides (A/B runs)
     static const int poly = [] {
