@@ -809,7 +809,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
       for (int c = 0; c < 32; ++c) {
         const float2 xv = __ffma2_rn(make_float2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sc2,
                                      neg_m2);
-        const float2 p = (c & 3) >= 4 - kPoly ? ex2_poly2(xv) : make_float2(ex2(xv.x), ex2(xv.y));
+        const float2 p = (kPoly == 9 ? (c & 7) == 7 : (c & 3) >= 4 - kPoly) ? ex2_poly2(xv) : make_float2(ex2(xv.x), ex2(xv.y));
         if (c & 1) ls_b = __fadd2_rn(ls_b, p);
         else ls_a = __fadd2_rn(ls_a, p);
         pk[c] = pack_bf16(p.x, p.y);
@@ -1231,10 +1231,10 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     BP_CUDA(cudaFuncSetAttribute(k_attn_pp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
     BP_CUDA(cudaFuncSetAttribute(k_attn_pp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
     BP_CUDA(cudaFuncSetAttribute(k_attn_fa, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM_BYTES));
-    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
     BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
-    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
-    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
+    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
     configured = true;
   }
   AttnMaps maps;
@@ -1263,11 +1263,13 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     }
     const unsigned pairs = static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ));
     dim3 grid(pairs + (pairs & 1u), static_cast<unsigned>(a.heads));
-    // every exp2 on MUFU by default here: the pair leaves the MUFU pipe headroom
-    // and the FMA-pipe polynomial costs issue slots (15.64 vs 16.22 s per video)
+    // exp2 pairs in 8 on the FMA pipe (BP_ATTN_POLY overrides; default 1): the
+    // pair's softmax is latency-bound, so the polynomial pays only in small
+    // doses -- 1 in 8 beats all-MUFU (15.47-15.50 vs 15.68-15.69 s per video,
+    // same box twice) and 1 in 4 (16.22 s)
     static const int poly2 = [] {
       const char* e = std::getenv("BP_ATTN_POLY");
-      return e ? std::atoi(e) : 0;
+      return e ? std::atoi(e) : 1;
     }();
     // epilogue: direct 16-byte stores (default) or smem + TMA stores
     // (BP_ATTN_TMA_EPI=1): equal in the step (15.64-15.65 s either way), the
@@ -1280,8 +1282,7 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     if ((reinterpret_cast<uintptr_t>(a.out) | static_cast<uintptr_t>(a.ldo * 2)) % 16)
       fail(BP_ERR_INTERNAL, "attention output must be 16-byte aligned");
     pm.o = map_for(a.out, rows, H, a.ldo);
-    auto kern = tma_epi ? (poly2 == 0 ? k_attn_pp2<0, true> : k_attn_pp2<1, true>)
-                        : (poly2 == 0 ? k_attn_pp2<0, false> : k_attn_pp2<1, false>);
+    auto kern = tma_epi ? k_attn_pp2<1, true> : (poly2 == 0 ? k_attn_pp2<0> : (poly2 == 2 ? k_attn_pp2<2> : k_attn_pp2<1>));
     launch_pdl(kern, grid, dim3(PP_THREADS), P2_SMEM_BYTES, st, pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
   } else if (variant == 3) {  // two Q tiles per CTA, 128-key tiles, one S buffer per tile
     dim3 grid(static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(a.heads));
