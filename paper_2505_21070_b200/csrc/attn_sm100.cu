@@ -639,7 +639,8 @@ struct AttnMapsP2 {
   CUtensorMap o;                  // output, 128-row boxes (epilogue TMA stores)
 };
 
-template <int kPoly, bool kTmaEpi = true>
+// kPoly8: exp2 pairs in 8 evaluated on the FMA pipe
+template <int kPoly8, bool kTmaEpi = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     k_attn_pp2(const __grid_constant__ AttnMapsP2 maps, int64_t rows, int64_t n0, int64_t n1, float scale_log2,
                bf16* __restrict__ out, int64_t ldo) {
@@ -809,7 +810,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
       for (int c = 0; c < 32; ++c) {
         const float2 xv = __ffma2_rn(make_float2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sc2,
                                      neg_m2);
-        const float2 p = (kPoly == 9 ? (c & 7) == 7 : (c & 3) >= 4 - kPoly) ? ex2_poly2(xv) : make_float2(ex2(xv.x), ex2(xv.y));
+        const float2 p = (c & 7) >= 8 - kPoly8 ? ex2_poly2(xv) : make_float2(ex2(xv.x), ex2(xv.y));
         if (c & 1) ls_b = __fadd2_rn(ls_b, p);
         else ls_a = __fadd2_rn(ls_a, p);
         pk[c] = pack_bf16(p.x, p.y);
