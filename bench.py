@@ -2,14 +2,18 @@
 """Benchmark of the block-wise denoising path (DualParal) on B200.
 
 A "step" is one whole video generation: noise pool build, all T + B - 1
-denoising rounds of the layer pipeline, emission of every clean block. The
-N=1 workload is BASELINE configs[1] (Wan2.1-1.3B-shape DiT, 81 frames 480p:
-21 latent frames -> 3 blocks of 8 + 4 context frames, T = 50, 150 passes);
-N>1 runs configs[2] (301 frames, 9 blocks) on the NCCL layer pipeline.
+denoising rounds of the layer pipeline, emission of every clean block. Every
+N runs the same workload, BASELINE configs[2] (Wan2.1-1.3B-shape DiT, 301
+frames 480p: 76 latent frames -> 9 blocks of 8 + 4 context frames, T = 50,
+450 passes), so a 1 -> 8 GPU curve is strong scaling of one video.
 Weights are random-init of that architecture, latents are the reference's
 synthetic noise pool; inputs larger than L2 (18720 x 1536 activations).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU implementation (the
+unmodified reference library compiled into oracle/_ref) on this host; it
+never imports this repo's package or loads its CUDA library.
 """
 from __future__ import annotations
 
@@ -17,11 +21,13 @@ import argparse
 import json
 import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
 import threading
 import time
+from types import SimpleNamespace
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -31,14 +37,13 @@ METRIC = "s per 1025-frame video & frames/s at 1/2/4/8 B200; peak HBM GB/GPU"
 WAN13 = dict(layers=30, hidden=1536, heads=12, ffn=8960, channels=64, height=30, width=52, context_len=512,
              num_b=8, num_c=8, steps=50)
 WORKLOADS = {
-    1: dict(WAN13, blocks=3, frames=81, name="Wan2.1-1.3B-shape 81f 480p (BASELINE configs[1])"),
-    "multi": dict(WAN13, blocks=9, frames=301, name="Wan2.1-1.3B-shape 301f 480p (BASELINE configs[2])"),
-    # wiring checks only (the mid parity config: 4 layers, h 256, 3 blocks x 6 steps)
+    "wan13-301": dict(WAN13, blocks=9, frames=301, name="Wan2.1-1.3B-shape 301f 480p (BASELINE configs[2])"),
+    "wan13-81": dict(WAN13, blocks=3, frames=81, name="Wan2.1-1.3B-shape 81f 480p (BASELINE configs[1])"),
+    # the paper's headline video length (BASELINE configs[3] names 8 GPUs)
+    "wan13-1025": dict(WAN13, blocks=32, frames=1025, name="Wan2.1-1.3B-shape 1025f 480p (BASELINE configs[3] video)"),
+    # wiring checks only (8 layers at the mid parity shape, 3 blocks x 6 steps)
     "tiny": dict(layers=8, hidden=256, heads=2, ffn=1024, channels=64, height=4, width=6, context_len=16,
                  num_b=8, num_c=8, steps=6, blocks=3, frames=41, name="8-layer mid parity shape (wiring check only)"),
-    # the paper's headline video length (BASELINE configs[3] names 8 GPUs);
-    # selectable at any N, e.g. N = 1 for the single-GPU reference point
-    "wan13-1025": dict(WAN13, blocks=32, frames=1025, name="Wan2.1-1.3B-shape 1025f 480p (BASELINE configs[3] video)"),
 }
 # BASELINE configs[4] (14B, 1025 frames 720p, 8 GPUs): the 8-stage layer split
 # on one GPU through the loopback transport, over a bounded sample of the
@@ -157,46 +162,112 @@ class ClockSampler:
                 "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
 
 
-def cpu_baseline(w, sched, threads=None, tokens_per_sample=16):
-    """Times the UNMODIFIED reference forward_chunk (oracle/_ref) on a bounded
-    sample: one Wan-width layer (h, heads, Lc, C) over `tokens_per_sample`
-    tokens, `threads` independent samples in parallel, then extrapolates the
-    video time as reference-algorithm FLOPs / measured FLOP rate."""
-    import numpy as np
-    from concurrent.futures import ThreadPoolExecutor
+# ---- the reference's CPU implementation (oracle/_ref: the UNMODIFIED reference
+# library), used by --impl reference and by the cpu_baseline leg ---------------------
+REF_DEFAULTS = dict(devices=2, order="reverse", cache="on", threaded=True, num_b=2, num_c=4, steps=8, blocks=6,
+                    retain_clean_context=True, layers=4, hidden=16, heads=2, channels=2, height=2, width=2,
+                    context_len=4, strategy="coordinated", seed_model=1, seed_noise=2, seed_context=3,
+                    fault_inject=False, record_trace=False, check_cache=False)  # engine.hpp:24-38, model.hpp:21-28
 
+
+def ref_config(**kw):
+    """A PipelineConfig as the reference spells it (no import of this repo's package)."""
+    return SimpleNamespace(**dict(REF_DEFAULTS, **kw))
+
+
+def ref_schedule(w, n):
+    """Passes and rounds of the workload's schedule from the reference's own
+    run_pipeline (engine.cpp:255-497), run at a schedule-only width (1 x 1
+    latent grid, h 8): they depend on T, Block_num, num_b, num_c and N only."""
     from oracle import ref
-    import paper_2505_21070_b200 as bp
+    cfg = ref_config(devices=n, layers=n, hidden=8, heads=2, channels=1, height=1, width=1, context_len=2,
+                     num_b=w["num_b"], num_c=w["num_c"], steps=w["steps"], blocks=w["blocks"], threaded=False)
+    out = ref.run(cfg)
+    passes = len(out["events"]) // n
+    return SimpleNamespace(npasses=passes, rounds=int(out["rounds"]))
 
-    if not ref.available():
-        return None
-    threads = threads or min(os.cpu_count() or 1, 16)
-    side = int(math.isqrt(tokens_per_sample))
-    cfg = bp.PipelineConfig(layers=1, hidden=w["hidden"], heads=w["heads"], channels=w["channels"], height=side,
-                            width=tokens_per_sample // side, context_len=w["context_len"], devices=1)
-    chunks = [ref.RefChunk(cfg, 1, 0, 1, 3) for _ in range(threads)]
-    rng = np.random.default_rng(0)
-    payload = rng.standard_normal((tokens_per_sample, w["channels"]))
 
-    def one(ch):
-        ch.forward(payload, [10], [0], mode="off")
+def host_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except Exception:
+        pass
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    return {"nproc": cores, "cpu_model": model, "glibc": "-".join(platform.libc_ver())}
 
-    with ThreadPoolExecutor(threads) as ex:
-        t0 = time.perf_counter()
-        list(ex.map(one, chunks))
-        dt = time.perf_counter() - t0
-    # the sample's own reference-algorithm FLOPs (reference FFN width 4h)
-    wr = dict(w, layers=1, ffn=4 * w["hidden"])
-    f_sample = pass_flops(wr, tokens_per_sample, 0, reference_algorithm=True)
-    rate = threads * f_sample / dt  # FLOP/s over `threads` cores
-    f_video, _ = video_flops(w, sched, reference_algorithm=True)
-    sec_video = f_video / rate
-    return {"value": w["frames"] / sec_video, "unit": "frames/s", "cores": threads, "kind": "reference",
-            "sample": (f"{threads} x reference forward_chunk, 1 layer at h={w['hidden']} heads={w['heads']} "
-                       f"Lc={w['context_len']} C={w['channels']}, {tokens_per_sample} tokens, fp64; "
-                       f"{rate / 1e9 / threads:.3f} GFLOP/s/core over {dt:.1f} s, extrapolated to "
-                       f"{f_video:.3e} reference FLOP per video"),
-            "s_per_video_extrapolated": sec_video}
+
+def reference_legs(include_mid):
+    """End-to-end reference run_pipeline legs: configs[0]
+    (tiny DiT, 2 layers, d 128, 4 heads, 4 blocks x 10 steps) best of 5, single-
+    threaded (1 device) and threaded (2 device threads + coordinator,
+    engine.cpp:280-285); optionally the mid parity config (4 layers, h 256,
+    4 x 6 grid, C 64, 3 blocks x 6 steps) once each, 1 and 4 devices."""
+    from oracle import ref
+
+    def best(cfg, reps):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            ref.run(cfg)
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+
+    cfg1 = dict(layers=2, hidden=128, heads=4, steps=10, blocks=4)
+    legs = {"configs0_single_thread_s": best(ref_config(**cfg1, devices=1, threaded=False), 5),
+            "configs0_threaded_2dev_s": best(ref_config(**cfg1, devices=2, threaded=True), 5),
+            "configs0_note": "reference run_pipeline end to end, best of 5 (wall clock)"}
+    if include_mid:
+        mid = dict(layers=4, hidden=256, heads=2, channels=64, height=4, width=6, context_len=16, num_b=8, num_c=8,
+                   steps=6, blocks=3)
+        legs["mid_single_thread_s"] = best(ref_config(**mid, devices=1, threaded=False), 1)
+        legs["mid_threaded_4dev_s"] = best(ref_config(**mid, devices=4, threaded=True), 1)
+        legs["mid_note"] = "mid parity config (SURVEY Appendix A), reference run_pipeline end to end, once"
+    return legs
+
+
+class RefSample:
+    """The bounded sample of the workload on the reference: the UNMODIFIED
+    reference forward_chunk of one Wan-width layer (h, heads, Lc, C) over
+    `tokens` tokens, `threads` chunks in parallel (one per host core). The
+    chunks (weights drawn by the reference, model.cpp:87-128) are built once;
+    each call times one forward per chunk and extrapolates the video time as
+    reference-algorithm FLOPs / measured FLOP rate."""
+
+    def __init__(self, w, sched, threads=None, tokens=16):
+        from oracle import ref
+        self.w, self.sched, self.tokens = w, sched, tokens
+        self.threads = threads or min(host_info()["nproc"], 16)
+        side = int(math.isqrt(tokens))
+        cfg = ref_config(layers=1, hidden=w["hidden"], heads=w["heads"], channels=w["channels"], height=side,
+                         width=tokens // side, context_len=w["context_len"], devices=1)
+        self.chunks = [ref.RefChunk(cfg, 1, 0, 1, 3) for _ in range(self.threads)]
+        import numpy as np
+        self.payload = np.random.default_rng(0).standard_normal((tokens, w["channels"]))
+
+    def measure(self):
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(self.threads) as ex:
+            t0 = time.perf_counter()
+            list(ex.map(lambda ch: ch.forward(self.payload, [10], [0], mode="off"), self.chunks))
+            dt = time.perf_counter() - t0
+        w = self.w
+        # the sample's own reference-algorithm FLOPs (reference FFN width 4h)
+        f_sample = pass_flops(dict(w, layers=1, ffn=4 * w["hidden"]), self.tokens, 0, reference_algorithm=True)
+        rate = self.threads * f_sample / dt  # FLOP/s over `threads` cores
+        f_video, _ = video_flops(w, self.sched, reference_algorithm=True)
+        sec_video = f_video / rate
+        return {"value": w["frames"] / sec_video, "unit": "frames/s", "cores": self.threads, "kind": "reference",
+                "sample": (f"{self.threads} x reference forward_chunk, 1 layer at h={w['hidden']} heads={w['heads']} "
+                           f"Lc={w['context_len']} C={w['channels']}, {self.tokens} tokens, fp64; "
+                           f"{rate / 1e9 / self.threads:.3f} GFLOP/s/core over {dt:.1f} s, extrapolated to "
+                           f"{f_video:.3e} reference FLOP per video ({self.sched.npasses} passes, "
+                           f"{self.sched.rounds} rounds from the reference's own schedule)"),
+                "s_per_video_extrapolated": sec_video}
 
 
 def run_wan14b(args):
@@ -255,6 +326,76 @@ def run_wan14b(args):
         "gpu_launches": st["kernel_launches"], "clocks": clk.summary()}))
 
 
+def reference_arm(args, w, n, rank):
+    """--impl reference: the reference's CPU implementation on this host
+    (rank 0 only; other ranks exit without work). Each step is one bounded
+    sample of the workload (RefSample, ~10-15 s); measured end-to-end legs
+    of the reference's own CPU configs are reported beside it."""
+    if rank != 0:
+        return
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libbp_ref.so not built"}))
+        return
+    sched = ref_schedule(w, n)
+    sample = RefSample(w, sched)
+    legs = reference_legs(include_mid=not args.quick_reference)
+    for _ in range(args.warmup):
+        pass  # the reference keeps no state between samples: nothing to warm
+    vals, ms = [], []
+    cb = None
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cb = sample.measure()
+        ms.append(1000 * (time.perf_counter() - t0))
+        vals.append(cb["value"])
+    value = statistics.mean(vals)
+    cb = dict(cb, value=value, measured_legs=legs, host=host_info())
+    try:  # evidence that this arm ran the reference library only (no repo CUDA library mapped)
+        with open("/proc/self/maps") as f:
+            cb["repo_libraries_loaded"] = sorted({ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")
+                                                  and ln.split()[-1].startswith(ROOT)})
+    except Exception:
+        pass
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": n,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(ms),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference random-init weights, coordinated noise pool)",
+        "config": workload_config(w, n, sched, args),
+        "cpu_baseline": cb, "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                                     "d2h_bytes_per_step": 0}}))
+
+
+def workload_config(w, n, sched, args):
+    return {"workload": w["name"], "layers": w["layers"], "hidden": w["hidden"], "heads": w["heads"],
+            "ffn": w["ffn"], "latent_grid": [w["height"], w["width"], w["channels"]], "context_len": w["context_len"],
+            "num_b": w["num_b"], "num_c": w["num_c"], "steps": w["steps"], "blocks": w["blocks"],
+            "frames": w["frames"], "passes": sched.npasses, "prefix_passes": sched.npasses - sched.rounds,
+            "parallelism": f"layer-pipeline x{n}" + (f" ({args.transport})" if n > 1 else ""),
+            "l2": "inputs larger than L2 (18720x1536 activations per pass)"}
+
+
+def ln_kernel_roofline(device, tokens, hidden, peaks):
+    """LayerNorm (the elementwise path's largest kernel) from kernel time:
+    back-to-back launches on [tokens, hidden] fp32 -> bf16 (larger than L2),
+    CUDA events on the launching stream, through the kernel self-test library
+    (built from the same objects as libbp_cuda.so)."""
+    import ctypes
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from kernels import testlib
+    ms = ctypes.c_double()
+    if testlib().bp_bench_ln(device, tokens, hidden, 20, ctypes.byref(ms)) != 0:
+        return None
+    bytes_launch = tokens * hidden * 6 + 2 * hidden * 4  # x read (fp32) + y written (bf16) + g, b
+    gbs = bytes_launch / (ms.value * 1e-3) / 1e9
+    return {"bound": "hbm", "kernel": "k_ln_bf16_reg (LayerNorm + affine, fp32 -> bf16)", "achieved": gbs,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"], "bytes_per_launch": bytes_launch,
+            "us_per_launch": ms.value * 1e3,
+            "timing": "kernel time: 20 back-to-back launches on device-resident [tokens, hidden] (inputs > L2), "
+                      "CUDA events on the launching stream"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -262,11 +403,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick-reference", action="store_true",
+                    help="reference arm without the mid-config end-to-end legs (~2 min of CPU)")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
                     help="N > 1 stage-boundary transport: NCCL send/recv or CUDA-IPC peer copies")
-    ap.add_argument("--workload", default="auto", choices=["auto", "wan14b", "wan13-301", "wan13-1025", "tiny"],
-                    help="auto: configs[1] at N=1, configs[2] at N>1; wan13-301 / wan13-1025: those videos at "
-                         "any N; wan14b: the configs[4] sample leg")
+    ap.add_argument("--workload", default="wan13-301", choices=["wan13-301", "wan13-81", "wan13-1025", "tiny",
+                                                                "wan14b"],
+                    help="wan13-301 (default, every N): configs[2]; wan13-81: configs[1]; wan13-1025: the "
+                         "configs[3] video at any N; wan14b: the configs[4] sample leg")
     args = ap.parse_args()
     if args.workload == "wan14b":
         return run_wan14b(args)
@@ -274,6 +418,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = max(args.gpus, world)
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return reference_arm(args, w, n, rank)
+
     if os.environ.get("BP_BENCH_ONE_GPU") == "1" and world > 1:
         # wiring check of the N > 1 path on a single GPU: every rank on device
         # 0, NCCL told the ranks are separate hosts (socket transport); the
@@ -282,13 +431,6 @@ def main():
         os.environ["NCCL_HOSTID"] = f"blockpipe-bench-rank-{rank}"
         os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
         os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
-    n = max(args.gpus, world)
-    if args.workload == "wan13-301":
-        w = WORKLOADS["multi"]
-    elif args.workload in ("wan13-1025", "tiny"):
-        w = WORKLOADS[args.workload]
-    else:
-        w = WORKLOADS[1] if n == 1 else WORKLOADS["multi"]
 
     import paper_2505_21070_b200 as bp
 
@@ -299,36 +441,7 @@ def main():
                             transport=args.transport if n > 1 else "loopback")
     sched = bp.Schedule(cfg)
     fl_video, n_prefix = video_flops(w, sched)
-    config = {"workload": w["name"], "layers": w["layers"], "hidden": w["hidden"], "heads": w["heads"],
-              "ffn": w["ffn"], "latent_grid": [w["height"], w["width"], w["channels"]], "context_len": w["context_len"],
-              "num_b": w["num_b"], "num_c": w["num_c"], "steps": w["steps"], "blocks": w["blocks"],
-              "frames": w["frames"], "passes": sched.npasses, "prefix_passes": n_prefix,
-              "parallelism": f"layer-pipeline x{n}" + (f" ({args.transport})" if n > 1 else ""), "l2": "inputs larger than L2 (18720x1536 activations per pass)"}
-
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        vals = []
-        cb = None
-        for _ in range(args.warmup):
-            pass  # the reference has no warm-up state; each step is a fresh bounded sample
-        t_all = time.perf_counter()
-        for _ in range(args.steps):
-            cb = cpu_baseline(w, sched)
-            if cb is None:
-                print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libbp_ref.so not built"}))
-                return
-            vals.append(cb["value"])
-        value = statistics.mean(vals)
-        print(json.dumps({
-            "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": n,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000 * (time.perf_counter() - t_all) / max(1, args.steps),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference random-init weights, coordinated noise pool)", "config": config,
-            "cpu_baseline": cb, "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
-                                         "d2h_bytes_per_step": 0}}))
-        return
+    config = workload_config(w, n, sched, args)
 
     dist = None
     ids = None
@@ -347,14 +460,7 @@ def main():
         if args.transport == "nccl":
             obj = [None]
             if rank == 0:
-                from paper_2505_21070_b200._lib import lib
-                import ctypes
-                buf = bytearray()
-                for _ in range(n):
-                    b = (ctypes.c_uint8 * 128)()
-                    assert lib.bp_nccl_unique_id(b) == 0
-                    buf += bytes(b)
-                obj = [bytes(buf)]
+                obj = [bp.nccl_unique_ids(n)]
             dist.broadcast_object_list(obj, src=0)
             ids = obj[0]
 
@@ -366,15 +472,26 @@ def main():
         if dist is not None:
             dist.barrier()
 
-    n_warm = max(3, args.warmup) if args.workload == "auto" else max(1, args.warmup)
-    for _ in range(n_warm):
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        import torch
+        t = torch.tensor([float(v)], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up videos (untimed); the last one carries CUDA events around every
+    # class of launches (self-attention, cross-attention, GEMMs, LayerNorm) for
+    # the roofline and the breakdown -- the timed videos carry none
+    n_warm = max(3, args.warmup)
+    for i in range(n_warm):
+        pipe.set_profiling(i == n_warm - 1)
         pipe.run_device()
+        if i == n_warm - 1:
+            prof = pipe.stats()
+    pipe.set_profiling(False)
     barrier()
-    lib_launch = []
-    gpu_ms = []
-    prof = {"attn_ms": 0.0, "gemm_ms": 0.0, "cross_ms": 0.0, "ln_ms": 0.0, "attn_launches": 0, "gemm_launches": 0,
-            "ln_launches": 0}
-    from paper_2505_21070_b200._lib import lib
+    lib_launch, gpu_ms = [], []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             pipe.run_device()
@@ -382,35 +499,14 @@ def main():
             gpu_ms.append(st["gpu_ms"])
             lib_launch.append(st["kernel_launches"])
     barrier()
-    # one more video, untimed, with CUDA events around every class of launches
-    # (self-attention, cross-attention, GEMMs, LayerNorm) for the rooflines and
-    # the breakdown; the timed steps above carry no profiling events
-    lib.bp_pipeline_set_profiling(pipe._h, 1)
-    pipe.run_device()
-    st = pipe.stats()
-    for k in prof:
-        prof[k] = st[k]
-    prof_video_s = st["gpu_ms"] / 1e3
-    lib.bp_pipeline_set_profiling(pipe._h, 0)
-    barrier()
-    ms = statistics.mean(gpu_ms)
-    if dist is not None:
-        import torch
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(statistics.mean(gpu_ms))
     stats = pipe.stats()
-    link_bytes = float(stats["boundary_bytes"])  # this rank's stage-boundary bytes of the last video
-    if dist is not None:
-        import torch
-        t = torch.tensor([link_bytes], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # busiest stage-boundary link
-        link_bytes = float(t.item())
+    link_bytes = max_over_ranks(stats["boundary_bytes"])  # busiest stage-boundary link of one video
 
     # e2e: the public API with host buffers. Rank 0 hands the engine the
     # reference's noise pool from pinned host memory (bp_pipeline_set_pool;
-    # uploaded host->device inside every run) and receives every emitted
-    # block's latents back in host memory; wall clock per step, max over ranks.
+    # uploaded host->device inside the run) and receives every emitted block's
+    # latents back in host memory; wall clock of the video, max over ranks.
     pool = None
     if rank == 0:
         m = w["num_b"] + w["num_c"] // 2
@@ -418,28 +514,20 @@ def main():
         pool[...] = bp.build_pool(w["num_b"], w["num_c"], (w["height"], w["width"], w["channels"]),
                                   bp.derive_seed(cfg.seed_noise, [0]), device=local)
         pipe.set_pool(pool)
-    e2e_vals = []
-    h2d = d2h = 0
-    for _ in range(max(1, min(args.steps, 2))):
-        barrier()
-        t0 = time.perf_counter()
-        blocks = pipe.run()
-        barrier()
-        dt = time.perf_counter() - t0
-        if dist is not None:
-            import torch
-            tt = torch.tensor([dt], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dt = float(tt.item())
-        e2e_vals.append(w["frames"] / dt)
-        est = pipe.stats()
-        h2d, d2h = est["h2d_bytes"], est["d2h_bytes"]
+    barrier()
+    t0 = time.perf_counter()
+    pipe.run()
+    barrier()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    est = pipe.stats()
+    h2d, d2h = est["h2d_bytes"], est["d2h_bytes"]
     if pool is not None:
         pipe.set_pool(None)
 
     if rank != 0:
         return
     peaks, peak_kind = load_peaks()
+    prof_video_s = prof["gpu_ms"] / 1e3
     attn_fl = self_attn_flops(w, sched)
     attn_s = prof["attn_ms"] / 1e3
     achieved = attn_fl / attn_s / 1e12 if attn_s > 0 else None
@@ -450,14 +538,19 @@ def main():
             traffic = json.load(f).get("dram_bytes_per_launch")
     except Exception:
         pass
-    cpu = None if args.no_cpu_baseline else cpu_baseline(w, sched)
+    cpu = None
+    if n == 1 and not args.no_cpu_baseline:
+        from oracle import ref
+        if ref.available():
+            cpu = RefSample(w, sched).measure()
+            cpu["measured_legs"] = reference_legs(include_mid=False)
+            cpu["host"] = host_info()
     s_video = ms / 1e3
     tokens_per_pass = (w["num_b"] + w["num_c"] // 2) * w["height"] * w["width"]
     out = {
         "metric": METRIC, "value": w["frames"] / s_video, "unit": "frames/s", "n_gpus": n, "steps": args.steps,
-        "warmup": n_warm, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if n > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (random-init Wan2.1-1.3B-shape weights, reference coordinated noise pool)",
+        "warmup": n_warm, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (random-init Wan2.1-1.3B-shape weights, reference coordinated noise pool)",
         "config": config,
         "s_per_video": s_video, "latent_frames_per_s": sum(b["frames"] for b in sched.blocks) / s_video,
         "peak_hbm_gb": stats["peak_bytes"] / 1e9,
@@ -466,23 +559,16 @@ def main():
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_kind": f"{peak_kind} sustained (kernel timed inside a long step)",
-                     "timing": "CUDA events around every launch of the class, in one extra video right after the timed steps (events inside the timed steps would perturb launch overlap)",
+                     "frac_of_burst": (achieved / peaks["bf16_tflops"]) if achieved else None,
+                     "timing": "CUDA events around every launch of the class in the last warm-up video (events "
+                               "inside the timed videos would perturb launch overlap)",
                      "share_of_step": attn_s / prof_video_s,
                      "gemm_tflops": None if prof["gemm_ms"] <= 0 else
-                     (fl_video - self_attn_flops(w, sched)) / (prof["gemm_ms"] / 1e3) / 1e12,
+                     (fl_video - attn_fl) / (prof["gemm_ms"] / 1e3) / 1e12,
                      "whole_step_frac": fl_video / s_video / 1e12 / peak},
-        # north_star: the elementwise path against HBM bandwidth -- the
-        # LayerNorm kernel (fp32 residual row in, bf16 operand row out: 6 B per
-        # element algorithmic), device time from CUDA events in the timed steps
-        "elementwise_roofline": None if prof["ln_ms"] <= 0 else {
-            "bound": "hbm", "kernel": "k_ln_bf16_reg (LayerNorm + affine, fp32 -> bf16)",
-            "achieved": prof["ln_launches"] * tokens_per_pass * w["hidden"] * 6 / (prof["ln_ms"] / 1e3) / 1e9,
-            "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": prof["ln_launches"] * tokens_per_pass * w["hidden"] * 6 / (prof["ln_ms"] / 1e3) / 1e9 / peaks["hbm_gbs"],
-            "bytes_per_launch": tokens_per_pass * w["hidden"] * 6, "share_of_step": prof["ln_ms"] / 1e3 / prof_video_s,
-            "note": "event windows around each launch include the launch gap; ncu kernel time is lower "
-                    "(profiles/r01b_summary.md)"},
-        # where the device time of a step goes (CUDA events around each class of
+        # north_star: the elementwise path against HBM bandwidth, from kernel time
+        "elementwise_roofline": ln_kernel_roofline(local, tokens_per_pass, w["hidden"], peaks),
+        # where the device time of a video goes (CUDA events around each class of
         # launches on the compute stream; "rest" = embedding, capture copies,
         # head, Euler steps, gathers and the gaps between launches)
         "step_breakdown_s": {
@@ -491,9 +577,9 @@ def main():
             "gemm": prof["gemm_ms"] / 1e3, "layernorm": prof["ln_ms"] / 1e3,
             "rest": prof_video_s - (prof["attn_ms"] + prof["cross_ms"] + prof["gemm_ms"] + prof["ln_ms"]) / 1e3},
         "cpu_baseline": cpu,
-        "e2e": {"value": statistics.mean(e2e_vals), "unit": "frames/s",
+        "e2e": {"value": w["frames"] / e2e_s, "unit": "frames/s", "s_per_video": e2e_s,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "note": "wall clock per video through bp_pipeline_run: the noise pool uploaded from pinned host "
+                "note": "wall clock of one video through bp_pipeline_run: the noise pool uploaded from pinned host "
                         "memory (bp_pipeline_set_pool) and every emitted block copied back to host"},
         # north_star: the slower of compute at peak and stage-boundary bytes over
         # NVLink (900 GB/s per direction) bounds the whole pipeline

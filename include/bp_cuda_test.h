@@ -27,12 +27,20 @@ BP_API bp_status bp_selftest_attn(int32_t device, int64_t rows, int32_t heads, i
                            const uint16_t* k0, const uint16_t* v0, int64_t n0, const uint16_t* k1,
                            const uint16_t* v1, int64_t n1, float scale, uint16_t* out);
 
+/* The same through the stage's cross-attention launcher (one key segment). */
+BP_API bp_status bp_selftest_attn_cross(int32_t device, int64_t rows, int32_t heads, int32_t dh, const uint16_t* q,
+                                 const uint16_t* k1, const uint16_t* v1, int64_t n1, float scale, uint16_t* out);
+
 /* Device time (ms, CUDA events on the launching stream) of `iters` back-to-back
  * launches of the current GEMM implementation on device-resident random data. */
 BP_API bp_status bp_bench_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int32_t epi, int32_t iters,
                         double* ms);
 BP_API bp_status bp_bench_attn(int32_t device, int64_t rows, int32_t heads, int32_t dh, int64_t n0, int64_t n1,
                         int32_t iters, double* ms);
+
+/* Device time (ms per launch) of `iters` back-to-back LayerNorm launches
+ * (fp32 [rows, n] -> bf16, the bf16 path's k_ln_bf16_reg). */
+BP_API bp_status bp_bench_ln(int32_t device, int64_t rows, int32_t n, int32_t iters, double* ms);
 
 #ifdef __cplusplus
 }

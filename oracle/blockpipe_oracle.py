@@ -190,6 +190,55 @@ def forward_chunk(ch, payload, levels, frame_ids, context, mode="off", cache=Non
     return out, captured, rec
 
 
+def sinusoid_rows(pos: np.ndarray, hidden: int) -> np.ndarray:
+    """position_embedding (model.cpp:155-163) for many positions at once
+    (numpy sin/cos: within an ulp or two of glibc's, enough for the
+    fp32 / bf16 tolerances this restatement checks at Wan shapes)."""
+    half = (hidden + 1) // 2
+    f = np.array([math.pow(10000.0, -2.0 * i / hidden) for i in range(half)])
+    ang = np.asarray(pos, dtype=np.float64)[:, None] * f[None, :]
+    e = np.zeros((ang.shape[0], hidden))
+    e[:, 0::2] = np.sin(ang)
+    e[:, 1::2] = np.cos(ang)[:, :hidden // 2]
+    return e
+
+
+def forward_chunk_rows(ch, payload, levels, frame_ids, context, out_rows, prefix=None, capture=()):
+    """forward_chunk (model.cpp:227-336) of a ONE-layer chunk, restated for
+    the output rows `out_rows` only, so it runs at Wan shapes on a host.
+    Every op except attention is per token, and attention needs the K/V of
+    every row (prefix first, model.cpp:302-318) but the queries of the
+    requested rows only. Returns (out[out_rows], (K, V) at the capture rows)."""
+    cfg = ch["cfg"]
+    assert len(ch["layers"]) == 1
+    tpf, h = cfg["height"] * cfg["width"], cfg["hidden"]
+    nf = len(levels)
+    if ch["begin"] == 0:  # model.cpp:245-260
+        x = payload @ ch["w_in"]
+        t = np.arange(nf * tpf)
+        f = t // tpf
+        pos = np.asarray(frame_ids, dtype=np.int64)[f] * tpf + (t - f * tpf)
+        te = sinusoid_rows(np.asarray(levels, dtype=np.int64) + 1000000, h)
+        x += sinusoid_rows(pos, h) + te[f]
+    else:
+        x = payload.copy()
+    w = ch["layers"][0]
+    ln1 = ln_affine(x, w["ln1_g"], w["ln1_b"])
+    k, v = ln1 @ w["wk"], ln1 @ w["wv"]
+    cap_rows = [fr * tpf + tt for fr in capture for tt in range(tpf)]
+    captured = (k[cap_rows].copy(), v[cap_rows].copy()) if cap_rows else None
+    if prefix is not None:
+        k, v = np.concatenate([prefix[0], k]), np.concatenate([prefix[1], v])
+    R = np.asarray(out_rows)
+    xr = x[R] + attention(ln1[R] @ w["wq"], k, v, cfg["heads"]) @ w["wo"]
+    ln2 = ln_affine(xr, w["ln2_g"], w["ln2_b"])
+    xr = xr + attention(ln2 @ w["cq"], context @ w["ck"], context @ w["cv"], cfg["heads"]) @ w["co"]
+    ln3 = ln_affine(xr, w["ln3_g"], w["ln3_b"])
+    xr = xr + gelu(ln3 @ w["w1"]) @ w["w2"]
+    out = xr @ ch["w_out"] if ch["end"] == cfg["layers"] else xr
+    return out, captured
+
+
 # ---- block_queue.cpp / noise.cpp / engine.cpp (serial, round-atomic) ----------------------------
 def run_pipeline(cfg: Dict, record_trace=False) -> Dict:
     """serial_oracle (engine.cpp:499-503): the run_pipeline round loop

@@ -5,11 +5,11 @@ from .errors import (BlockpipeError, CacheError, ConfigError, CudaError, Dimensi
                      NcclError, PartitionError, QueueError, SchedulerError, SchedulingError)
 from .config import PipelineConfig
 from .api import (Pipeline, Schedule, Stage, build_pool, coordinated_noise_ids, derive_seed,
-                  measure_bubbles, normals, pinned_empty, run_pipeline, scheduler_step, serial_oracle)
+                  measure_bubbles, nccl_unique_ids, normals, pinned_empty, run_pipeline, scheduler_step, serial_oracle)
 
 __all__ = [
     "BlockpipeError", "CacheError", "ConfigError", "CudaError", "DimensionError", "IoError", "NcclError",
     "PartitionError", "QueueError", "SchedulerError", "SchedulingError", "PipelineConfig", "Pipeline",
     "Schedule", "Stage", "build_pool", "coordinated_noise_ids", "derive_seed", "measure_bubbles",
-    "normals", "pinned_empty", "run_pipeline", "scheduler_step", "serial_oracle",
+    "nccl_unique_ids", "normals", "pinned_empty", "run_pipeline", "scheduler_step", "serial_oracle",
 ]

@@ -133,17 +133,6 @@ _SIGS = {
 
 EXPORTED = tuple(_SIGS)
 
-# kernel-level self-test hooks (include/bp_cuda_test.h)
-_TEST_SIGS = {
-    "bp_set_kernel_impl": (i32, [i32, i32]),
-    "bp_selftest_gemm": (i32, [i32, i32, i32, i32, i32, C.c_void_p, i64, C.c_void_p, C.c_void_p, i64]),
-    "bp_selftest_attn": (i32, [i32, i64, i32, i32, C.c_void_p, C.c_void_p, C.c_void_p, i64, C.c_void_p,
-                               C.c_void_p, i64, C.c_float, C.c_void_p]),
-    "bp_bench_gemm": (i32, [i32, i32, i32, i32, i32, i32, P(f64)]),
-    "bp_bench_attn": (i32, [i32, i64, i32, i32, i64, i64, i32, P(f64)]),
-}
-_SIGS.update(_TEST_SIGS)
-
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(lib, _name)
     _fn.restype = _res

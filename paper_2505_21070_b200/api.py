@@ -223,11 +223,18 @@ def measure_bubbles(events: np.ndarray, devices: int) -> Dict[str, Any]:
           "warmup_idle": 0, "steady_idle": 0, "cooldown_idle": 0, "ratio": 0.0}
     if len(events) == 0:
         return st
-    per = [sorted((int(e[0]), int(e[4])) for e in events if int(e[1]) == d) for d in range(devices)]
+    if devices < 1:
+        raise errors.SchedulingError("malformed event log: no devices")
+    if any(int(e[1]) < 0 or int(e[1]) >= devices for e in events):
+        raise errors.SchedulingError("malformed event log: device out of range")
+    # per-device events in log order, as engine.cpp:510-530 walks them
+    per = [[(int(e[0]), int(e[4])) for e in events if int(e[1]) == d] for d in range(devices)]
     first, last = int(events[:, 0].min()), int(events[:, 0].max())
     busy = len(per[0])
     if any(len(v) != busy for v in per):
         raise errors.SchedulingError("malformed event log: devices saw different pass counts")
+    if any(v[i][0] <= v[i - 1][0] for v in per for i in range(1, len(v))):
+        raise errors.SchedulingError("malformed event log: duplicate slot on one device")
     st.update(first_slot=first, last_slot=last, busy_per_device=busy,
               idle_per_device=(last - first + 1) - busy)
     keys = ("warmup_idle", "steady_idle", "cooldown_idle")
@@ -276,6 +283,17 @@ def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
     buf = (C.c_uint8 * nbytes).from_address(mem.ptr.value)
     buf._bp_pinned = mem
     return np.frombuffer(buf, dtype=dt, count=n).reshape(shape)
+
+
+def nccl_unique_ids(world: int) -> bytes:
+    """`world` NCCL unique ids (128 bytes each), one per pipeline channel, made
+    on the rank that broadcasts them to the others (ncclGetUniqueId)."""
+    buf = bytearray()
+    for _ in range(world):
+        b = (C.c_uint8 * 128)()
+        check(lib.bp_nccl_unique_id(b))
+        buf += bytes(b)
+    return bytes(buf)
 
 
 # ---- engine.hpp: the pipeline ---------------------------------------------------------------
@@ -354,6 +372,11 @@ class Pipeline:
             raise TypeError("pool must be a C-contiguous float64 array")
         self._pool = pool  # borrowed by the engine for every later run
         check(lib.bp_pipeline_set_pool(self._h, _ptr(pool, f64), pool.size))
+
+    def set_profiling(self, on: bool) -> None:
+        """CUDA events around every class of launches in later runs (the
+        per-class device times appear in stats()); off for timed runs."""
+        check(lib.bp_pipeline_set_profiling(self._h, int(bool(on))))
 
     def run_device(self) -> None:
         """One whole generation with the emitted latents left in HBM (no

@@ -1225,19 +1225,15 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     launch_attn_simt(a, rows, st);
     return;
   }
-  static bool configured = false;
-  if (!configured) {
-    BP_CUDA(cudaFuncSetAttribute(k_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    BP_CUDA(cudaFuncSetAttribute(k_attn_pp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
-    BP_CUDA(cudaFuncSetAttribute(k_attn_pp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
-    BP_CUDA(cudaFuncSetAttribute(k_attn_pp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM_BYTES));
-    BP_CUDA(cudaFuncSetAttribute(k_attn_fa, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_SMEM_BYTES));
-    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
-    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
-    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
-    BP_CUDA(cudaFuncSetAttribute(k_attn_pp2<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM_BYTES));
-    configured = true;
-  }
+  set_smem_attr(k_attn_tc, SMEM_BYTES);
+  set_smem_attr(k_attn_pp<0>, PP_SMEM_BYTES);
+  set_smem_attr(k_attn_pp<1>, PP_SMEM_BYTES);
+  set_smem_attr(k_attn_pp<2>, PP_SMEM_BYTES);
+  set_smem_attr(k_attn_fa, FA_SMEM_BYTES);
+  set_smem_attr(k_attn_pp2<0>, P2_SMEM_BYTES);
+  set_smem_attr(k_attn_pp2<1>, P2_SMEM_BYTES);
+  set_smem_attr(k_attn_pp2<2>, P2_SMEM_BYTES);
+  set_smem_attr(k_attn_pp2<1, true>, P2_SMEM_BYTES);
   AttnMaps maps;
   maps.q = map_for(a.q, rows, H, a.ldq);
   maps.k1 = map_for(a.k1, a.n1, H, a.ldk1);

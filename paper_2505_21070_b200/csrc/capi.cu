@@ -3,7 +3,10 @@
 
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "device.cuh"
@@ -29,6 +32,20 @@ void require_device(int device) {
 }  // namespace
 
 void set_last_error(const std::string& m) { t_last_error = m; }
+
+void set_smem_attr_impl(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  BP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (!done.insert({fn, dev}).second) return;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) {
+    done.erase({fn, dev});
+    fail(BP_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  }
+}
 
 }  // namespace bp
 
@@ -121,15 +138,19 @@ bp_status bp_forward_chunk(bp_stage* h, const bp_chunk_in* in, bp_chunk_out* out
     if (!h || !in || !out) bp::fail(BP_ERR_CONFIG, "null argument");
     bp::Stage& s = *h->s;
     BP_CUDA(cudaSetDevice(h->device));
-    const int tpf = 0;  // unused; tokens come from the stage's geometry below
-    (void)tpf;
     const int64_t frames = in->nframes;
-    // forward_chunk's shape checks (model.cpp:230-266)
-    const int64_t tokens = frames * static_cast<int64_t>(s.hidden() > 0 ? 1 : 1);
-    (void)tokens;
+    // forward_chunk's shape checks (model.cpp:230-266), before anything is uploaded
+    if (frames < 0 || in->rows < 0 || in->ncapture < 0) bp::fail(BP_ERR_DIMENSION, "negative size");
+    if (in->rows != frames * s.tokens_per_frame())
+      bp::fail(BP_ERR_DIMENSION, "payload rows do not match frames * tokens_per_frame");
+    if (frames > 0 && (!in->frame_levels || !in->frame_ids || !in->payload)) bp::fail(BP_ERR_CONFIG, "null argument");
+    if (in->ncapture > 0 && !in->capture_frames) bp::fail(BP_ERR_CONFIG, "null argument");
+    for (int32_t c = 0; c < in->ncapture; ++c)
+      if (in->capture_frames[c] < 0 || in->capture_frames[c] >= frames)
+        bp::fail(BP_ERR_DIMENSION, "capture frame out of range");
+    if (in->mode < BP_CACHE_DISABLED || in->mode > BP_CACHE_RECOMPUTE) bp::fail(BP_ERR_CONFIG, "unknown cache mode");
+    if (in->use_prev < 0 || in->use_prev > 4) bp::fail(BP_ERR_CONFIG, "unknown use_prev");
     bp::StageInput si;
-    const int64_t tpf64 = in->nframes > 0 ? in->rows / std::max<int64_t>(1, in->nframes) : 0;
-    (void)tpf64;
     // tokens = frames * tokens_per_frame, checked against the payload rows
     si.nframes = in->nframes;
     si.tokens = in->rows;

@@ -32,6 +32,12 @@ inline void count_launch() {
   BP_CUDA(cudaPeekAtLastError());
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device);
+// the attribute is per device context, and the bookkeeping is thread-safe.
+void set_smem_attr_impl(const void* fn, int bytes);
+template <typename F>
+inline void set_smem_attr(F* fn, int bytes) { set_smem_attr_impl(reinterpret_cast<const void*>(fn), bytes); }
+
 // Device allocation tracking for the peak-HBM report.
 extern std::atomic<int64_t> g_dev_bytes, g_dev_peak;
 

@@ -486,12 +486,7 @@ std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 template <int EPI, bool kCg2 = false>
 void launch_pair(const CUtensorMap& ma, const CUtensorMap& mbh, int M, int N, int K, void* C, int64_t ldc,
                  const CUtensorMap& mc, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    BP_CUDA(cudaFuncSetAttribute(k_gemm_pair<EPI, kCg2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 PairLayout<kCg2>::kSmem));
-    configured = true;
-  }
+  set_smem_attr(k_gemm_pair<EPI, kCg2>, PairLayout<kCg2>::kSmem);
   const int pairs = (((M + BM - 1) / BM + 1) / 2) * ((N + BN - 1) / BN);
   const int clusters = pairs < kNumSms / 2 ? pairs : kNumSms / 2;
   launch_pdl(k_gemm_pair<EPI, kCg2>, dim3(2 * clusters), dim3(kThreads), PairLayout<kCg2>::kSmem, st, ma, mbh, M, N, K,
@@ -501,11 +496,7 @@ void launch_pair(const CUtensorMap& ma, const CUtensorMap& mbh, int M, int N, in
 template <int EPI>
 void launch_epi(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, void* C, int64_t ldc,
                 cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    BP_CUDA(cudaFuncSetAttribute(k_gemm_tc<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    configured = true;
-  }
+  set_smem_attr(k_gemm_tc<EPI>, SMEM_BYTES);
   const int total = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = total < kNumSms ? total : kNumSms;
   k_gemm_tc<EPI><<<grid, kThreads, SMEM_BYTES, st>>>(ma, mb, M, N, K, C, ldc);

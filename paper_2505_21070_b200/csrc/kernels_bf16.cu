@@ -174,85 +174,12 @@ void launch_embed_table(const double* freq, int h, int tpf, double* ttab, cudaSt
 
 
 // ---- fp32 side GEMMs of the bf16 path (entry embedding, head) ------------------------
-// C[M,N] (+)= A[M,K] B[K,N], all fp32 row-major, K % 32 == 0, N % 64 == 0, rows
-// 16-byte aligned. 128 x 64 tile per CTA, 8 x 4 outputs per thread as packed
-// FFMA2 pairs, k ascending. These sit outside the cached == recompute
-// invariant (they do not produce K/V), so no unfused reference order is kept.
-template <bool kResidual>
-__global__ void __launch_bounds__(256) k_gemm_f32_tile(const float* __restrict__ A, int64_t lda,
-                                                       const float* __restrict__ B, int64_t ldb, int M, int N, int K,
-                                                       float* __restrict__ Cm, int64_t ldc) {
-  constexpr int BM = 128, BN = 64, BK = 32;
-  __shared__ __align__(16) float As[BK][BM + 4];  // transposed A tile
-  __shared__ __align__(16) float Bs[BK][BN];
-  const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;  // cols tx*4.., rows ty*8..
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  float2 acc[8][2];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
-  for (int k0 = 0; k0 < K; k0 += BK) {
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {  // A: 128 rows x 8 float4
-      const int e = tid + v * 256, r = e >> 3, c4 = e & 7;
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (m0 + r < M) a = *reinterpret_cast<const float4*>(A + static_cast<int64_t>(m0 + r) * lda + k0 + c4 * 4);
-      As[c4 * 4 + 0][r] = a.x;
-      As[c4 * 4 + 1][r] = a.y;
-      As[c4 * 4 + 2][r] = a.z;
-      As[c4 * 4 + 3][r] = a.w;
-    }
-#pragma unroll
-    for (int v = 0; v < 2; ++v) {  // B: 32 rows x 16 float4
-      const int e = tid + v * 256, r = e >> 4, c4 = e & 15;
-      *reinterpret_cast<float4*>(&Bs[r][c4 * 4]) =
-          *reinterpret_cast<const float4*>(B + static_cast<int64_t>(k0 + r) * ldb + n0 + c4 * 4);
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int kk = 0; kk < BK; ++kk) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][ty * 8 + 4]);
-      const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
-      const float2 b01 = make_float2(b.x, b.y), b23 = make_float2(b.z, b.w);
-      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float2 aa = make_float2(av[i], av[i]);
-        acc[i][0] = __ffma2_rn(aa, b01, acc[i][0]);
-        acc[i][1] = __ffma2_rn(aa, b23, acc[i][1]);
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int r = m0 + ty * 8 + i;
-    if (r >= M) continue;
-    float4* dst = reinterpret_cast<float4*>(Cm + static_cast<int64_t>(r) * ldc + n0 + tx * 4);
-    float4 o = make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
-    if (kResidual) {
-      const float4 c = *dst;
-      o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
-    }
-    *dst = o;
-  }
-}
-
+// The fp32 tile GEMM lives with the SIMT kernels (kernels_simt.cu); these GEMMs
+// sit outside the cached == recompute invariant (they do not produce K/V).
 void launch_gemm_f32_tile(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K, float* C,
                           int64_t ldc, bool residual, cudaStream_t st) {
-  const bool fits = K % 32 == 0 && N % 64 == 0 && lda % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 &&
-                    (reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) % 16 == 0;
-  if (!fits) {  // odd shapes: the generic SIMT GEMM
-    launch_matmul<float>(A, lda, B, ldb, M, N, K, C, ldc, residual ? kEpiResidual : kEpiNone, residual ? C : nullptr,
-                         residual ? ldc : 0, st);
-    return;
-  }
-  if (M <= 0) return;
-  dim3 grid(static_cast<unsigned>(N / 64), static_cast<unsigned>((M + 127) / 128));
-  if (residual) k_gemm_f32_tile<true><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, C, ldc);
-  else k_gemm_f32_tile<false><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, C, ldc);
-  count_launch();
+  launch_matmul<float>(A, lda, B, ldb, M, N, K, C, ldc, residual ? kEpiResidual : kEpiNone, residual ? C : nullptr,
+                       residual ? ldc : 0, st);
 }
 
 void launch_embed_fast(const double* lat, const float* w_in32, const double* freq, const double* ttab,

@@ -225,10 +225,97 @@ __global__ void __launch_bounds__(256) k_matmul(const T* __restrict__ A, int64_t
   }
 }
 
+// fp32 tile GEMM (the fp32 verification path at Wan shapes, and the bf16
+// path's fp32 side GEMMs): 128 x 64 tile per CTA, 8 x 4 outputs per thread as
+// packed FFMA2 pairs, k ascending from zero with one FMA per k -- the same
+// per-element sequence as k_matmul<float>, so results do not depend on which
+// of the two kernels ran (nor on an output row's position: cached == recompute).
+// Needs K % 32 == 0, N % 64 == 0 and 16-byte aligned rows.
+template <int EPI>
+__global__ void __launch_bounds__(256) k_matmul_f32_tile(const float* __restrict__ A, int64_t lda,
+                                                         const float* __restrict__ B, int64_t ldb, int M, int N,
+                                                         int K, float* Cm, int64_t ldc, const float* R, int64_t ldr) {
+  constexpr int BM = 128, BN = 64, BK = 32;
+  __shared__ __align__(16) float As[BK][BM + 4];  // transposed A tile
+  __shared__ __align__(16) float Bs[BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;  // cols tx*4.., rows ty*8..
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  float2 acc[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
+  for (int k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {  // A: 128 rows x 8 float4
+      const int e = tid + v * 256, r = e >> 3, c4 = e & 7;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (m0 + r < M) a = *reinterpret_cast<const float4*>(A + static_cast<int64_t>(m0 + r) * lda + k0 + c4 * 4);
+      As[c4 * 4 + 0][r] = a.x;
+      As[c4 * 4 + 1][r] = a.y;
+      As[c4 * 4 + 2][r] = a.z;
+      As[c4 * 4 + 3][r] = a.w;
+    }
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {  // B: 32 rows x 16 float4
+      const int e = tid + v * 256, r = e >> 4, c4 = e & 15;
+      *reinterpret_cast<float4*>(&Bs[r][c4 * 4]) =
+          *reinterpret_cast<const float4*>(B + static_cast<int64_t>(k0 + r) * ldb + n0 + c4 * 4);
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < BK; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][ty * 8 + 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float2 b01 = make_float2(b.x, b.y), b23 = make_float2(b.z, b.w);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float2 aa = make_float2(av[i], av[i]);
+        acc[i][0] = __ffma2_rn(aa, b01, acc[i][0]);
+        acc[i][1] = __ffma2_rn(aa, b23, acc[i][1]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = m0 + ty * 8 + i;
+    if (r >= M) continue;
+    float o[4] = {acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y};
+    if (EPI == kEpiGelu) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        o[j] = Ar<float>::mul(Ar<float>::mul(0.5f, o[j]),
+                              Ar<float>::add(1.f, erff(Ar<float>::div(o[j], 1.4142135623730951f))));
+    } else if (EPI == kEpiResidual) {
+      const float4 c = *reinterpret_cast<const float4*>(R + static_cast<int64_t>(r) * ldr + n0 + tx * 4);
+      o[0] = c.x + o[0]; o[1] = c.y + o[1]; o[2] = c.z + o[2]; o[3] = c.w + o[3];
+    }
+    *reinterpret_cast<float4*>(Cm + static_cast<int64_t>(r) * ldc + n0 + tx * 4) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 template <typename T>
 void launch_matmul(const T* A, int64_t lda, const T* B, int64_t ldb, int M, int N, int K, T* C,
                    int64_t ldc, int epi, const T* R, int64_t ldr, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
+  if constexpr (sizeof(T) == 4) {
+    const bool fits = K % 32 == 0 && N % 64 == 0 && K > 0 && lda % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 &&
+                      (epi != kEpiResidual || ldr % 4 == 0) &&
+                      ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+                        reinterpret_cast<uintptr_t>(C) | reinterpret_cast<uintptr_t>(R)) & 15) == 0;
+    if (fits) {
+      dim3 grid(static_cast<unsigned>(N / 64), static_cast<unsigned>((M + 127) / 128));
+      switch (epi) {
+        case kEpiNone: k_matmul_f32_tile<kEpiNone><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, C, ldc, R, ldr); break;
+        case kEpiGelu: k_matmul_f32_tile<kEpiGelu><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, C, ldc, R, ldr); break;
+        default: k_matmul_f32_tile<kEpiResidual><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, C, ldc, R, ldr); break;
+      }
+      count_launch();
+      return;
+    }
+  }
   dim3 grid((N + 63) / 64, (M + 63) / 64);
   switch (epi) {
     case kEpiNone: k_matmul<T, kEpiNone><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, C, ldc, R, ldr); break;
@@ -297,15 +384,168 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs<T> a) {
   if (threadIdx.x + 128 < a.dh) orow[threadIdx.x + 128] = acc1;
 }
 
+// fp32 verification attention at Wan shapes: flash-style tiles of 64 query
+// rows x 64 keys for one head per CTA, online softmax (running max / sum,
+// expf), the two KV segments walked in order. Scores are (q.k) * scale as in
+// model.cpp:55-58; the normalisation divides once at the end. S = Q K^T and
+// O += P V run from shared memory as 4x4 / 4x(DH/16) register tiles.
+template <int DH>
+__global__ void __launch_bounds__(256, 2) k_attn_f32_flash(AttnArgs<float> a, int64_t rows) {
+  constexpr int BQ = 64, BK = 64, CPT = DH / 16, D4 = DH / 4;
+  extern __shared__ __align__(16) float fsm[];
+  float* Qt = fsm;             // [DH][BQ]
+  float* Kt = Qt + DH * BQ;    // [DH][BK]
+  float* Vs = Kt + DH * BK;    // [BK][DH]
+  float* Pt = Vs + BK * DH;    // [BK][BQ]
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t q0 = static_cast<int64_t>(blockIdx.x) * BQ;
+  const int c0 = blockIdx.y * DH;
+  for (int e = tid; e < BQ * D4; e += 256) {
+    const int r = e % BQ, d4 = e / BQ;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (q0 + r < rows) v = *reinterpret_cast<const float4*>(a.q + (q0 + r) * a.ldq + c0 + d4 * 4);
+    Qt[(d4 * 4 + 0) * BQ + r] = v.x;
+    Qt[(d4 * 4 + 1) * BQ + r] = v.y;
+    Qt[(d4 * 4 + 2) * BQ + r] = v.z;
+    Qt[(d4 * 4 + 3) * BQ + r] = v.w;
+  }
+  float m[4], l[4], o[4][CPT];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    m[i] = -INFINITY;
+    l[i] = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) o[i][c] = 0.f;
+  }
+  const int64_t nkv = a.n0 + a.n1;
+  for (int64_t k0 = 0; k0 < nkv; k0 += BK) {
+    __syncthreads();  // the previous tile's P.V is done with Vs / Pt
+    for (int e = tid; e < BK * D4; e += 256) {  // K transposed: key index fastest (conflict-free stores)
+      const int r = e % BK, d4 = e / BK;
+      const int64_t j = k0 + r;
+      float4 kv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j < nkv) {
+        const float* kp = j < a.n0 ? a.k0 + j * a.ldk0 : a.k1 + (j - a.n0) * a.ldk1;
+        kv = *reinterpret_cast<const float4*>(kp + c0 + d4 * 4);
+      }
+      Kt[(d4 * 4 + 0) * BK + r] = kv.x;
+      Kt[(d4 * 4 + 1) * BK + r] = kv.y;
+      Kt[(d4 * 4 + 2) * BK + r] = kv.z;
+      Kt[(d4 * 4 + 3) * BK + r] = kv.w;
+    }
+    for (int e = tid; e < BK * D4; e += 256) {  // V row-major: column fastest (coalesced)
+      const int r = e / D4, d4 = e % D4;
+      const int64_t j = k0 + r;
+      float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j < nkv) {
+        const float* vp = j < a.n0 ? a.v0 + j * a.ldv0 : a.v1 + (j - a.n0) * a.ldv1;
+        vv = *reinterpret_cast<const float4*>(vp + c0 + d4 * 4);
+      }
+      *reinterpret_cast<float4*>(Vs + r * DH + d4 * 4) = vv;
+    }
+    __syncthreads();
+    float s[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s[i][j] = 0.f;
+#pragma unroll 4
+    for (int d = 0; d < DH; ++d) {
+      const float4 qa = *reinterpret_cast<const float4*>(Qt + d * BQ + ty * 4);
+      const float4 kb = *reinterpret_cast<const float4*>(Kt + d * BK + tx * 4);
+      const float qv[4] = {qa.x, qa.y, qa.z, qa.w}, kw[4] = {kb.x, kb.y, kb.z, kb.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s[i][j] = fmaf(qv[i], kw[j], s[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        s[i][j] = (k0 + tx * 4 + j < nkv) ? s[i][j] * a.scale : -INFINITY;
+        mx = fmaxf(mx, s[i][j]);
+      }
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      const float mn = fmaxf(m[i], mx);
+      const float alpha = expf(m[i] - mn);
+      float rs = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        s[i][j] = expf(s[i][j] - mn);
+        rs += s[i][j];
+      }
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, off);
+      l[i] = l[i] * alpha + rs;
+      m[i] = mn;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) o[i][c] *= alpha;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<float4*>(Pt + (tx * 4 + j) * BQ + ty * 4) = make_float4(s[0][j], s[1][j], s[2][j], s[3][j]);
+    __syncthreads();
+#pragma unroll 2
+    for (int k = 0; k < BK; ++k) {
+      const float4 pa = *reinterpret_cast<const float4*>(Pt + k * BQ + ty * 4);
+      const float pv[4] = {pa.x, pa.y, pa.z, pa.w};
+#pragma unroll
+      for (int c4 = 0; c4 < CPT / 4; ++c4) {
+        const float4 vb = *reinterpret_cast<const float4*>(Vs + k * DH + tx * CPT + c4 * 4);
+        const float vv[4] = {vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) o[i][c4 * 4 + c] = fmaf(pv[i], vv[c], o[i][c4 * 4 + c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = q0 + ty * 4 + i;
+    if (r >= rows) continue;
+    const float inv = 1.f / l[i];
+    float* orow = a.out + r * a.ldo + c0 + tx * CPT;
+#pragma unroll
+    for (int c4 = 0; c4 < CPT / 4; ++c4)
+      *reinterpret_cast<float4*>(orow + c4 * 4) =
+          make_float4(o[i][c4 * 4] * inv, o[i][c4 * 4 + 1] * inv, o[i][c4 * 4 + 2] * inv, o[i][c4 * 4 + 3] * inv);
+  }
+}
+
+template <int DH>
+void launch_attn_f32_flash(const AttnArgs<float>& a, int64_t rows, int heads, cudaStream_t st) {
+  const size_t smem = sizeof(float) * (2 * DH * 64 + 64 * DH + 64 * 64);
+  set_smem_attr(k_attn_f32_flash<DH>, static_cast<int>(smem));
+  dim3 grid(static_cast<unsigned>((rows + 63) / 64), heads);
+  k_attn_f32_flash<DH><<<grid, 256, smem, st>>>(a, rows);
+  count_launch();
+}
+
 template <typename T>
 void launch_attention(const AttnArgs<T>& a, int64_t rows, int heads, cudaStream_t st) {
   if (rows <= 0) return;
   if (a.dh > 256) fail(BP_ERR_CONFIG, "SIMT attention supports head dim <= 256");
+  if constexpr (sizeof(T) == 4) {
+    const bool aligned = ((a.ldq | a.ldk1 | a.ldv1 | a.ldo | (a.n0 ? (a.ldk0 | a.ldv0) : 0)) & 3) == 0 &&
+                         ((reinterpret_cast<uintptr_t>(a.q) | reinterpret_cast<uintptr_t>(a.k1) |
+                           reinterpret_cast<uintptr_t>(a.v1) | reinterpret_cast<uintptr_t>(a.out) |
+                           (a.n0 ? (reinterpret_cast<uintptr_t>(a.k0) | reinterpret_cast<uintptr_t>(a.v0)) : 0)) & 15) == 0;
+    if (aligned && a.n0 + a.n1 > 0 && (a.dh == 128 || a.dh == 64)) {
+      if (a.dh == 128) launch_attn_f32_flash<128>(a, rows, heads, st);
+      else launch_attn_f32_flash<64>(a, rows, heads, st);
+      return;
+    }
+  }
   dim3 grid(static_cast<unsigned>(rows), heads);
   const size_t smem = sizeof(T) * (a.dh + 128);
   k_attention<T><<<grid, 128, smem, st>>>(a);
   count_launch();
 }
+
 template void launch_attention<double>(const AttnArgs<double>&, int64_t, int, cudaStream_t);
 template void launch_attention<float>(const AttnArgs<float>&, int64_t, int, cudaStream_t);
 

@@ -48,9 +48,10 @@ bp_status bp_selftest_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int3
   });
 }
 
-bp_status bp_selftest_attn(int32_t device, int64_t rows, int32_t heads, int32_t dh, const uint16_t* q,
-                           const uint16_t* k0, const uint16_t* v0, int64_t n0, const uint16_t* k1,
-                           const uint16_t* v1, int64_t n1, float scale, uint16_t* out) {
+namespace {
+bp_status selftest_attn(bool cross, int32_t device, int64_t rows, int32_t heads, int32_t dh, const uint16_t* q,
+                        const uint16_t* k0, const uint16_t* v0, int64_t n0, const uint16_t* k1,
+                        const uint16_t* v1, int64_t n1, float scale, uint16_t* out) {
   return bp::guarded([&] {
     BP_CUDA(cudaSetDevice(device));
     const int64_t H = static_cast<int64_t>(heads) * dh;
@@ -71,10 +72,23 @@ bp_status bp_selftest_attn(int32_t device, int64_t rows, int32_t heads, int32_t 
     a.k1 = dk1.as<bp::bf16>(); a.ldk1 = H; a.v1 = dv1.as<bp::bf16>(); a.ldv1 = H; a.n1 = n1;
     a.out = dout.as<bp::bf16>(); a.ldo = H;
     a.heads = heads; a.dh = dh; a.scale = scale;
-    bp::launch_attn_bf16(a, rows, nullptr);
+    if (cross) bp::launch_attn_bf16_cross(a, rows, nullptr);
+    else bp::launch_attn_bf16(a, rows, nullptr);
     BP_CUDA(cudaDeviceSynchronize());
     BP_CUDA(cudaMemcpy(out, dout.p, static_cast<size_t>(rows) * H * 2, cudaMemcpyDeviceToHost));
   });
+}
+}  // namespace
+
+bp_status bp_selftest_attn(int32_t device, int64_t rows, int32_t heads, int32_t dh, const uint16_t* q,
+                           const uint16_t* k0, const uint16_t* v0, int64_t n0, const uint16_t* k1,
+                           const uint16_t* v1, int64_t n1, float scale, uint16_t* out) {
+  return selftest_attn(false, device, rows, heads, dh, q, k0, v0, n0, k1, v1, n1, scale, out);
+}
+
+bp_status bp_selftest_attn_cross(int32_t device, int64_t rows, int32_t heads, int32_t dh, const uint16_t* q,
+                                 const uint16_t* k1, const uint16_t* v1, int64_t n1, float scale, uint16_t* out) {
+  return selftest_attn(true, device, rows, heads, dh, q, nullptr, nullptr, 0, k1, v1, n1, scale, out);
 }
 
 bp_status bp_bench_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int32_t epi, int32_t iters, double* ms) {
@@ -145,3 +159,32 @@ bp_status bp_bench_attn(int32_t device, int64_t rows, int32_t heads, int32_t dh,
 }
 
 }  // extern "C"
+
+bp_status bp_bench_ln(int32_t device, int64_t rows, int32_t n, int32_t iters, double* ms) {
+  return bp::guarded([&] {
+    BP_CUDA(cudaSetDevice(device));
+    bp::DevBuf x, g, y;
+    x.alloc(static_cast<size_t>(rows) * n * 4);
+    g.alloc(static_cast<size_t>(2 * n) * 4);
+    y.alloc(static_cast<size_t>(rows) * n * 2);
+    BP_CUDA(cudaMemset(x.p, 0x3f, static_cast<size_t>(rows) * n * 4));
+    BP_CUDA(cudaMemset(g.p, 0x3f, static_cast<size_t>(2 * n) * 4));
+    cudaStream_t st;
+    BP_CUDA(cudaStreamCreate(&st));
+    const float* gp = g.as<float>();
+    for (int i = 0; i < 3; ++i) bp::launch_ln_bf16(x.as<float>(), n, gp, gp + n, rows, n, y.as<bp::bf16>(), st);
+    cudaEvent_t e0, e1;
+    BP_CUDA(cudaEventCreate(&e0));
+    BP_CUDA(cudaEventCreate(&e1));
+    BP_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; ++i) bp::launch_ln_bf16(x.as<float>(), n, gp, gp + n, rows, n, y.as<bp::bf16>(), st);
+    BP_CUDA(cudaEventRecord(e1, st));
+    BP_CUDA(cudaEventSynchronize(e1));
+    float t = 0;
+    BP_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *ms = t / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+  });
+}

@@ -274,7 +274,7 @@ void Stage::recorded_rows(int layer, double* host_out) {
   BP_CUDA(cudaStreamSynchronize(stream_));
 }
 
-void Stage::ensure_workspace(int64_t tokens, int64_t capture) {
+void Stage::ensure_workspace(int64_t tokens, int64_t capture, bool new_cache, int use_prev) {
   const bool bf = prec_ == BP_PREC_BF16;
   const size_t te = prec_ == BP_PREC_F64 ? 8 : 4;
   const size_t me = bf ? 2 : te;
@@ -296,12 +296,15 @@ void Stage::ensure_workspace(int64_t tokens, int64_t capture) {
   qkv_.reserve(S * 3 * H * me);
   // the recording is written before the previous one is read: per parity
   if (capture > 0) recbuf_[parity_].reserve(nl * P * H * te);
-  // The KV cache of pass n is read by pass n+1's attention of layer l before
-  // that pass overwrites layer l's entry, so one buffer suffices; a growth
-  // keeps the old allocation alive until the next growth.
-  if (capture > 0 && nl * P * 2 * H * me > cap_.bytes) {
-    cap_old_ = std::move(cap_);
-    cap_.alloc(nl * P * 2 * H * me);
+  // The resident KV cache (read as the prefix when use_prev == 1) is read by
+  // layer l's attention before this pass writes layer l's new capture. With an
+  // equal capture size, layer l's new entry lands exactly on its old one, so
+  // the entry is reused in place. A different size would shift the layer
+  // offsets (layer 0's new entry could overwrite layer 1's old one before it
+  // is read), so such a capture goes to the other buffer.
+  if (new_cache) {
+    if (use_prev == 1 && capture != cache_.tokens) cap_sel_ ^= 1;
+    cap_[cap_sel_].reserve(nl * P * 2 * H * me);  // never the buffer being read (equal sizes need no growth)
   }
   if (capture > cap_capture_ || rec_.tokens > cap_capture_ || cache_.tokens > cap_capture_) {
     const int64_t p = std::max({capture, rec_.tokens, cache_.tokens, cap_capture_});
@@ -317,7 +320,7 @@ void Stage::ensure_workspace(int64_t tokens, int64_t capture) {
 // Runs of consecutive capture frames move with one launch.
 void Stage::capture_kv(const StageInput& in, int li, const void* qkv, size_t eb, Entry* nc) {
   const int64_t H = h_, P = static_cast<int64_t>(in.capture_frames.size()) * tpf_;
-  char* dst = cap_.as<char>() + static_cast<int64_t>(li) * P * 2 * H * static_cast<int64_t>(eb);
+  char* dst = cap_[cap_sel_].as<char>() + static_cast<int64_t>(li) * P * 2 * H * static_cast<int64_t>(eb);
   const char* src = static_cast<const char*>(qkv);
   const int64_t rs = 3 * H * static_cast<int64_t>(eb), rd = 2 * H * static_cast<int64_t>(eb);
   size_t f = 0;
@@ -382,7 +385,7 @@ const void* Stage::forward_simt(const StageInput& in) {
   const bool capturing = P > 0;
   const bool new_cache = capturing && in.mode == BP_CACHE_CACHED;
   const bool new_rec = capturing && (in.mode == BP_CACHE_RECOMPUTE || in.record_inputs);
-  ensure_workspace(S, P);
+  ensure_workspace(S, P, new_cache, in.use_prev);
   cudaStream_t st = stream_;
   T* x = x_.as<T>();
   T* ln = ln_.as<T>();
@@ -487,7 +490,7 @@ const void* Stage::forward_bf16(const StageInput& in) {
   const bool capturing = P > 0;
   const bool new_cache = capturing && in.mode == BP_CACHE_CACHED;
   const bool new_rec = capturing && (in.mode == BP_CACHE_RECOMPUTE || in.record_inputs);
-  ensure_workspace(S, P);
+  ensure_workspace(S, P, new_cache, in.use_prev);
   cudaStream_t st = stream_;
   float* x = x_.as<float>();
   bf16* ln = ln_.as<bf16>();

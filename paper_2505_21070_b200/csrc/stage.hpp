@@ -44,6 +44,7 @@ class Stage {
   size_t eps_bytes() const { return prec_ == BP_PREC_F64 ? 8 : 4; }
   int hidden() const { return m_.hidden; }
   int channels() const { return m_.channels; }
+  int tokens_per_frame() const { return tpf_; }
   int local_layers() const { return end_ - begin_; }
   cudaStream_t stream() const { return stream_; }
 
@@ -105,7 +106,7 @@ class Stage {
   DevBuf hostpre_;
   int64_t host_rows_ = 0;
   int host_kind_ = 0;
-  void ensure_workspace(int64_t tokens, int64_t capture_tokens);
+  void ensure_workspace(int64_t tokens, int64_t capture_tokens, bool new_cache = false, int use_prev = 0);
   void kv_prefix_from_recording(int li, const void* rec_rows, int64_t rows, void* kv_out);
   void capture_kv(const StageInput& in, int li, const void* qkv, size_t eb, Entry* nc);
 
@@ -130,8 +131,8 @@ class Stage {
   DevBuf x_, ln_, attn_, cq_, hmid_, eps_, kvp_, lnp_;
   DevBuf qkv_;             // [tokens][3h], reused by every layer
   DevBuf recbuf_[2];       // [L_local][capture][h] per parity (written before the old one is read)
-  DevBuf cap_, cap_old_;   // KV feature cache [L_local][capture][2h]; cap_old_ keeps a
-                           // replaced allocation alive for the pass that still reads it
+  DevBuf cap_[2];          // KV feature cache [L_local][capture][2h]; the second buffer
+  int cap_sel_ = 0;        // takes a capture whose size differs from the resident entry's
   DevBuf scratch_;         // audit
   int parity_ = 0;
   Entry cache_, rec_;

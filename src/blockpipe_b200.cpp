@@ -466,8 +466,11 @@ BubbleStats measure_bubbles(const EventLog& log) {
     last = std::max(last, e.slot);
   }
   const int64_t busy = static_cast<int64_t>(per[0].size());
-  for (const auto& v : per)
+  for (const auto& v : per) {
     if (static_cast<int64_t>(v.size()) != busy) throw SchedulingError("malformed event log: devices saw different pass counts");
+    for (size_t i = 1; i < v.size(); ++i)
+      if (v[i]->slot <= v[i - 1]->slot) throw SchedulingError("malformed event log: duplicate slot on one device");
+  }
   st.first_slot = first;
   st.last_slot = last;
   st.busy_per_device = busy;

@@ -5,6 +5,38 @@ import os
 
 import numpy as np
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TESTLIB_PATH = os.path.join(ROOT, "paper_2505_21070_b200", "lib", "libbp_cuda_test.so")
+
+i32, i64, f64 = C.c_int32, C.c_int64, C.c_double
+# kernel-level self-test hooks (include/bp_cuda_test.h), served by the test
+# library built from the product's objects plus selftest.cu
+TEST_SIGS = {
+    "bp_last_error": (C.c_char_p, []),
+    "bp_set_kernel_impl": (i32, [i32, i32]),
+    "bp_selftest_gemm": (i32, [i32, i32, i32, i32, i32, C.c_void_p, i64, C.c_void_p, C.c_void_p, i64]),
+    "bp_selftest_attn": (i32, [i32, i64, i32, i32, C.c_void_p, C.c_void_p, C.c_void_p, i64, C.c_void_p,
+                               C.c_void_p, i64, C.c_float, C.c_void_p]),
+    "bp_selftest_attn_cross": (i32, [i32, i64, i32, i32, C.c_void_p, C.c_void_p, C.c_void_p, i64, C.c_float,
+                                     C.c_void_p]),
+    "bp_bench_gemm": (i32, [i32, i32, i32, i32, i32, i32, C.POINTER(f64)]),
+    "bp_bench_attn": (i32, [i32, i64, i32, i32, i64, i64, i32, C.POINTER(f64)]),
+    "bp_bench_ln": (i32, [i32, i64, i32, i32, C.POINTER(f64)]),
+}
+_testlib = None
+
+
+def testlib():
+    global _testlib
+    if _testlib is None:
+        L = C.CDLL(TESTLIB_PATH)
+        for name, (res, args) in TEST_SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _testlib = L
+    return _testlib
+
 
 def to_bf16_bits(x: np.ndarray) -> np.ndarray:
     f = np.ascontiguousarray(x, dtype=np.float32)
@@ -25,6 +57,16 @@ def gemm(lib, A_bits, W_bits, C_init, epi, lda=None):
     st = lib.bp_selftest_gemm(0, M, N, K, epi, A_bits.ctypes.data, lda, W_bits.ctypes.data, Cb.ctypes.data, N)
     assert st == 0, lib.bp_last_error()
     return Cb
+
+
+def attn_cross(lib, q, k1, v1, heads, dh, scale):
+    """The stage's cross-attention launcher (one key segment)."""
+    rows = q.shape[0]
+    out = np.zeros((rows, heads * dh), dtype=np.uint16)
+    st = lib.bp_selftest_attn_cross(0, rows, heads, dh, q.ctypes.data, k1.ctypes.data, v1.ctypes.data, k1.shape[0],
+                                    C.c_float(scale), out.ctypes.data)
+    assert st == 0, lib.bp_last_error()
+    return out
 
 
 def attn(lib, q, k0, v0, k1, v1, heads, dh, scale):

@@ -1,0 +1,166 @@
+"""Parity at the shapes the bench runs (VERDICT r01 "parity at scale", SURVEY
+H3). Three tiers, each against a pinned checker:
+
+* one Wan-width layer at the FULL token shape of configs[1] (S = 18720
+  tokens per pass, a cached prefix of P = 6240) and of configs[4] (14B width,
+  S = 43200, P = 14400): a capture pass and a cached-prefix pass through
+  bp_forward_chunk in fp32 and bf16 against the numpy fp64 restatement
+  (oracle/blockpipe_oracle.py, itself pinned to the reference's goldens at
+  <= 1e-12) on sampled output rows -- forward_chunk (model.cpp:227-336) is
+  per-token except attention, so sampled rows are exact;
+* the whole pipeline at configs[1]'s token shape (30 x 52 grid, C 64,
+  h 1536, F 8960, 12 heads, Lc 512, num_b = num_c = 8), 2 blocks x 3 steps so
+  tail passes, prefix passes and cache capture -> consume all run: bf16
+  latents and every pass's eps against the fp32 verification path;
+* the self-attention kernel at the production launch (q 18720 x kv
+  6240 + 18720, 12 heads) and the cross-attention kernel (kv 512) against
+  fp64 attention on sampled query rows of every head.
+
+Tolerances are north_star's: fp32 <= 1e-4, bf16 <= 2e-2 (latents); the
+per-pass eps and kernel bounds are written next to each assert. Measured
+values go to $BP_PARITY_REPORT (a JSON-lines file) when it is set."""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+from kernels import attn, attn_cross, from_bf16_bits, testlib, to_bf16_bits
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+def report(**kw):
+    path = os.environ.get("BP_PARITY_REPORT")
+    print(json.dumps(kw))
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(kw) + "\n")
+
+
+def sample_rows(n, k, seed):
+    rng = np.random.default_rng(seed)
+    rows = np.unique(np.concatenate([[0, n - 1], rng.choice(n, size=k - 2, replace=False)]))
+    return rows
+
+
+WAN13 = dict(hidden=1536, heads=12, ffn=8960, channels=64, height=30, width=52, context_len=512)
+WAN14 = dict(hidden=5120, heads=40, ffn=13824, channels=64, height=45, width=80, context_len=512)
+
+
+@pytest.mark.parametrize("shape,name", [(WAN13, "wan13-480p"), (WAN14, "wan14b-720p")])
+def test_one_layer_full_shape_vs_oracle(bp, shape, name):
+    """First + last chunk of a one-layer model (entry embedding, the layer, the
+    head) over a 12-frame block: pass A captures the leading 4 centre frames
+    (P = 4 * tpf rows), pass B attends over [that cache ++ its own 12 frames]."""
+    from oracle import blockpipe_oracle as O
+    cfg = dict(shape, layers=1)
+    tpf = cfg["height"] * cfg["width"]
+    S = 12 * tpf
+    rng = np.random.default_rng(11)
+    xa, xb = rng.standard_normal((S, 64)), rng.standard_normal((S, 64))
+    lv_a, id_a = [50] * 12, list(range(0, 12))
+    lv_b, id_b = [49] * 4 + [50] * 8, list(range(8, 20))
+    cap = [4, 5, 6, 7]
+    rows = sample_rows(S, 384, 5)
+    t0 = time.time()
+    ch = O.build_chunk(cfg, 5, 0, 1)
+    ctx = O.build_context(cfg, 6)
+    want_a, kv = O.forward_chunk_rows(ch, xa, lv_a, id_a, ctx, rows, capture=cap)
+    want_b, _ = O.forward_chunk_rows(ch, xb, lv_b, id_b, ctx, rows, prefix=kv)
+    t_oracle = time.time() - t0
+    for prec, tol in (("f32", 1e-4), ("bf16", 2e-2)):
+        st = bp.Stage(bp.PipelineConfig(**cfg), 5, 0, 1, 6, precision=prec)
+        a = st.forward_chunk(xa, lv_a, id_a, capture_frames=cap, mode="on")
+        assert a["captured"] and a["captured_tokens"] == 4 * tpf
+        b = st.forward_chunk(xb, lv_b, id_b, mode="on", use_prev=1)
+        ra, rb = rel(a["payload"][rows], want_a), rel(b["payload"][rows], want_b)
+        report(test="one_layer_full_shape", shape=name, precision=prec, tokens=S, prefix=4 * tpf,
+               sampled_rows=len(rows), rel_l2_capture_pass=ra, rel_l2_prefix_pass=rb, tol=tol,
+               oracle_s=round(t_oracle, 1))
+        assert ra <= tol and rb <= tol, (prec, ra, rb)
+        st.close()
+
+
+@pytest.mark.parametrize("layers", [4, 30])
+def test_pipeline_bf16_vs_f32_at_configs1_shape(bp, layers):
+    """configs[1]'s token shape through run_pipeline: bf16 (the benchmarked
+    path) against the fp32 verification path, latents and every pass's eps."""
+    base = dict(WAN13, layers=layers, num_b=8, num_c=8, steps=3, blocks=2, devices=1, record_trace=True)
+    t0 = time.time()
+    f32 = bp.run_pipeline(dict(base, precision="f32"))
+    t_f32 = time.time() - t0
+    b16 = bp.run_pipeline(dict(base, precision="bf16"))
+    la = np.concatenate([b["frames"].ravel() for b in b16["blocks"]])
+    lb = np.concatenate([b["frames"].ravel() for b in f32["blocks"]])
+    assert la.size == (12 + 8) * 30 * 52 * 64
+    r_lat = rel(la, lb)
+    assert len(b16["trace"]) == len(f32["trace"]) == 6
+    r_eps = []
+    for x, y in zip(b16["trace"], f32["trace"]):
+        assert (x["round"], x["block_id"]) == (y["round"], y["block_id"])
+        r_eps.append(rel(x["eps"], y["eps"]))
+    # the model's contribution to the latents is O(1) of the noise, so the
+    # latents bound is north_star's 2e-2; eps (the model output itself) gets 3e-2
+    report(test="pipeline_bf16_vs_f32", layers=layers, tokens=18720, prefix=6240, passes=6,
+           rel_l2_latents=r_lat, rel_l2_eps_per_pass=r_eps, f32_run_s=round(t_f32, 1))
+    assert r_lat <= 2e-2, r_lat
+    assert max(r_eps) <= 3e-2, r_eps
+
+
+@pytest.fixture(scope="module")
+def tlib(bp):
+    return testlib()
+
+
+def _sampled_attention(q, k, v, rows, heads, dh, scale):
+    out = np.zeros((len(rows), heads * dh))
+    for hd in range(heads):
+        sl = slice(hd * dh, (hd + 1) * dh)
+        s = (q[rows][:, sl].astype(np.float64) @ k[:, sl].T.astype(np.float64)) * scale
+        s = np.exp(s - s.max(axis=1, keepdims=True))
+        out[:, sl] = (s / s.sum(axis=1, keepdims=True)) @ v[:, sl].astype(np.float64)
+    return out
+
+
+def test_self_attention_production_launch(tlib):
+    """k_attn_pp2 at the prefix-pass launch of configs[1] (390 key tiles that
+    straddle the cache/current boundary): bf16 inputs, fp64 reference on 512
+    sampled query rows of all 12 heads; the kernel's only roundings are P and
+    O to bf16, bound 1e-2 (as the kernel tests)."""
+    rows, n0, n1, heads, dh = 18720, 6240, 18720, 12, 128
+    rng = np.random.default_rng(21)
+    H = heads * dh
+    q = to_bf16_bits(rng.standard_normal((rows, H)))
+    k0, v0 = to_bf16_bits(rng.standard_normal((n0, H))), to_bf16_bits(rng.standard_normal((n0, H)))
+    k1, v1 = to_bf16_bits(rng.standard_normal((n1, H))), to_bf16_bits(rng.standard_normal((n1, H)))
+    scale = 1 / np.sqrt(dh)
+    got = from_bf16_bits(attn(tlib, q, k0, v0, k1, v1, heads, dh, scale)).astype(np.float64)
+    sr = sample_rows(rows, 512, 3)
+    want = _sampled_attention(from_bf16_bits(q), from_bf16_bits(np.concatenate([k0, k1])),
+                              from_bf16_bits(np.concatenate([v0, v1])), sr, heads, dh, scale)
+    per_head = [rel(got[sr][:, h * dh:(h + 1) * dh], want[:, h * dh:(h + 1) * dh]) for h in range(heads)]
+    report(test="self_attention_production_launch", q=rows, kv=[n0, n1], heads=heads, sampled_rows=len(sr),
+           rel_l2=rel(got[sr], want), rel_l2_worst_head=max(per_head))
+    assert max(per_head) < 1e-2, per_head
+    assert np.isfinite(got).all()
+
+
+def test_cross_attention_production_launch(tlib):
+    rows, n1, heads, dh = 18720, 512, 12, 128
+    rng = np.random.default_rng(22)
+    H = heads * dh
+    q = to_bf16_bits(rng.standard_normal((rows, H)))
+    k1, v1 = to_bf16_bits(rng.standard_normal((n1, H))), to_bf16_bits(rng.standard_normal((n1, H)))
+    scale = 1 / np.sqrt(dh)
+    got = from_bf16_bits(attn_cross(tlib, q, k1, v1, heads, dh, scale)).astype(np.float64)
+    sr = sample_rows(rows, 512, 4)
+    want = _sampled_attention(from_bf16_bits(q), from_bf16_bits(k1), from_bf16_bits(v1), sr, heads, dh, scale)
+    r = rel(got[sr], want)
+    report(test="cross_attention_production_launch", q=rows, kv=n1, heads=heads, sampled_rows=len(sr), rel_l2=r)
+    assert r < 1e-2, r

@@ -72,3 +72,23 @@ def test_reference_library_matches_goldens(ref):
     r = ref.run(cfg)
     lat = np.concatenate([b["frames"].ravel() for b in r["blocks"]])
     assert ref.fnv1a64([lat]) == G["cfg1"]["fnv"]
+
+
+def test_forward_chunk_rows_matches_full_restatement():
+    """The sampled-rows restatement used at Wan shapes (one-layer chunk)
+    equals the full restatement on the rows it returns, capture and prefix
+    routes included."""
+    from oracle import blockpipe_oracle as O
+    cfg = {"layers": 1, "hidden": 16, "heads": 2, "channels": 4, "height": 2, "width": 3, "context_len": 5, "ffn": 24}
+    ch = O.build_chunk(cfg, 7, 0, 1)
+    ctx = O.build_context(cfg, 8)
+    rng = np.random.default_rng(1)
+    x0, x1 = rng.standard_normal((4 * 6, 4)), rng.standard_normal((4 * 6, 4))
+    full0, cap0, _ = O.forward_chunk(ch, x0, [9, 9, 9, 9], [0, 1, 2, 3], ctx, mode="on", capture=[1, 2])
+    rows = [0, 5, 7, 23]
+    part0, pcap = O.forward_chunk_rows(ch, x0, [9, 9, 9, 9], [0, 1, 2, 3], ctx, rows, capture=[1, 2])
+    assert np.allclose(part0, full0[rows], rtol=1e-12, atol=1e-12)
+    assert np.array_equal(pcap[0], cap0[0][0]) and np.array_equal(pcap[1], cap0[0][1])
+    full1, _, _ = O.forward_chunk(ch, x1, [8] * 4, [2, 3, 4, 5], ctx, mode="on", cache=cap0)
+    part1, _ = O.forward_chunk_rows(ch, x1, [8] * 4, [2, 3, 4, 5], ctx, rows, prefix=pcap)
+    assert np.allclose(part1, full1[rows], rtol=1e-12, atol=1e-12)

@@ -52,6 +52,22 @@ def test_single_device_busy(bp):  # test_engine.cpp:53-64
     assert st["idle_per_device"] == 0 and st["ratio"] == 0.0 and st["busy_per_device"] == 16
 
 
+def test_malformed_event_logs(bp):
+    """measure_bubbles' validation (engine.cpp:508-530): a duplicated slot on
+    one device, a device index out of range, unequal pass counts."""
+    ev = bp.Schedule(tiny(devices=2, steps=4, blocks=3)).events.copy()
+    firsts = [np.flatnonzero(ev[:, 1] == d)[0] for d in range(2)]
+    dup = np.concatenate([ev, ev[firsts]])  # every device sees its first slot twice
+    with pytest.raises(bp.SchedulingError, match="duplicate slot on one device"):
+        bp.measure_bubbles(dup, 2)
+    bad = ev.copy()
+    bad[0, 1] = 5
+    with pytest.raises(bp.SchedulingError, match="device out of range"):
+        bp.measure_bubbles(bad, 2)
+    with pytest.raises(bp.SchedulingError, match="different pass counts"):
+        bp.measure_bubbles(ev[1:], 2)
+
+
 def test_bubble_formula_proximity(bp):  # test_engine.cpp:152-173
     for n, steps, blocks in [(2, 8, 6), (4, 10, 8), (4, 50, 4)]:
         s = bp.Schedule(tiny(devices=n, steps=steps, blocks=blocks))

@@ -1,7 +1,9 @@
 """FFN-up GEMM shape with each epilogue (bf16 store, erf-GELU, fp32 store):\nthe cost of the epilogue over the mainloop.  python tools/gemm_epilogue_probe.py"""
 import ctypes, os, sys
 sys.path.insert(0, os.getcwd())
-from paper_2505_21070_b200._lib import lib
+sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+from kernels import testlib
+lib = testlib()
 ms = ctypes.c_double()
 for epi, tag in ((0, "store"), (1, "gelu"), (3, "f32 store")):
     assert lib.bp_bench_gemm(0, 18720, 8960, 1536, epi, 20, ctypes.byref(ms)) == 0
