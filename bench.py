@@ -383,9 +383,9 @@ def ln_kernel_roofline(device, tokens, hidden, peaks):
     (built from the same objects as libbp_cuda.so)."""
     import ctypes
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from kernels import testlib
+    from kernels import load_testlib
     ms = ctypes.c_double()
-    if testlib().bp_bench_ln(device, tokens, hidden, 20, ctypes.byref(ms)) != 0:
+    if load_testlib().bp_bench_ln(device, tokens, hidden, 20, ctypes.byref(ms)) != 0:
         return None
     bytes_launch = tokens * hidden * 6 + 2 * hidden * 4  # x read (fp32) + y written (bf16) + g, b
     gbs = bytes_launch / (ms.value * 1e-3) / 1e9

@@ -11,6 +11,55 @@
 
 namespace bp {
 
+NoiseIds draw_noise_ids(int strategy, bool first, int num_b, int num_c, const std::vector<int>& tail_window,
+                        int64_t frame_elems, HostRng& rng) {
+  const int M = num_b + num_c / 2, ctx = num_c / 2;
+  NoiseIds n;
+  n.frames = first ? M : num_b;
+  if (strategy == BP_INIT_FRESH) {  // fresh Gaussians from the append stream
+    n.fresh = true;
+    n.fresh_state = rng.state;
+    rng.skip_normals(static_cast<int64_t>(n.frames) * frame_elems);
+    return n;
+  }
+  if (first) {  // draw_first_block (noise.cpp:135-152)
+    if (strategy == BP_INIT_REPEAT) {
+      for (int i = 0; i < M; ++i) n.ids.push_back(i);
+    } else {
+      n.ids = rng.permutation(M);
+    }
+    return n;
+  }
+  switch (strategy) {  // draw_next_block (noise.cpp:154-178)
+    case BP_INIT_COORDINATED: {  // init_next_block (noise.cpp:77-101)
+      if (static_cast<int>(tail_window.size()) != ctx) fail(BP_ERR_QUEUE, "tail window must hold num_c/2 ids");
+      std::set<int> excluded(tail_window.begin(), tail_window.end());
+      if (static_cast<int>(excluded.size()) != ctx) fail(BP_ERR_QUEUE, "tail window ids must be distinct");
+      for (int e : excluded)
+        if (e < 0 || e >= M) fail(BP_ERR_QUEUE, "tail window id out of pool range");
+      std::vector<int> remaining;
+      for (int i = 0; i < M; ++i)
+        if (!excluded.count(i)) remaining.push_back(i);
+      for (int p : rng.permutation(static_cast<int>(remaining.size())))
+        n.ids.push_back(remaining[static_cast<size_t>(p)]);
+      break;
+    }
+    case BP_INIT_COMPLETE_SHUFFLE:
+    case BP_INIT_SUBSET: {
+      const std::vector<int> perm = rng.permutation(M);
+      n.ids.assign(perm.begin(), perm.begin() + num_b);
+      break;
+    }
+    case BP_INIT_REPEAT:
+      for (int i = M - num_b; i < M; ++i) n.ids.push_back(i);
+      break;
+    default:
+      fail(BP_ERR_CONFIG, "unknown noise strategy");
+  }
+  return n;
+}
+
+
 int ffn_width(const bp_model_desc& m) { return m.ffn > 0 ? m.ffn : 4 * m.hidden; }
 
 // ModelConfig::validate (model.cpp:76-85).
@@ -138,61 +187,20 @@ Schedule build_schedule(const bp_pipeline_desc& d) {
   auto make_block = [&](int64_t id) {
     SchedBlock b;
     b.id = id;
-    const int strat = d.strategy;
-    if (id == 1) {
-      if (strat == BP_INIT_REPEAT) {
-        for (int i = 0; i < M; ++i) b.noise_ids.push_back(i);
-      } else if (strat == BP_INIT_FRESH) {
-        b.fresh = true;
-        b.fresh_state = append_rng.state;
-        append_rng.skip_normals(static_cast<int64_t>(M) * hwc);
-      } else {
-        b.noise_ids = append_rng.permutation(M);
+    std::vector<int> window;
+    if (id > 1 && ctx > 0) {
+      const SchedBlock& tail = s.blocks[static_cast<size_t>(q.back().id - 1)];
+      if (static_cast<int>(tail.noise_ids.size()) >= ctx) {
+        window.assign(tail.noise_ids.end() - ctx, tail.noise_ids.end());
+      } else if (d.strategy == BP_INIT_COORDINATED) {
+        fail(BP_ERR_QUEUE, "tail block lacks noise ids for the exclusion window");
       }
-      b.frames = M;
-    } else {
-      std::vector<int> window;
-      if (ctx > 0) {
-        const SchedBlock& tail = s.blocks[static_cast<size_t>(q.back().id - 1)];
-        if (static_cast<int>(tail.noise_ids.size()) >= ctx) {
-          window.assign(tail.noise_ids.end() - ctx, tail.noise_ids.end());
-        } else if (strat == BP_INIT_COORDINATED) {
-          fail(BP_ERR_QUEUE, "tail block lacks noise ids for the exclusion window");
-        }
-      }
-      switch (strat) {
-        case BP_INIT_COORDINATED: {  // init_next_block (noise.cpp:77-101)
-          if (static_cast<int>(window.size()) != ctx)
-            fail(BP_ERR_QUEUE, "tail window must hold num_c/2 ids");
-          std::set<int> excluded(window.begin(), window.end());
-          if (static_cast<int>(excluded.size()) != ctx)
-            fail(BP_ERR_QUEUE, "tail window ids must be distinct");
-          for (int e : excluded)
-            if (e < 0 || e >= M) fail(BP_ERR_QUEUE, "tail window id out of pool range");
-          std::vector<int> remaining;
-          for (int i = 0; i < M; ++i)
-            if (!excluded.count(i)) remaining.push_back(i);
-          const std::vector<int> perm = append_rng.permutation(static_cast<int>(remaining.size()));
-          for (int p : perm) b.noise_ids.push_back(remaining[static_cast<size_t>(p)]);
-          break;
-        }
-        case BP_INIT_COMPLETE_SHUFFLE:
-        case BP_INIT_SUBSET: {
-          const std::vector<int> perm = append_rng.permutation(M);
-          b.noise_ids.assign(perm.begin(), perm.begin() + d.num_b);
-          break;
-        }
-        case BP_INIT_FRESH:
-          b.fresh = true;
-          b.fresh_state = append_rng.state;
-          append_rng.skip_normals(static_cast<int64_t>(d.num_b) * hwc);
-          break;
-        case BP_INIT_REPEAT:
-          for (int i = M - d.num_b; i < M; ++i) b.noise_ids.push_back(i);
-          break;
-      }
-      b.frames = d.num_b;
     }
+    NoiseIds n = draw_noise_ids(d.strategy, id == 1, d.num_b, d.num_c, window, hwc, append_rng);
+    b.noise_ids = std::move(n.ids);
+    b.frames = n.frames;
+    b.fresh = n.fresh;
+    b.fresh_state = n.fresh_state;
     for (int k = 0; k < b.frames; ++k) b.frame_ids.push_back(next_frame_id++);
     return b;
   };

@@ -29,6 +29,20 @@ struct SchedBlock {
   int64_t append_round = 0;
 };
 
+// draw_first_block / draw_next_block (noise.cpp:135-178) on the host integer
+// stream: the pool ids of one block, or (kFresh) the stream position of its
+// frames * frame_elems fresh normals, which the stream then skips. A first
+// block has num_b + num_c/2 frames, later blocks num_b.
+struct NoiseIds {
+  std::vector<int> ids;
+  int frames = 0;
+  bool fresh = false;
+  uint64_t fresh_state = 0;
+};
+struct HostRng;
+NoiseIds draw_noise_ids(int strategy, bool first, int num_b, int num_c, const std::vector<int>& tail_window,
+                        int64_t frame_elems, HostRng& rng);
+
 struct SchedPass {
   int64_t index = 0, round = 0, block = 0;
   int level = 0, phase = 0;

@@ -26,7 +26,7 @@ TEST_SIGS = {
 _testlib = None
 
 
-def testlib():
+def load_testlib():
     global _testlib
     if _testlib is None:
         L = C.CDLL(TESTLIB_PATH)

@@ -52,8 +52,8 @@ def test_only_c_abi_is_exported(bp):
         return {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
 
     assert exported(_lib.LIB_PATH) == declared_functions()
-    testlib = os.path.join(os.path.dirname(_lib.LIB_PATH), "libbp_cuda_test.so")
-    assert exported(testlib) == declared_functions(("bp_cuda.h", "bp_cuda_test.h"))
+    load_testlib = os.path.join(os.path.dirname(_lib.LIB_PATH), "libbp_cuda_test.so")
+    assert exported(load_testlib) == declared_functions(("bp_cuda.h", "bp_cuda_test.h"))
 
 
 def test_compute_entry_points_fail_loudly_without_gpu(bp):

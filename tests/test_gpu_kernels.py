@@ -2,14 +2,14 @@
 import numpy as np
 import pytest
 
-from kernels import DEFAULT_ATTN_IMPL, DEFAULT_GEMM_IMPL, attn, from_bf16_bits, gemm, ref_attn, testlib, to_bf16_bits
+from kernels import DEFAULT_ATTN_IMPL, DEFAULT_GEMM_IMPL, attn, from_bf16_bits, gemm, ref_attn, load_testlib, to_bf16_bits
 
 pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(scope="module")
 def lib(bp):
-    L = testlib()
+    L = load_testlib()
     yield L
     L.bp_set_kernel_impl(DEFAULT_GEMM_IMPL, DEFAULT_ATTN_IMPL)
 

@@ -26,7 +26,7 @@ import time
 import numpy as np
 import pytest
 
-from kernels import attn, attn_cross, from_bf16_bits, testlib, to_bf16_bits
+from kernels import attn, attn_cross, from_bf16_bits, load_testlib, to_bf16_bits
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -115,7 +115,7 @@ def test_pipeline_bf16_vs_f32_at_configs1_shape(bp, layers):
 
 @pytest.fixture(scope="module")
 def tlib(bp):
-    return testlib()
+    return load_testlib()
 
 
 def _sampled_attention(q, k, v, rows, heads, dh, scale):

@@ -3,8 +3,8 @@ shapes (a debugging aid):  python tools/attn_probe.py IMPL"""
 import sys, os
 sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
 import numpy as np
-from kernels import attn, ref_attn, to_bf16_bits, from_bf16_bits, DEFAULT_GEMM_IMPL, testlib
-lib = testlib()
+from kernels import attn, ref_attn, to_bf16_bits, from_bf16_bits, DEFAULT_GEMM_IMPL, load_testlib
+lib = load_testlib()
 impl = int(sys.argv[1])
 for (rows, n0, n1, heads) in [(96,0,512,3),(96,0,512,1),(128,0,512,3),(256,0,512,3),(96,0,448,3),(96,0,576,3),(96,0,512,2),(300,0,512,1),(96,0,256,3),(96,0,384,3)]:
     dh=128; rng=np.random.default_rng(rows+n0*3+n1+heads); H=heads*dh

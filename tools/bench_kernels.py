@@ -9,9 +9,9 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
-from kernels import testlib  # noqa: E402
+from kernels import load_testlib  # noqa: E402
 
-lib = testlib()
+lib = load_testlib()
 
 what = sys.argv[1] if len(sys.argv) > 1 else "attn"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3

@@ -2,8 +2,8 @@
 import ctypes, os, sys
 sys.path.insert(0, os.getcwd())
 sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
-from kernels import testlib
-lib = testlib()
+from kernels import load_testlib
+lib = load_testlib()
 ms = ctypes.c_double()
 for epi, tag in ((0, "store"), (1, "gelu"), (3, "f32 store")):
     assert lib.bp_bench_gemm(0, 18720, 8960, 1536, epi, 20, ctypes.byref(ms)) == 0
