@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <deque>
 #include <initializer_list>
 #include <memory>
 #include <optional>
@@ -51,6 +52,22 @@ struct Tensor {
   bool all_finite() const;
   Tensor reshaped(std::vector<int64_t> s) const;
 };
+
+// Free functions of P/tensor.hpp:36-57. matmul / softmax_rows / layer_norm /
+// add / sub / scale run on the GPU (bp_matmul, bp_softmax_rows,
+// bp_layer_norm, bp_elementwise: the reference's operation order, so results
+// are bitwise or within 1e-13 of the reference's); vcat_rows / slice_rows /
+// take_rows are row copies of the host container. Same shape checks and
+// DimensionError messages as tensor.cpp.
+Tensor matmul(const Tensor& a, const Tensor& b);
+Tensor softmax_rows(const Tensor& x);
+Tensor layer_norm(const Tensor& x, double eps);
+Tensor add(const Tensor& a, const Tensor& b);
+Tensor sub(const Tensor& a, const Tensor& b);
+Tensor scale(const Tensor& a, double s);
+Tensor vcat_rows(const Tensor& a, const Tensor& b);
+Tensor slice_rows(const Tensor& x, int64_t begin, int64_t end);
+Tensor take_rows(const Tensor& x, const std::vector<int64_t>& idx);
 
 // ---------------------------------------------------------------- rng (P/rng.hpp)
 // The integer stream runs on the host; normal_tensor draws on the GPU (bit-exact).
@@ -147,8 +164,65 @@ enum class InitStrategy { kCoordinated, kCompleteShuffle, kSubset, kFresh, kRepe
 InitStrategy parse_strategy(const std::string& name);
 std::string strategy_name(InitStrategy s);
 
+// P/noise.hpp:40-68. Ids come from the host integer stream of `rng` (advanced
+// exactly as the reference advances it); frames are stacked from the pool on
+// the GPU (bp_gather_block / bp_noise_draw), fresh normals drawn on the GPU.
+struct NoiseDraw {
+  Tensor frames;               // [f, H, W, C]
+  std::vector<int> noise_ids;  // pool ids per frame; empty for kFresh
+};
+NoiseDraw init_first_block(const NoisePool& pool, RandomSource& rng);
+NoiseDraw init_next_block(const NoisePool& pool, const std::vector<int>& tail_window_ids, RandomSource& rng);
+NoiseDraw init_baseline(InitStrategy variant, const NoisePool& pool, RandomSource& rng);
+NoiseDraw draw_first_block(InitStrategy s, const NoisePool& pool, RandomSource& rng);
+NoiseDraw draw_next_block(InitStrategy s, const NoisePool& pool, const std::vector<int>& tail_window_ids,
+                          RandomSource& rng);
+
+// P/block_queue.hpp:13-102: the FIFO of latent blocks on the host (the engine
+// itself replays the same lifecycle from its static schedule, schedule.cpp).
+struct LatentBlock {
+  int64_t block_id = 0;
+  Tensor frames;                      // current state [f, H, W, C]
+  std::optional<Tensor> prev_frames;  // state before the last update
+  int level = 0;
+  int updates = 0;
+  std::vector<int> noise_ids;
+  std::vector<int64_t> frame_ids;
+  int64_t frame_count() const { return frames.rows() == 0 ? 0 : frames.shape[0]; }
+};
+struct RetainedContext {
+  int64_t source_block_id = 0;
+  Tensor frames;  // [num_c/2, H, W, C], level 0
+  std::vector<int64_t> frame_ids;
+};
+struct QueueState {
+  QueueParams params;
+  std::deque<LatentBlock> blocks;  // head first
+  int64_t appended_count = 0;
+  std::optional<RetainedContext> retained;
+  std::vector<int64_t> popped_ids;
+  const LatentBlock* find(int64_t block_id) const;
+  LatentBlock* find(int64_t block_id);
+  int context_frames() const { return params.num_c / 2; }
+};
+struct ExtendedBlock {
+  enum class CtxSource { kNone, kInQueue, kRetained };
+  int64_t center_id = 0;
+  CtxSource source = CtxSource::kNone;
+  int64_t ctx_block_id = 0;
+  Tensor explicit_frames;
+  std::vector<int> explicit_levels;
+  std::vector<int64_t> explicit_frame_ids;
+  std::optional<int64_t> cached_context_id;
+};
+void apply_update(QueueState& q, int64_t block_id, Tensor frames);
+QueueState advance(QueueState q, std::optional<LatentBlock> new_block);
+std::vector<int64_t> processing_order(const QueueState& q, Order order);
+ExtendedBlock assemble_extended(const QueueState& q, int64_t block_id, Order order);
+bool levels_are_unit_ladder(const QueueState& q);
+
 // ---------------------------------------------------------------- engine (P/engine.hpp)
-enum class Transport { kLoopback = 0, kNccl = 1 };
+enum class Transport { kLoopback = 0, kNccl = 1, kIpc = 2 };  // bp_transport
 struct PipelineConfig {
   int devices = 2;
   Order order = Order::kReverse;

@@ -110,6 +110,29 @@ BP_API bp_status bp_normals(int32_t device, uint64_t state, int64_t n, double si
 BP_API bp_status bp_noise_pool(int32_t device, int32_t num_b, int32_t num_c, const int64_t frame_shape[3],
                         uint64_t noise_seed, double* out, int32_t out_is_device);
 
+/* stack_entries (noise.cpp:12-22): out[i] = pool entry ids[i], each entry
+ * frame_elems = H*W*C doubles; ids must lie in [0, pool_size). Host buffers,
+ * or device buffers when io_on_device != 0. */
+BP_API bp_status bp_gather_block(int32_t device, const double* pool, int32_t pool_size, int64_t frame_elems,
+                                 const int32_t* ids, int32_t nids, double* out, int32_t io_on_device);
+
+/* draw_first_block (first != 0) / draw_next_block (noise.cpp:135-178) with
+ * strategy bp_init_strategy: the pool ids on the host from *rng_state (the
+ * append RandomSource's state, advanced in place exactly as the reference
+ * advances it), the frames on the GPU -- pool entries stacked by id, or for
+ * BP_INIT_FRESH fresh normals of the same stream (bit-exact). pool holds
+ * pool_size = num_b + num_c/2 entries of H*W*C doubles (build_pool's layout);
+ * tail_window_ids (ntail = num_c/2 ids) is the coordinated exclusion window,
+ * ignored by the baselines. out_frames needs (first ? pool_size : num_b) *
+ * H*W*C doubles, out_ids as many ints; *out_frames_count / *out_nids receive
+ * the frame count and the number of ids (0 for fresh). Host buffers, or
+ * device buffers (pool, out_frames) when io_on_device != 0. */
+BP_API bp_status bp_noise_draw(int32_t device, int32_t strategy, int32_t first, int32_t num_b, int32_t num_c,
+                               const int64_t frame_shape[3], const double* pool, int32_t pool_size,
+                               const int32_t* tail_window_ids, int32_t ntail, uint64_t* rng_state,
+                               double* out_frames, int32_t* out_ids, int32_t* out_frames_count, int32_t* out_nids,
+                               int32_t io_on_device);
+
 /* ---- model.hpp: one pipeline stage (ModelChunk) -------------------------------- */
 typedef struct bp_stage bp_stage;
 
@@ -180,6 +203,11 @@ BP_API bp_status bp_scheduler_step(int32_t device, const double* x, const double
 /* matmul (tensor.cpp:84-109): out[m,n] = a[m,k] @ b[k,n]; ascending-k accumulation. */
 BP_API bp_status bp_matmul(int32_t device, const double* a, const double* b, int64_t m, int64_t k, int64_t n,
                            double* out);
+/* add / sub / scale (tensor.cpp:148-172) over n doubles: op 0 out = a + b,
+ * op 1 out = a - b, op 2 out = a * s (b unused). One IEEE operation per
+ * element, bitwise the reference's. */
+BP_API bp_status bp_elementwise(int32_t device, int32_t op, const double* a, const double* b, int64_t n, double s,
+                                double* out);
 /* softmax_rows (tensor.cpp:111-126) over [rows, cols]. */
 BP_API bp_status bp_softmax_rows(int32_t device, const double* x, int64_t rows, int64_t cols, double* out);
 /* layer_norm (tensor.cpp:128-146), no affine, over [rows, cols]. */

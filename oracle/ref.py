@@ -77,6 +77,8 @@ def lib():
         L.bpref_method_cost.argtypes = [C.c_char_p, P(i64), P(f64), C.c_int, P(f64)]
         L.bpref_noise_walk.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, u64, C.c_int, P(C.c_int),
                                        P(C.c_int)]
+        L.bpref_noise_walk_frames.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, P(i64), u64, C.c_int,
+                                              P(C.c_int), P(C.c_int), P(f64), P(i64)]
         _lib = L
     return _lib
 
@@ -284,6 +286,26 @@ def noise_walk(strategy: str, appends: int, num_b: int, num_c: int, seed: int):
     counts = (C.c_int * (appends + 1))()
     _ck(lib().bpref_noise_walk(strategy.encode(), appends, num_b, num_c, seed, cap, ids, counts))
     return [[ids[r * cap + k] for k in range(counts[r])] for r in range(appends + 1)]
+
+
+def noise_walk_frames(strategy: str, appends: int, num_b: int, num_c: int, shape, seed: int):
+    """The reference's draw_first_block + `appends` draw_next_block calls:
+    [(noise_ids, frames [f, H, W, C])] per draw."""
+    cap = num_b + num_c // 2
+    per = int(np.prod(shape))
+    ids = (C.c_int * ((appends + 1) * cap))()
+    counts = (C.c_int * (appends + 1))()
+    frames = np.empty((appends + 1) * cap * per)
+    sh = (i64 * 3)(*shape)
+    nv = i64()
+    _ck(lib().bpref_noise_walk_frames(strategy.encode(), appends, num_b, num_c, sh, seed, cap, ids, counts,
+                                      frames.ctypes.data_as(P(f64)), C.byref(nv)))
+    out, at = [], 0
+    for r in range(appends + 1):
+        f = cap if r == 0 else num_b
+        out.append(([ids[r * cap + k] for k in range(counts[r])], frames[at:at + f * per].reshape((f,) + tuple(shape))))
+        at += f * per
+    return out
 
 
 def permutation(seed: int, n: int) -> np.ndarray:

@@ -378,3 +378,34 @@ extern "C" int bpref_noise_walk(const char* strategy, int appends, int num_b, in
     }
   });
 }
+
+// draw_first_block then `appends` draw_next_block calls (the engine's window
+// rule, engine.cpp:301-324) over a pool of frame_shape; frames of every draw
+// concatenated into frames_out (capacity (appends + 1) * M * H*W*C), ids as
+// bpref_noise_walk.
+extern "C" int bpref_noise_walk_frames(const char* strategy, int appends, int num_b, int num_c, const int64_t* shape,
+                                       uint64_t seed, int cap_per, int* ids, int* counts, double* frames_out,
+                                       int64_t* nvals) {
+  return guard([&] {
+    const InitStrategy s = parse_strategy(strategy);
+    NoisePool pool = build_pool(num_b, num_c, {shape[0], shape[1], shape[2]}, seed);
+    RandomSource rng(derive_seed(seed, {1}));
+    int64_t at = 0;
+    auto put = [&](int row, const NoiseDraw& d) {
+      counts[row] = static_cast<int>(d.noise_ids.size());
+      for (int k = 0; k < cap_per; ++k)
+        ids[row * cap_per + k] = k < static_cast<int>(d.noise_ids.size()) ? d.noise_ids[static_cast<size_t>(k)] : -1;
+      for (double v : d.frames.data) frames_out[at++] = v;
+    };
+    NoiseDraw cur = draw_first_block(s, pool, rng);
+    put(0, cur);
+    for (int i = 1; i <= appends; ++i) {
+      std::vector<int> window;
+      const int w = num_c / 2;
+      if (w > 0 && static_cast<int>(cur.noise_ids.size()) >= w) window.assign(cur.noise_ids.end() - w, cur.noise_ids.end());
+      cur = draw_next_block(s, pool, window, rng);
+      put(i, cur);
+    }
+    *nvals = at;
+  });
+}

@@ -96,6 +96,10 @@ _SIGS = {
     "bp_stage_cache_audit": (i32, [C.c_void_p, C.c_char_p, i32]),
     "bp_scheduler_step": (i32, [i32, P(f64), P(f64), i64, i32, i32, P(f64)]),
     "bp_matmul": (i32, [i32, P(f64), P(f64), i64, i64, i64, P(f64)]),
+    "bp_elementwise": (i32, [i32, i32, P(f64), P(f64), i64, f64, P(f64)]),
+    "bp_gather_block": (i32, [i32, P(f64), i32, i64, P(i32), i32, P(f64), i32]),
+    "bp_noise_draw": (i32, [i32, i32, i32, i32, i32, P(i64), P(f64), i32, P(i32), i32, P(u64), P(f64), P(i32),
+                            P(i32), P(i32), i32]),
     "bp_softmax_rows": (i32, [i32, P(f64), i64, i64, P(f64)]),
     "bp_layer_norm": (i32, [i32, P(f64), i64, i64, f64, P(f64)]),
     "bp_schedule_create": (i32, [P(PipelineDesc), P(C.c_void_p)]),

@@ -54,6 +54,49 @@ def build_pool(num_b: int, num_c: int, frame_shape: Sequence[int], noise_seed: i
     return out
 
 
+def gather_block(pool: np.ndarray, ids: Sequence[int], device: int = 0) -> np.ndarray:
+    """stack_entries (noise.cpp:12-22) on the GPU: pool [M, H, W, C] -> [len(ids), H, W, C]."""
+    pool = np.ascontiguousarray(pool, dtype=np.float64)
+    idx = np.ascontiguousarray(ids, dtype=np.int32)
+    per = int(np.prod(pool.shape[1:]))
+    out = np.empty((len(idx),) + pool.shape[1:], dtype=np.float64)
+    check(lib.bp_gather_block(device, _ptr(pool, f64), pool.shape[0], per, _ptr(idx, i32), len(idx),
+                              _ptr(out, f64), 0))
+    return out
+
+
+def _noise_draw(strategy: str, first: bool, pool: np.ndarray, num_b: int, num_c: int,
+                tail_window_ids: Sequence[int], rng_state: int, device: int) -> Dict[str, Any]:
+    from .config import STRATEGIES
+    if strategy not in STRATEGIES:
+        raise errors.ConfigError(f"unknown noise strategy: {strategy}")
+    pool = np.ascontiguousarray(pool, dtype=np.float64)
+    shape = (i64 * 3)(*pool.shape[1:])
+    cap = pool.shape[0] if first else num_b
+    frames = np.empty((cap,) + pool.shape[1:], dtype=np.float64)
+    ids = np.zeros(max(cap, 1), dtype=np.int32)
+    win = np.ascontiguousarray(tail_window_ids, dtype=np.int32)
+    state = u64(rng_state)
+    nf, ni = i32(), i32()
+    check(lib.bp_noise_draw(device, STRATEGIES[strategy], int(first), num_b, num_c, shape, _ptr(pool, f64),
+                            pool.shape[0], _ptr(win, i32), len(win), C.byref(state), _ptr(frames, f64),
+                            _ptr(ids, i32), C.byref(nf), C.byref(ni), 0))
+    return {"frames": frames[:nf.value], "noise_ids": ids[:ni.value].tolist(), "rng_state": int(state.value)}
+
+
+def draw_first_block(strategy: str, pool: np.ndarray, num_b: int, num_c: int, rng_state: int,
+                     device: int = 0) -> Dict[str, Any]:
+    """draw_first_block (noise.cpp:135-152): NoiseDraw {frames, noise_ids} and
+    the append RandomSource's state after the draw."""
+    return _noise_draw(strategy, True, pool, num_b, num_c, (), rng_state, device)
+
+
+def draw_next_block(strategy: str, pool: np.ndarray, num_b: int, num_c: int, tail_window_ids: Sequence[int],
+                    rng_state: int, device: int = 0) -> Dict[str, Any]:
+    """draw_next_block (noise.cpp:154-178); coordinated excludes tail_window_ids."""
+    return _noise_draw(strategy, False, pool, num_b, num_c, tail_window_ids, rng_state, device)
+
+
 def scheduler_step(x: np.ndarray, eps: np.ndarray, level: int, steps: int, device: int = 0) -> np.ndarray:
     """scheduler_step (model.cpp:338-345) on the GPU."""
     x = np.ascontiguousarray(x, dtype=np.float64)

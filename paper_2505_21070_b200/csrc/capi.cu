@@ -114,6 +114,83 @@ bp_status bp_noise_pool(int32_t device, int32_t num_b, int32_t num_c, const int6
   });
 }
 
+namespace {
+// Frames of one block from the pool by id, on the device; host or device I/O.
+void gather_block(const double* pool, int32_t pool_size, int64_t per, const std::vector<int32_t>& ids, double* out,
+                  bool on_device) {
+  for (int32_t id : ids)
+    if (id < 0 || id >= pool_size) bp::fail(BP_ERR_QUEUE, "noise id out of pool range");
+  const int n = static_cast<int>(ids.size());
+  bp::DevBuf dids, dpool, dout;
+  dids.alloc(static_cast<size_t>(n) * 4 + 4);
+  if (n > 0) BP_CUDA(cudaMemcpy(dids.p, ids.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice));
+  const double* src = pool;
+  double* dst = out;
+  if (!on_device) {
+    dpool.alloc(static_cast<size_t>(pool_size) * per * 8 + 8);
+    BP_CUDA(cudaMemcpy(dpool.p, pool, static_cast<size_t>(pool_size) * per * 8, cudaMemcpyHostToDevice));
+    src = dpool.as<double>();
+    dout.alloc(static_cast<size_t>(n) * per * 8 + 8);
+    dst = dout.as<double>();
+  }
+  bp::launch_gather_ids(src, per, dids.as<int32_t>(), n, dst, nullptr);
+  BP_CUDA(cudaDeviceSynchronize());
+  if (!on_device && n > 0) BP_CUDA(cudaMemcpy(out, dst, static_cast<size_t>(n) * per * 8, cudaMemcpyDeviceToHost));
+}
+}  // namespace
+
+bp_status bp_gather_block(int32_t device, const double* pool, int32_t pool_size, int64_t frame_elems,
+                          const int32_t* ids, int32_t nids, double* out, int32_t io_on_device) {
+  return bp::guarded([&] {
+    if (pool_size < 0 || frame_elems < 0 || nids < 0) bp::fail(BP_ERR_DIMENSION, "negative size");
+    if ((nids > 0 && (!ids || !out)) || (pool_size > 0 && !pool)) bp::fail(BP_ERR_CONFIG, "null argument");
+    bp::require_device(device);
+    gather_block(pool, pool_size, frame_elems, std::vector<int32_t>(ids, ids + nids), out, io_on_device != 0);
+  });
+}
+
+bp_status bp_noise_draw(int32_t device, int32_t strategy, int32_t first, int32_t num_b, int32_t num_c,
+                        const int64_t frame_shape[3], const double* pool, int32_t pool_size,
+                        const int32_t* tail_window_ids, int32_t ntail, uint64_t* rng_state, double* out_frames,
+                        int32_t* out_ids, int32_t* out_frames_count, int32_t* out_nids, int32_t io_on_device) {
+  return bp::guarded([&] {
+    if (!frame_shape || !rng_state || !out_frames_count || !out_nids) bp::fail(BP_ERR_CONFIG, "null argument");
+    if (strategy < BP_INIT_COORDINATED || strategy > BP_INIT_REPEAT) bp::fail(BP_ERR_CONFIG, "unknown noise strategy");
+    if (num_b < 1) bp::fail(BP_ERR_CONFIG, "num_b must be >= 1");
+    if (num_c < 0 || num_c % 2 != 0) bp::fail(BP_ERR_CONFIG, "num_c must be even and >= 0");
+    if (pool_size != num_b + num_c / 2) bp::fail(BP_ERR_CONFIG, "pool must hold num_b + num_c/2 entries");
+    if (ntail < 0 || (ntail > 0 && !tail_window_ids)) bp::fail(BP_ERR_CONFIG, "bad tail window");
+    const int64_t per = frame_shape[0] * frame_shape[1] * frame_shape[2];
+    if (per < 0) bp::fail(BP_ERR_DIMENSION, "negative frame shape");
+    bp::require_device(device);
+    bp::HostRng rng(*rng_state);
+    const std::vector<int> window(tail_window_ids, tail_window_ids + ntail);
+    bp::NoiseIds n = bp::draw_noise_ids(strategy, first != 0, num_b, num_c, window, per, rng);
+    const int64_t count = static_cast<int64_t>(n.frames) * per;
+    if (n.fresh) {  // rng.normal_tensor({frames, H, W, C}) (noise.cpp:118-122, 142-148)
+      bp::DevBuf tmp;
+      double* dst = out_frames;
+      if (!io_on_device) {
+        tmp.alloc(static_cast<size_t>(count) * 8 + 8);
+        dst = tmp.as<double>();
+      }
+      bp::launch_normal_fill(n.fresh_state, count, 1.0, dst, nullptr);
+      BP_CUDA(cudaDeviceSynchronize());
+      if (!io_on_device && count > 0)
+        BP_CUDA(cudaMemcpy(out_frames, dst, static_cast<size_t>(count) * 8, cudaMemcpyDeviceToHost));
+    } else {
+      if (!pool) bp::fail(BP_ERR_CONFIG, "null pool");
+      gather_block(pool, pool_size, per, std::vector<int32_t>(n.ids.begin(), n.ids.end()), out_frames,
+                   io_on_device != 0);
+    }
+    if (out_ids)
+      for (size_t i = 0; i < n.ids.size(); ++i) out_ids[i] = n.ids[i];
+    *out_frames_count = n.frames;
+    *out_nids = static_cast<int32_t>(n.ids.size());
+    *rng_state = rng.state;
+  });
+}
+
 bp_status bp_stage_create(int32_t device, const bp_model_desc* model, uint64_t seed_model,
                           uint64_t seed_context, int32_t layer_begin, int32_t layer_end, int32_t precision,
                           bp_stage** out) {
@@ -316,6 +393,21 @@ bp_status bp_matmul(int32_t device, const double* a, const double* b, int64_t m,
                                      dc, n, bp::kEpiNone, nullptr, 0, nullptr);
     }
     HostOp::out(out, dc, m * n);
+  });
+}
+
+bp_status bp_elementwise(int32_t device, int32_t op, const double* a, const double* b, int64_t n, double s,
+                         double* out) {
+  return bp::guarded([&] {
+    if (op < 0 || op > 2) bp::fail(BP_ERR_CONFIG, "elementwise op must be 0 (add), 1 (sub) or 2 (scale)");
+    if (n < 0) bp::fail(BP_ERR_DIMENSION, "negative count");
+    bp::require_device(device);
+    HostOp o;
+    const double* da = o.in(a, n);
+    const double* db = op == 2 ? nullptr : o.in(b, n);
+    double* dc = o.scratch(n);
+    bp::launch_elementwise(op, da, db, n, s, dc, nullptr);
+    HostOp::out(out, dc, n);
   });
 }
 

@@ -90,6 +90,8 @@ struct GatherSegs {
 void launch_normal_fill(uint64_t state, int64_t n, double sigma, double* out, cudaStream_t st);
 void launch_pool_differs(const double* pool, int m, int64_t per, int* differs, cudaStream_t st);
 void launch_gather_rows(const GatherSegs& segs, int64_t cols, double* dst, cudaStream_t st);
+void launch_gather_ids(const double* pool, int64_t per, const int32_t* ids, int n, double* out, cudaStream_t st);
+void launch_elementwise(int op, const double* a, const double* b, int64_t n, double s, double* out, cudaStream_t st);
 template <typename TE>
 void launch_scheduler_step(const double* x, const TE* eps, int64_t n, int steps, double* out,
                            cudaStream_t st);

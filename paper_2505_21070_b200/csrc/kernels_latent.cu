@@ -78,6 +78,41 @@ void launch_gather_rows(const GatherSegs& segs, int64_t cols, double* dst, cudaS
   count_launch();
 }
 
+// stack_entries (noise.cpp:12-22) for an arbitrary id list: out[i] = pool[ids[i]].
+__global__ void k_gather_ids(const double* __restrict__ pool, int64_t per, const int32_t* __restrict__ ids, int n,
+                             double* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(n) * per;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t i = e / per;
+    out[e] = pool[static_cast<int64_t>(ids[i]) * per + (e - i * per)];
+  }
+}
+
+void launch_gather_ids(const double* pool, int64_t per, const int32_t* ids, int n, double* out, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(n) * per;
+  if (total <= 0) return;
+  const int64_t want = (total + 255) / 256;
+  k_gather_ids<<<static_cast<int>(want < kNumSms * 8 ? want : kNumSms * 8), 256, 0, st>>>(pool, per, ids, n, out);
+  count_launch();
+}
+
+// add / sub / scale (tensor.cpp:148-172): one IEEE operation per element, as
+// the reference (out = a; out op= b), so results are bitwise the reference's.
+__global__ void k_elementwise(int op, const double* __restrict__ a, const double* __restrict__ b, int64_t n, double s,
+                              double* __restrict__ out) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = op == 0 ? __dadd_rn(a[i], b[i]) : op == 1 ? __dsub_rn(a[i], b[i]) : __dmul_rn(a[i], s);
+}
+
+void launch_elementwise(int op, const double* a, const double* b, int64_t n, double s, double* out, cudaStream_t st) {
+  if (n <= 0) return;
+  const int64_t want = (n + 255) / 256;
+  k_elementwise<<<static_cast<int>(want < kNumSms * 8 ? want : kNumSms * 8), 256, 0, st>>>(op, a, b, n, s, out);
+  count_launch();
+}
+
 // scheduler_step (model.cpp:338-345): x - eps * (1/steps), exactly the
 // reference's two roundings (scale, then sub). eps is the center rows of the
 // last stage's output, converted to fp64.

@@ -156,7 +156,6 @@ Schedule build_schedule(const bp_pipeline_desc& d) {
   const int T = d.steps;
   const int B = d.block_num;
   const int ctx = d.num_c / 2;
-  const int M = d.num_b + ctx;  // pool size (noise.cpp:35)
   const int64_t tpf = static_cast<int64_t>(d.model.height) * d.model.width;
   const int64_t hwc = tpf * d.model.channels;
   const bool reverse = d.order == BP_ORDER_REVERSE;

@@ -269,14 +269,6 @@ Tensor scheduler_step(const Tensor& x_t, const Tensor& eps_t, int level, int ste
 }
 
 // ---------------------------------------------------------------- queue / noise
-void QueueParams::validate() const {
-  if (num_b < 1) throw ConfigError("num_b must be >= 1");
-  if (num_c < 0 || num_c % 2 != 0) throw ConfigError("num_c must be even and >= 0");
-  if (num_c / 2 > num_b) throw ConfigError("num_c/2 must not exceed num_b");
-  if (steps < 1) throw ConfigError("steps must be >= 1");
-  if (block_num < 1) throw ConfigError("block_num must be >= 1");
-}
-
 NoisePool build_pool(int num_b, int num_c, std::vector<int64_t> frame_shape, uint64_t noise_seed) {
   if (frame_shape.size() != 3) throw DimensionError("frame_shape must be [H, W, C]");
   NoisePool p;

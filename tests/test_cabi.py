@@ -64,6 +64,11 @@ def test_compute_entry_points_fail_loudly_without_gpu(bp):
         bp.normals(1, 10)
     with pytest.raises(bp.CudaError):
         bp.run_pipeline({"devices": 1})
+    import numpy as np
+    with pytest.raises(bp.CudaError):
+        bp.gather_block(np.zeros((6, 1, 1, 1)), [0])
+    with pytest.raises(bp.CudaError):
+        bp.draw_first_block("coordinated", np.zeros((6, 1, 1, 1)), 4, 4, 1)
     import _blockpipe
     import numpy as np
     for fn in (lambda: _blockpipe.matmul(np.eye(2), np.eye(2)), lambda: _blockpipe.softmax_rows(np.eye(2)),

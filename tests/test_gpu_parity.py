@@ -253,3 +253,53 @@ def test_wan_size_invariants(bp):
     assert np.isfinite(a).all()
     assert np.array_equal(a, b)
     assert np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("strategy", ["coordinated", "complete-shuffle", "subset", "fresh", "repeat"])
+def test_noise_draws_vs_reference(bp, ref, strategy):
+    """draw_first_block + 6 x draw_next_block (noise.cpp:135-178) through
+    bp_noise_draw against the reference's own draws: ids and the append
+    stream bit-exact, frames bitwise (stacked pool entries, or fresh normals)."""
+    num_b, num_c, shape, seed = 8, 8, (3, 4, 2), 5
+    want = ref.noise_walk_frames(strategy, 6, num_b, num_c, shape, seed)
+    pool = bp.build_pool(num_b, num_c, shape, seed)
+    got = [bp.draw_first_block(strategy, pool, num_b, num_c, bp.derive_seed(seed, [1]))]
+    for _ in range(6):
+        ids = got[-1]["noise_ids"]
+        window = ids[-(num_c // 2):] if len(ids) >= num_c // 2 else []
+        got.append(bp.draw_next_block(strategy, pool, num_b, num_c, window, got[-1]["rng_state"]))
+    for g, (ids, frames) in zip(got, want):
+        assert g["noise_ids"] == ids
+        assert np.array_equal(g["frames"], frames)
+
+
+def test_gather_block_and_window_errors(bp):
+    pool = bp.build_pool(4, 4, (2, 3, 2), 9)
+    assert np.array_equal(bp.gather_block(pool, [5, 0, 5]), pool[[5, 0, 5]])
+    with pytest.raises(bp.QueueError):
+        bp.gather_block(pool, [6])
+    for bad in ([1, 1], [1], [1, 99]):  # noise.cpp:79-90
+        with pytest.raises(bp.QueueError):
+            bp.draw_next_block("coordinated", pool, 4, 4, bad, 3)
+
+
+@pytest.mark.parametrize("prec,tol", [("f64", 1e-12), ("bf16", 2e-2)])
+def test_capture_size_change_uses_intact_cache(bp, ref, prec, tol):
+    """A pass that consumes a resident 2-frame cache while capturing 4 frames
+    (and the pass after it, on that 4-frame cache) over 3 layers: the new
+    capture must not overwrite cached K/V of a later layer before that layer
+    reads it (the reference keeps the two entries apart, model.cpp:302-324)."""
+    cfg = bp.PipelineConfig(layers=3, hidden=128, heads=1, channels=4, height=2, width=4, context_len=8)
+    rng = np.random.default_rng(8)
+    xs = [rng.standard_normal((6 * 8, 4)) for _ in range(3)]
+    lv, ids = [7] * 6, list(range(6))
+    st = bp.Stage(cfg, 3, 0, 3, 4, precision=prec)
+    rc = ref.RefChunk(cfg, 3, 0, 3, 4)
+    st.forward_chunk(xs[0], lv, ids, capture_frames=[0, 1], mode="on")
+    rc.forward(xs[0], lv, ids, capture=[0, 1], mode="on")
+    a = st.forward_chunk(xs[1], lv, ids, capture_frames=[0, 1, 2, 3], mode="on", use_prev=1)["payload"]
+    b = rc.forward(xs[1], lv, ids, capture=[0, 1, 2, 3], mode="on", use_prev=1)
+    assert rel(a, b) <= tol
+    a = st.forward_chunk(xs[2], lv, ids, mode="on", use_prev=1)["payload"]
+    b = rc.forward(xs[2], lv, ids, mode="on", use_prev=1)
+    assert rel(a, b) <= tol
