@@ -121,3 +121,36 @@ def test_attention_bench(lib):
         assert lib.bp_bench_attn(0, rows, 12, 128, n0, n1, 5, ms) == 0, lib.bp_last_error()
         tf = 4 * rows * (n0 + n1) * 12 * 128 / (ms.value * 1e-3) / 1e12
         print(f"attn q={rows} kv={n0}+{n1}: {ms.value:.3f} ms  {tf:.0f} TFLOP/s")
+
+
+def test_attention_boundary_sweep(lib):
+    """Tile-boundary sweep of the default kernels: rows around the 128-row
+    query tile and the 256-row CTA pair, both key segments around the 64-key
+    tile (self-attention, k_attn_pp2), and the key count alone for the
+    cross-attention launcher (k_attn_pp)."""
+    from kernels import attn_cross
+    dh, heads = 128, 1
+    edges = (63, 64, 65, 127, 128, 129)
+    worst = 0.0
+    for rows in (127, 128, 129, 255, 256, 257):
+        rng = np.random.default_rng(rows)
+        q = to_bf16_bits(rng.standard_normal((rows, dh)))
+        kk = to_bf16_bits(rng.standard_normal((260, dh)))
+        vv = to_bf16_bits(rng.standard_normal((260, dh)))
+        for n0 in edges:
+            for n1 in edges:
+                k0, v0 = np.ascontiguousarray(kk[:n0]), np.ascontiguousarray(vv[:n0])
+                k1, v1 = np.ascontiguousarray(kk[130:130 + n1]), np.ascontiguousarray(vv[130:130 + n1])
+                got = from_bf16_bits(attn(lib, q, k0, v0, k1, v1, heads, dh, 1 / np.sqrt(dh))).astype(np.float64)
+                want = ref_attn(from_bf16_bits(q), from_bf16_bits(np.concatenate([k0, k1])),
+                                from_bf16_bits(np.concatenate([v0, v1])), heads, dh, 1 / np.sqrt(dh))
+                r = np.linalg.norm(got - want) / np.linalg.norm(want)
+                worst = max(worst, r)
+                assert r < 1e-2, (rows, n0, n1, r)
+        for n1 in edges:
+            k1, v1 = np.ascontiguousarray(kk[:n1]), np.ascontiguousarray(vv[:n1])
+            got = from_bf16_bits(attn_cross(lib, q, k1, v1, heads, dh, 1 / np.sqrt(dh))).astype(np.float64)
+            want = ref_attn(from_bf16_bits(q), from_bf16_bits(k1), from_bf16_bits(v1), heads, dh, 1 / np.sqrt(dh))
+            r = np.linalg.norm(got - want) / np.linalg.norm(want)
+            assert r < 1e-2, (rows, n1, r)
+    print("worst rel-L2", worst)
