@@ -235,6 +235,15 @@ struct PipelineConfig {
   bool fault_inject_ulp = false, record_trace = false, check_cache = false;
   Transport transport = Transport::kLoopback;  // extension
   bool uneven_split = false;                   // extension
+  // Extension, multi-process transports (kNccl / kIpc, one process per
+  // stage): this process's rank in [0, world), world == devices; the ranks
+  // rendezvous through files in bootstrap_dir (a fresh directory every rank
+  // sees). run_pipeline then returns the blocks on rank 0 only (the other
+  // ranks' RunResult carries the schedule, no frames). kLoopback runs every
+  // stage in this process on model.device.
+  int rank = 0, world = 1;
+  std::string bootstrap_dir;
+  int bootstrap_timeout_ms = 120000;
   void validate() const;
 };
 

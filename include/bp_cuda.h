@@ -266,6 +266,17 @@ BP_API bp_status bp_nccl_unique_id(uint8_t out[128]);
 BP_API bp_status bp_pipeline_create(const bp_pipeline_desc* desc, int32_t rank, int32_t world,
                              int32_t device, const uint8_t* nccl_ids, bp_pipeline** out);
 BP_API bp_status bp_pipeline_destroy(bp_pipeline* p);
+/* File rendezvous for the multi-process transports, no MPI / PyTorch needed:
+ * every rank passes the same fresh directory (on a filesystem all ranks
+ * see). bp_bootstrap_nccl_ids: rank 0 creates the `world` NCCL unique ids
+ * (ncclGetUniqueId) and publishes them; every rank receives them in ids_out
+ * (world x 128 bytes) for bp_pipeline_create. bp_bootstrap_ipc: publishes
+ * this rank's IPC handle, waits for every rank's and connects (the
+ * bp_ipc_handle + bp_ipc_connect exchange). Both block up to timeout_ms and
+ * fail with BP_ERR_IO. */
+BP_API bp_status bp_bootstrap_nccl_ids(const char* dir, int32_t rank, int32_t world, int32_t timeout_ms,
+                                       uint8_t* ids_out);
+BP_API bp_status bp_bootstrap_ipc(bp_pipeline* p, const char* dir, int32_t rank, int32_t world, int32_t timeout_ms);
 /* IPC transport handshake: each rank exports the handle of its receive block
  * (64 bytes), the caller all-gathers them in rank order, then every rank
  * connects before its first run. */
@@ -297,6 +308,9 @@ typedef struct {
   int64_t ln_launches;
   int64_t h2d_bytes;        /* host->device bytes of the last run (host-supplied pool) */
   int64_t d2h_bytes;        /* device->host bytes of the last run (emitted latents)   */
+  int64_t boundary_copies;  /* device copies of hidden states at stage boundaries in the last
+                               run (0 for the multi-process transports: received in place) */
+  int64_t registered_buffers; /* stage-boundary buffers NCCL accepted for registration */
 } bp_pipeline_stats;
 BP_API bp_status bp_pipeline_get_stats(bp_pipeline* p, bp_pipeline_stats* out);
 /* Per-kernel-class timing with CUDA events on the launching stream (0/1). */

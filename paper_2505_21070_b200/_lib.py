@@ -75,7 +75,8 @@ class PipelineStats(C.Structure):
     _fields_ = [("gpu_ms", f64), ("passes", i64), ("kernel_launches", i64), ("peak_bytes", i64),
                 ("boundary_bytes", i64), ("attn_ms", f64), ("gemm_ms", f64), ("cross_ms", f64),
                 ("attn_launches", i64), ("gemm_launches", i64), ("cross_launches", i64),
-                ("ln_ms", f64), ("ln_launches", i64), ("h2d_bytes", i64), ("d2h_bytes", i64)]
+                ("ln_ms", f64), ("ln_launches", i64), ("h2d_bytes", i64), ("d2h_bytes", i64),
+                ("boundary_copies", i64), ("registered_buffers", i64)]
 
 
 EMIT_FN = C.CFUNCTYPE(None, C.c_void_p, i64, i64, P(f64), P(i32), i32, P(i64))
@@ -122,6 +123,8 @@ _SIGS = {
     "bp_pipeline_create": (i32, [P(PipelineDesc), i32, i32, i32, P(C.c_uint8), P(C.c_void_p)]),
     "bp_pipeline_destroy": (i32, [C.c_void_p]),
     "bp_ipc_handle": (i32, [C.c_void_p, P(C.c_uint8)]),
+    "bp_bootstrap_nccl_ids": (i32, [C.c_char_p, i32, i32, i32, P(C.c_uint8)]),
+    "bp_bootstrap_ipc": (i32, [C.c_void_p, C.c_char_p, i32, i32, i32]),
     "bp_ipc_connect": (i32, [C.c_void_p, P(C.c_uint8)]),
     "bp_ipc_counters": (i32, [C.c_void_p, P(C.c_uint32)]),
     "bp_pipeline_run": (i32, [C.c_void_p, EMIT_FN, C.c_void_p]),

@@ -345,28 +345,41 @@ class Pipeline:
 
     def __init__(self, config: ConfigLike, rank: int = 0, world: int = 1, device: int = 0,
                  nccl_ids: Optional[bytes] = None,
-                 ipc_exchange: Optional[Callable[[bytes], Sequence[bytes]]] = None):
-        """nccl_ids: world x 128-byte NCCL unique ids (transport "nccl").
-        ipc_exchange: all-gathers this rank's 64-byte IPC handle and returns
-        every rank's handle in rank order (transport "ipc", world > 1)."""
+                 ipc_exchange: Optional[Callable[[bytes], Sequence[bytes]]] = None,
+                 bootstrap_dir: Optional[str] = None, bootstrap_timeout_ms: int = 120000):
+        """Multi-process transports (one process per stage, world = devices):
+        either bootstrap_dir -- a fresh directory every rank can see; the ranks
+        rendezvous through files there (bp_bootstrap_nccl_ids /
+        bp_bootstrap_ipc), no other runtime needed -- or the caller's own
+        exchange: nccl_ids (world x 128-byte NCCL unique ids, transport
+        "nccl") / ipc_exchange (all-gathers this rank's 64-byte IPC handle and
+        returns every rank's in rank order, transport "ipc")."""
         self.cfg = _cfg(config)
         self._h = C.c_void_p()
         desc = self.cfg.to_desc()
+        multi = world > 1 and self.cfg.transport in ("nccl", "ipc")
+        if multi and bootstrap_dir is not None and self.cfg.transport == "nccl" and nccl_ids is None:
+            got = (C.c_uint8 * (128 * world))()
+            check(lib.bp_bootstrap_nccl_ids(bootstrap_dir.encode(), rank, world, bootstrap_timeout_ms, got))
+            nccl_ids = bytes(got)
         ids = None
         if nccl_ids is not None:
             buf = (C.c_uint8 * len(nccl_ids)).from_buffer_copy(nccl_ids)
             ids = C.cast(buf, C.POINTER(C.c_uint8))
         check(lib.bp_pipeline_create(C.byref(desc), rank, world, device, ids, C.byref(self._h)))
         if self.cfg.transport == "ipc" and world > 1:
-            if ipc_exchange is None:
-                raise errors.ConfigError("transport 'ipc' needs ipc_exchange to share the ranks' handles")
-            mine = (C.c_uint8 * 64)()
-            check(lib.bp_ipc_handle(self._h, mine))
-            allh = b"".join(bytes(h) for h in ipc_exchange(bytes(mine)))
-            if len(allh) != 64 * world:
-                raise errors.ConfigError("ipc_exchange must return one 64-byte handle per rank")
-            hb = (C.c_uint8 * len(allh)).from_buffer_copy(allh)
-            check(lib.bp_ipc_connect(self._h, hb))
+            if bootstrap_dir is not None and ipc_exchange is None:
+                check(lib.bp_bootstrap_ipc(self._h, bootstrap_dir.encode(), rank, world, bootstrap_timeout_ms))
+            else:
+                if ipc_exchange is None:
+                    raise errors.ConfigError("transport 'ipc' needs ipc_exchange or bootstrap_dir to share handles")
+                mine = (C.c_uint8 * 64)()
+                check(lib.bp_ipc_handle(self._h, mine))
+                allh = b"".join(bytes(h) for h in ipc_exchange(bytes(mine)))
+                if len(allh) != 64 * world:
+                    raise errors.ConfigError("ipc_exchange must return one 64-byte handle per rank")
+                hb = (C.c_uint8 * len(allh)).from_buffer_copy(allh)
+                check(lib.bp_ipc_connect(self._h, hb))
         self.schedule = Schedule(self.cfg)
 
     def close(self):

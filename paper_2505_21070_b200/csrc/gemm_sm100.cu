@@ -15,6 +15,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -483,12 +484,15 @@ struct MapKeyHash {
 };
 std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
+std::atomic<int> g_sm_reserve{0};
+
 template <int EPI, bool kCg2 = false>
 void launch_pair(const CUtensorMap& ma, const CUtensorMap& mbh, int M, int N, int K, void* C, int64_t ldc,
                  const CUtensorMap& mc, cudaStream_t st) {
   set_smem_attr(k_gemm_pair<EPI, kCg2>, PairLayout<kCg2>::kSmem);
   const int pairs = (((M + BM - 1) / BM + 1) / 2) * ((N + BN - 1) / BN);
-  const int clusters = pairs < kNumSms / 2 ? pairs : kNumSms / 2;
+  const int avail = (kNumSms - g_sm_reserve.load(std::memory_order_relaxed)) / 2;
+  const int clusters = pairs < avail ? pairs : avail;
   launch_pdl(k_gemm_pair<EPI, kCg2>, dim3(2 * clusters), dim3(kThreads), PairLayout<kCg2>::kSmem, st, ma, mbh, M, N, K,
              C, ldc, mc);
 }
@@ -563,6 +567,12 @@ static const CUtensorMap& cached_map_f32(const void* p, uint64_t rows, uint64_t 
   make_tmap_2d_f32(&m, p, rows, cols, ld, br, bc);
   return g_maps.emplace(k, m).first->second;
 }
+
+void set_sm_reserve(int sms) {
+  if (sms < 0 || sms > kNumSms - 2) fail(BP_ERR_CONFIG, "SM reservation out of range");
+  g_sm_reserve.store(sms);
+}
+int sm_reserve() { return g_sm_reserve.load(); }
 
 void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C, int64_t ldc, int epi,
                     cudaStream_t st, int variant) {

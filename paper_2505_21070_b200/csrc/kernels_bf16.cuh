@@ -37,6 +37,12 @@ void launch_gemm_bf16(const bf16* A, int64_t lda, const bf16* W, int M, int N, i
                       int64_t ldc, int epi, cudaStream_t st);
 // Which GEMM implementation launch_gemm_bf16 uses: 1 = tcgen05 (default), 0 = SIMT check path.
 void set_gemm_impl(int impl);
+// SMs the persistent GEMM grids leave free (0 by default): the NCCL executor
+// reserves a few for NCCL's send/recv kernels, which cannot co-reside with a
+// ~200 KB-smem GEMM CTA -- a receive kernel parked on an SM would otherwise
+// hold back one cluster's whole tile stream until its data arrives.
+void set_sm_reserve(int sms);
+int sm_reserve();
 int gemm_impl();
 
 struct AttnBf16Args {

@@ -21,6 +21,11 @@ struct NcclApi {
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // user-buffer API (NCCL >= 2.19); null when the loaded NCCL lacks it
+  ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+  ncclResult_t (*MemFree)(void*) = nullptr;
+  ncclResult_t (*CommRegister)(ncclComm_t, void*, size_t, void**) = nullptr;
+  ncclResult_t (*CommDeregister)(ncclComm_t, void*) = nullptr;
 };
 
 inline const NcclApi& nccl() {
@@ -44,6 +49,10 @@ inline const NcclApi& nccl() {
     api.Send = reinterpret_cast<decltype(api.Send)>(dlsym(h, "ncclSend"));
     api.Recv = reinterpret_cast<decltype(api.Recv)>(dlsym(h, "ncclRecv"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    api.MemAlloc = reinterpret_cast<decltype(api.MemAlloc)>(dlsym(h, "ncclMemAlloc"));
+    api.MemFree = reinterpret_cast<decltype(api.MemFree)>(dlsym(h, "ncclMemFree"));
+    api.CommRegister = reinterpret_cast<decltype(api.CommRegister)>(dlsym(h, "ncclCommRegister"));
+    api.CommDeregister = reinterpret_cast<decltype(api.CommDeregister)>(dlsym(h, "ncclCommDeregister"));
   });
   if (!api.Send) fail(BP_ERR_NCCL, "NCCL unavailable: " + err);
   return api;

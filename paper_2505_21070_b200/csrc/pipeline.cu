@@ -9,6 +9,10 @@
 #include "nccl_dl.hpp"
 
 #include <algorithm>
+#include <string>
+#include <unistd.h>
+#include <thread>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -16,6 +20,7 @@
 #include <vector>
 
 #include "device.cuh"
+#include "kernels_bf16.cuh"
 #include "kernels_simt.cuh"
 #include "schedule.hpp"
 #include "stage.hpp"
@@ -71,10 +76,23 @@ class Pipeline {
   // NCCL
   ncclComm_t comm_prev_ = nullptr, comm_next_ = nullptr, comm_eps_ = nullptr;
   cudaStream_t s_recv_ = nullptr, s_send_ = nullptr, s_eps_ = nullptr;
-  DevBuf rbuf_[2], ebuf_[2];
+  DevBuf ebuf_[2];
+  // Stage-boundary ring (multi-process): the local stage's residual stream
+  // has kRing slots; a pass receives into its slot, runs every layer in place
+  // and is sent from the same slot, so no device copies sit on the boundary.
+  // NCCL: slots from ncclMemAlloc, registered with the channels' comms where
+  // NCCL accepts it (zero-copy P2P over NVLink); IPC: the slots of ranks > 0
+  // ARE the exported receive ring the predecessor's peer copies land in.
+  static constexpr int kRing = 3;
+  void* alloc_ring_buffer(size_t bytes);
+  void register_buffer(ncclComm_t comm, void* p, size_t bytes);
+  std::vector<DevBuf> own_ring_;
+  std::vector<void*> nccl_mem_;
+  std::vector<std::pair<ncclComm_t, void*>> nccl_regs_;
+  int64_t registered_ = 0;
 
  public:
-  // IPC transport: this rank's exported block = [hidden ring: 2 slots]
+  // IPC transport: this rank's exported block = [hidden ring: kRing slots]
   // [eps ring: 2 slots][counters]; the same layout on every rank.
   //   cnt[0] hidden passes delivered into my ring (written by rank - 1)
   //   cnt[1] eps passes delivered into my eps ring (rank 0; written by N - 1)
@@ -88,11 +106,12 @@ class Pipeline {
  private:
   bool multi() const { return d_.transport != BP_TRANSPORT_LOOPBACK && d_.devices > 1; }
   bool ipc() const { return d_.transport == BP_TRANSPORT_IPC && d_.devices > 1; }
+  // hidden ring: kRing slots (slot i % kRing); eps ring: 2 slots (i & 1)
   char* ipc_slot(char* block, int which, int64_t i) const {
-    return block + (which == 0 ? 0 : 2 * ipc_hid_) + (i & 1) * (which == 0 ? ipc_hid_ : ipc_eps_);
+    return which == 0 ? block + (i % kRing) * ipc_hid_ : block + kRing * ipc_hid_ + (i & 1) * ipc_eps_;
   }
   uint32_t* ipc_cnt(char* block, int k) const {
-    return reinterpret_cast<uint32_t*>(block + 2 * ipc_hid_ + 2 * ipc_eps_) + k;
+    return reinterpret_cast<uint32_t*>(block + kRing * ipc_hid_ + 2 * ipc_eps_) + k;
   }
   void ipc_send(char* peer, int which, int64_t i, const void* src, size_t bytes, cudaStream_t s);
   void ipc_wait_delivered(int which, int64_t i, cudaStream_t s);
@@ -212,6 +231,10 @@ Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, c
     // non-zero ranks need the per-pass frame metadata only on stage 0 (rank 0)
   }
   if (d.transport == BP_TRANSPORT_NCCL && N > 1) {
+    // NCCL's p2p kernels (a send, a receive, rank 0's eps receive) need SMs
+    // the persistent GEMMs do not hold (BP_SM_RESERVE overrides the 4)
+    const char* res = std::getenv("BP_SM_RESERVE");
+    set_sm_reserve(res ? std::atoi(res) : 4);
     auto id_of = [&](int k) {
       ncclUniqueId u;
       std::memcpy(&u, ids + 128 * k, sizeof(u));
@@ -225,11 +248,26 @@ Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, c
     BP_CUDA(cudaStreamCreateWithFlags(&s_recv_, cudaStreamNonBlocking));
     BP_CUDA(cudaStreamCreateWithFlags(&s_send_, cudaStreamNonBlocking));
     BP_CUDA(cudaStreamCreateWithFlags(&s_eps_, cudaStreamNonBlocking));
-    const Stage& s = *stages_[static_cast<size_t>(rank_)];
+    Stage& s = *stages_[static_cast<size_t>(rank_)];
     const size_t hid = static_cast<size_t>(sched.max_tokens) * d.model.hidden * s.act_bytes();
     const size_t eps = static_cast<size_t>(sched.max_tokens) * C_ * s.eps_bytes();
-    if (rank_ > 0) { rbuf_[0].alloc(hid); rbuf_[1].alloc(hid); }
-    if (rank_ == 0) { ebuf_[0].alloc(eps); ebuf_[1].alloc(eps); }
+    std::vector<void*> xs, es;
+    for (int k = 0; k < kRing; ++k) {
+      xs.push_back(alloc_ring_buffer(hid));
+      if (comm_prev_) register_buffer(comm_prev_, xs.back(), hid);  // receives land here
+      if (comm_next_) register_buffer(comm_next_, xs.back(), hid);  // and are sent on from here
+      if (s.is_last()) {
+        es.push_back(alloc_ring_buffer(eps));
+        register_buffer(comm_eps_, es.back(), eps);
+      }
+    }
+    s.set_ring(kRing, sched.max_tokens, xs, es);
+    if (rank_ == 0) {
+      for (int k = 0; k < 2; ++k) {
+        ebuf_[k].alloc(eps);
+        register_buffer(comm_eps_, ebuf_[k].p, eps);
+      }
+    }
     // Connect every channel now, in an order with no cycle. NCCL connects a
     // point-to-point pair lazily at its first operation and blocks until the
     // peer takes part; the run's first operations are receives on BOTH ends
@@ -260,12 +298,21 @@ Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, c
     BP_CUDA(cudaStreamCreateWithFlags(&s_recv_, cudaStreamNonBlocking));
     BP_CUDA(cudaStreamCreateWithFlags(&s_send_, cudaStreamNonBlocking));
     BP_CUDA(cudaStreamCreateWithFlags(&s_eps_, cudaStreamNonBlocking));
-    const Stage& s = *stages_[static_cast<size_t>(rank_)];
+    Stage& s = *stages_[static_cast<size_t>(rank_)];
     auto align256 = [](size_t n) { return (n + 255) & ~static_cast<size_t>(255); };
     ipc_hid_ = align256(static_cast<size_t>(sched.max_tokens) * d.model.hidden * s.act_bytes());
     ipc_eps_ = align256(static_cast<size_t>(sched.max_tokens) * C_ * s.eps_bytes());
-    ipc_block_.alloc(2 * ipc_hid_ + 2 * ipc_eps_ + 256);
+    ipc_block_.alloc(kRing * ipc_hid_ + 2 * ipc_eps_ + 256);
     BP_CUDA(cudaMemset(ipc_cnt(ipc_block_.as<char>(), 0), 0, 256));
+    std::vector<void*> xs, es;
+    for (int k = 0; k < kRing; ++k) {
+      // ranks > 0 run their layers in the receive slots themselves; rank 0
+      // (whose input is the embedding) keeps its own residual ring
+      xs.push_back(rank_ > 0 ? static_cast<void*>(ipc_slot(ipc_block_.as<char>(), 0, k))
+                             : alloc_ring_buffer(ipc_hid_));
+      if (s.is_last()) es.push_back(alloc_ring_buffer(ipc_eps_));
+    }
+    stages_[static_cast<size_t>(rank_)]->set_ring(kRing, sched.max_tokens, xs, es);
   }
   BP_CUDA(cudaDeviceSynchronize());
 }
@@ -273,8 +320,13 @@ Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, c
 Pipeline::~Pipeline() {
   cudaSetDevice(device_);
   cudaDeviceSynchronize();
+  if (d_.transport == BP_TRANSPORT_NCCL && d_.devices > 1) set_sm_reserve(0);
   for (char* q : opened_) cudaIpcCloseMemHandle(q);
   for (double* h : pinned_) cudaFreeHost(h);
+  stages_.clear();  // the stages' rings may live in the buffers released below
+  for (auto& r : nccl_regs_) bp::nccl().CommDeregister(r.first, r.second);
+  for (void* q : nccl_mem_) bp::nccl().MemFree(q);
+  own_ring_.clear();
   if (comm_prev_) bp::nccl().CommDestroy(comm_prev_);
   if (comm_next_) bp::nccl().CommDestroy(comm_next_);
   if (comm_eps_) bp::nccl().CommDestroy(comm_eps_);
@@ -472,21 +524,22 @@ static const bool g_ipc_trace = std::getenv("BP_IPC_TRACE") != nullptr;
 static_assert(sizeof(long long) == 8, "");
 void Pipeline::ipc_send(char* peer, int which, int64_t i, const void* src, size_t bytes, cudaStream_t s) {
   if (g_ipc_trace) std::fprintf(stderr, "[rank %d] send ch%d pass %lld (%zu B)\n", rank_, which, static_cast<long long>(i), bytes);
-  // slot i & 1 is free once pass i - 2 is released; the first two passes of a
-  // run wait until every pass of the previous run is released (the receiver
-  // may still be finishing it when this rank starts the next run)
+  // the slot of pass i is free once pass i - R is released (R = kRing hidden
+  // slots, 2 eps slots); the first R passes of a run wait until every pass of
+  // the previous run is released (the receiver may still be finishing it)
   const uint32_t base = ipc_epoch_;
+  const int64_t R = which == 0 ? kRing : 2;
   stream_wait_geq(s, ipc_cnt(ipc_block_.as<char>(), which == 0 ? 2 : 3),
-                  i >= 2 ? base + static_cast<uint32_t>(i - 1) : base);
+                  i >= R ? base + static_cast<uint32_t>(i - R + 1) : base);
   BP_CUDA(cudaMemcpyAsync(ipc_slot(peer, which, i), src, bytes, cudaMemcpyDeviceToDevice, s));
   stream_write(s, ipc_cnt(peer, which == 0 ? 0 : 1), base + static_cast<uint32_t>(i + 1));
 }
-// Receiver side: pass i has landed in my slot i & 1.
+// Receiver side: pass i has landed in my slot of it.
 void Pipeline::ipc_wait_delivered(int which, int64_t i, cudaStream_t s) {
   if (g_ipc_trace) std::fprintf(stderr, "[rank %d] recv ch%d pass %lld\n", rank_, which, static_cast<long long>(i));
   stream_wait_geq(s, ipc_cnt(ipc_block_.as<char>(), which == 0 ? 0 : 1), ipc_epoch_ + static_cast<uint32_t>(i + 1));
 }
-// Receiver side: slot i & 1 has been consumed (stream-ordered after its use).
+// Receiver side: pass i's slot has been consumed (stream-ordered after its use).
 void Pipeline::ipc_release(char* peer, int which, int64_t i, cudaStream_t s) {
   stream_write(s, ipc_cnt(peer, which == 0 ? 2 : 3), ipc_epoch_ + static_cast<uint32_t>(i + 1));
 }
@@ -523,6 +576,12 @@ void Pipeline::run(bp_emit_fn emit, void* user) {
 
 void Pipeline::run_rank0_loopback(bp_emit_fn emit, void* user) {
   cudaStream_t st = st_;
+  auto copies = [&] {
+    int64_t c = 0;
+    for (auto& sp : stages_) c += sp ? sp->input_copies() : 0;
+    return c;
+  };
+  const int64_t copies_at_start = copies();
   cudaEvent_t e0, e1;
   BP_CUDA(cudaEventCreate(&e0));
   BP_CUDA(cudaEventCreate(&e1));
@@ -559,6 +618,8 @@ void Pipeline::run_rank0_loopback(bp_emit_fn emit, void* user) {
   BP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   stats.gpu_ms = ms;
   stats.boundary_bytes = boundary;
+  stats.boundary_copies = copies() - copies_at_start;
+  stats.registered_buffers = 0;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (emit) {
@@ -570,11 +631,47 @@ void Pipeline::run_rank0_loopback(bp_emit_fn emit, void* user) {
   }
 }
 
+void* Pipeline::alloc_ring_buffer(size_t bytes) {
+  if (d_.transport == BP_TRANSPORT_NCCL && bp::nccl().MemAlloc && bp::nccl().MemFree) {
+    void* q = nullptr;
+    if (bp::nccl().MemAlloc(&q, bytes) == ncclSuccess && q) {
+      nccl_mem_.push_back(q);
+      const int64_t now = g_dev_bytes.fetch_add(static_cast<int64_t>(bytes)) + static_cast<int64_t>(bytes);
+      int64_t peak = g_dev_peak.load();
+      while (now > peak && !g_dev_peak.compare_exchange_weak(peak, now)) {}
+      return q;
+    }
+  }
+  own_ring_.emplace_back();
+  own_ring_.back().alloc(bytes);
+  return own_ring_.back().p;
+}
+
+// Best effort: NCCL registers user buffers for zero-copy transfers where its
+// transport supports it (NVLink P2P); elsewhere (e.g. the socket transport of
+// the one-GPU tests) the call fails and the transfer goes through NCCL's own
+// staging, with identical results.
+void Pipeline::register_buffer(ncclComm_t comm, void* p, size_t bytes) {
+  if (!comm || !p || d_.transport != BP_TRANSPORT_NCCL || !bp::nccl().CommRegister) return;
+  if (std::find(nccl_mem_.begin(), nccl_mem_.end(), p) == nccl_mem_.end() &&
+      std::getenv("BP_NCCL_REGISTER_ALL") == nullptr)
+    return;  // only cuMem (ncclMemAlloc) buffers qualify for NVLink zero-copy
+  void* h = nullptr;
+  if (bp::nccl().CommRegister(comm, p, bytes, &h) == ncclSuccess && h) {
+    nccl_regs_.push_back({comm, h});
+    ++registered_;
+  }
+}
+
 // One process per GPU. Stream layout per rank: st_ (compute), s_recv_
 // (hidden state from rank-1), s_send_ (hidden state to rank+1), s_eps_
-// (eps return N-1 -> 0). Two-deep buffer rings; every cross-stream edge is an
-// event. Rank 0 orders its compute stream by the logical slot clock so the
-// data dependencies of the ideal schedule are never inverted.
+// (eps return N-1 -> 0); every cross-stream edge is an event. The local
+// stage's residual stream is a kRing-slot ring (see kRing): pass i receives
+// into slot i % kRing, runs its layers in place and is sent from that slot,
+// so the boundary has no device-to-device copies. A slot is reused by pass
+// i + kRing once pass i's send (or, on the last rank, its forward) is done.
+// Rank 0 orders its compute stream by the logical slot clock so the data
+// dependencies of the ideal schedule are never inverted.
 void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
   const int N = d_.devices;
   const int j = rank_;
@@ -584,6 +681,7 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
   const ncclDataType_t adt = abytes == 8 ? ncclFloat64 : ncclFloat32;
   const ncclDataType_t edt = ebytes == 8 ? ncclFloat64 : ncclFloat32;
   const int H = d_.model.hidden;
+  const bool last = s.is_last();
   std::vector<cudaEvent_t> ev_fwd(P), ev_recv(P), ev_sent(P), ev_used(P);
   for (int64_t i = 0; i < P; ++i) {
     BP_CUDA(cudaEventCreateWithFlags(&ev_fwd[i], cudaEventDisableTiming));
@@ -595,29 +693,26 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
   BP_CUDA(cudaEventCreate(&e0));
   BP_CUDA(cudaEventCreate(&e1));
   BP_CUDA(cudaEventRecord(e0, st_));
-  // Stage outputs alternate between two staging copies so a send can
-  // overlap the next forward.
-  DevBuf out_ring[2];
-  const size_t out_bytes = static_cast<size_t>(sched.max_tokens) *
-                           (s.is_last() ? static_cast<size_t>(C_) * ebytes : static_cast<size_t>(H) * abytes);
-  out_ring[0].alloc(out_bytes);
-  out_ring[1].alloc(out_bytes);
+  const int64_t copies_at_start = s.input_copies();
   int64_t boundary = 0;
+  const bool use_ipc = ipc();
+  // the event after which pass i's ring slot may be overwritten: its send
+  // (the slot holds the outgoing hidden state, or the last rank's eps), and
+  // on the last rank also its forward (the x slot is not sent from there)
+  auto slot_free = [&](int64_t i) { return ev_sent[i]; };
 
   auto forward_pass = [&](const SchedPass& p, const void* payload) {
     StageInput in;
     before_stage(p, j, s, &in);
     in.payload = payload;
+    in.slot = static_cast<int>(p.index % kRing);
+    const int64_t i = p.index;
+    if (i >= kRing && (j == 0 || last)) BP_CUDA(cudaStreamWaitEvent(st_, slot_free(i - kRing), 0));
     const void* out = s.forward(in);
     after_stage(p, j, s);
-    const int64_t i = p.index;
-    if (i >= 2) BP_CUDA(cudaStreamWaitEvent(st_, ev_sent[i - 2], 0));  // ring slot free
-    const size_t n = static_cast<size_t>(p.tokens) * (s.is_last() ? C_ * ebytes : H * abytes);
-    BP_CUDA(cudaMemcpyAsync(out_ring[i & 1].p, out, n, cudaMemcpyDeviceToDevice, st_));
     BP_CUDA(cudaEventRecord(ev_fwd[i], st_));
-    return out_ring[i & 1].p;
+    return out;
   };
-  const bool use_ipc = ipc();
   // channel 0: hidden state j -> j+1; channel 1: eps N-1 -> 0
   auto send_to = [&](ncclComm_t comm, cudaStream_t ss, const SchedPass& p, const void* buf, int peer,
                      size_t count, ncclDataType_t dt) {
@@ -633,9 +728,6 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
   };
   auto eps_buf = [&](int64_t i) -> void* {
     return use_ipc ? static_cast<void*>(ipc_slot(ipc_block_.as<char>(), 1, i)) : ebuf_[i & 1].p;
-  };
-  auto hid_buf = [&](int64_t i) -> void* {
-    return use_ipc ? static_cast<void*>(ipc_slot(ipc_block_.as<char>(), 0, i)) : rbuf_[i & 1].p;
   };
 
   if (j == 0) {
@@ -681,44 +773,52 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
       }
     }
   } else {
+    // receive i lands in ring slot i % kRing once pass i - kRing left it:
+    // sent on (middle ranks) or consumed by the forward (last rank, whose
+    // output is the eps slot)
+    auto x_free = [&](int64_t i) { return last ? ev_fwd[i] : ev_sent[i]; };
     auto post_recv = [&](int64_t i) {
       if (i >= P) return;
       const SchedPass& p = sched.passes[static_cast<size_t>(i)];
       if (use_ipc) {
-        if (i >= 2) {  // give slot i & 1 back once forward(i - 2) has copied it in
-          BP_CUDA(cudaStreamWaitEvent(s_recv_, ev_used[i - 2], 0));
-          ipc_release(peer_prev_, 0, i - 2, s_recv_);
+        if (i >= kRing) {  // give slot i % kRing back to the sender
+          BP_CUDA(cudaStreamWaitEvent(s_recv_, x_free(i - kRing), 0));
+          ipc_release(peer_prev_, 0, i - kRing, s_recv_);
         }
         ipc_wait_delivered(0, i, s_recv_);
       } else {
-        if (i >= 2) BP_CUDA(cudaStreamWaitEvent(s_recv_, ev_used[i - 2], 0));
-        BP_NCCL(bp::nccl().Recv(rbuf_[i & 1].p, static_cast<size_t>(p.tokens) * H, adt, 0, comm_prev_, s_recv_));
+        if (i >= kRing) BP_CUDA(cudaStreamWaitEvent(s_recv_, x_free(i - kRing), 0));
+        BP_NCCL(bp::nccl().Recv(s.x_slot(static_cast<int>(i % kRing)), static_cast<size_t>(p.tokens) * H, adt, 0,
+                                comm_prev_, s_recv_));
       }
       BP_CUDA(cudaEventRecord(ev_recv[i], s_recv_));
     };
-    post_recv(0);
-    post_recv(1);
+    // a receive is posted once the event it waits on has been recorded: pass
+    // i + kRing - 1's receive right after pass i - 1's send / forward
+    for (int64_t i = 0; i < std::min<int64_t>(kRing - 1, P); ++i) post_recv(i);
     for (int64_t i = 0; i < P; ++i) {
       const SchedPass& p = sched.passes[static_cast<size_t>(i)];
       BP_CUDA(cudaStreamWaitEvent(st_, ev_recv[i], 0));
-      const void* out = forward_pass(p, hid_buf(i));
-      BP_CUDA(cudaEventRecord(ev_used[i], st_));  // input copied into the stage's residual stream
-      post_recv(i + 2);
-      if (j + 1 < N) {
+      const void* out = forward_pass(p, s.x_slot(static_cast<int>(i % kRing)));
+      BP_CUDA(cudaEventRecord(ev_used[i], st_));
+      if (!last) {
         send_to(comm_next_, s_send_, p, out, 1, static_cast<size_t>(p.tokens) * H, adt);
         boundary += p.tokens * H * static_cast<int64_t>(abytes);
       } else {
         send_to(comm_eps_, s_send_, p, out, use_ipc ? -1 : 1, static_cast<size_t>(p.tokens) * C_, edt);
       }
+      post_recv(i + kRing - 1);
     }
   }
-  if (use_ipc) {  // release the last two slots so the counters line up for the next run
-    for (int64_t i = std::max<int64_t>(0, P - 2); i < P; ++i) {
-      if (j == 0) {
+  if (use_ipc) {  // release the last slots so the counters line up for the next run
+    if (j == 0) {
+      for (int64_t i = std::max<int64_t>(0, P - 2); i < P; ++i) {
         BP_CUDA(cudaStreamWaitEvent(s_eps_, ev_used[i], 0));
         ipc_release(peer_eps_, 1, i, s_eps_);
-      } else {
-        BP_CUDA(cudaStreamWaitEvent(s_recv_, ev_used[i], 0));
+      }
+    } else {
+      for (int64_t i = std::max<int64_t>(0, P - kRing); i < P; ++i) {
+        BP_CUDA(cudaStreamWaitEvent(s_recv_, last ? ev_fwd[i] : ev_sent[i], 0));
         ipc_release(peer_prev_, 0, i, s_recv_);
       }
     }
@@ -742,6 +842,8 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
   BP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   stats.gpu_ms = ms;
   stats.boundary_bytes = boundary;
+  stats.boundary_copies = s.input_copies() - copies_at_start;
+  stats.registered_buffers = registered_;
   for (int64_t i = 0; i < P; ++i) {
     cudaEventDestroy(ev_fwd[i]); cudaEventDestroy(ev_recv[i]);
     cudaEventDestroy(ev_sent[i]); cudaEventDestroy(ev_used[i]);
@@ -784,6 +886,71 @@ bp_status bp_pipeline_create(const bp_pipeline_desc* desc, int32_t rank, int32_t
     auto h = std::make_unique<bp_pipeline>();
     h->p = std::make_unique<bp::Pipeline>(*desc, rank, world, device, nccl_ids);
     *out = h.release();
+  });
+}
+
+}  // extern "C"
+
+namespace {
+// File rendezvous for the multi-process transports: `name` appears in `dir`
+// atomically (written to a private temporary, then renamed), readers poll.
+void publish_file(const std::string& dir, const std::string& name, const void* data, size_t n) {
+  const std::string tmp = dir + "/." + name + ".tmp." + std::to_string(static_cast<long>(getpid()));
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) bp::fail(BP_ERR_IO, "bootstrap: cannot write " + tmp);
+  const bool ok = std::fwrite(data, 1, n, f) == n;
+  std::fclose(f);
+  if (!ok || std::rename(tmp.c_str(), (dir + "/" + name).c_str()) != 0)
+    bp::fail(BP_ERR_IO, "bootstrap: cannot publish " + dir + "/" + name);
+}
+void await_file(const std::string& dir, const std::string& name, void* data, size_t n, int32_t timeout_ms) {
+  const std::string path = dir + "/" + name;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (f) {
+      const size_t got = std::fread(data, 1, n, f);
+      std::fclose(f);
+      if (got == n) return;
+    }
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(timeout_ms))
+      bp::fail(BP_ERR_IO, "bootstrap: timed out waiting for " + path);
+    std::this_thread::sleep_for(std::chrono::milliseconds(5));
+  }
+}
+}  // namespace
+
+extern "C" {
+
+bp_status bp_bootstrap_nccl_ids(const char* dir, int32_t rank, int32_t world, int32_t timeout_ms,
+                                uint8_t* ids_out) {
+  return bp::guarded([&] {
+    if (!dir || !ids_out) bp::fail(BP_ERR_CONFIG, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) bp::fail(BP_ERR_CONFIG, "bad rank / world");
+    const size_t n = static_cast<size_t>(world) * 128;
+    if (rank == 0) {
+      std::vector<uint8_t> ids(n);
+      for (int k = 0; k < world; ++k) {
+        ncclUniqueId u;
+        BP_NCCL(bp::nccl().GetUniqueId(&u));
+        std::memcpy(ids.data() + 128 * k, &u, 128);
+      }
+      publish_file(dir, "nccl_ids", ids.data(), n);
+    }
+    await_file(dir, "nccl_ids", ids_out, n, timeout_ms);
+  });
+}
+
+bp_status bp_bootstrap_ipc(bp_pipeline* p, const char* dir, int32_t rank, int32_t world, int32_t timeout_ms) {
+  return bp::guarded([&] {
+    if (!p || !dir) bp::fail(BP_ERR_CONFIG, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) bp::fail(BP_ERR_CONFIG, "bad rank / world");
+    uint8_t mine[64];
+    p->p->ipc_handle(mine);
+    publish_file(dir, "ipc." + std::to_string(rank), mine, 64);
+    std::vector<uint8_t> all(static_cast<size_t>(world) * 64);
+    for (int r = 0; r < world; ++r) await_file(dir, "ipc." + std::to_string(r), all.data() + 64 * r, 64, timeout_ms);
+    p->p->ipc_connect(all.data());
   });
 }
 

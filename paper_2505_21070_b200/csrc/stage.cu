@@ -274,19 +274,50 @@ void Stage::recorded_rows(int layer, double* host_out) {
   BP_CUDA(cudaStreamSynchronize(stream_));
 }
 
+void Stage::set_ring(int depth, int64_t max_tokens, const std::vector<void*>& x_slots,
+                     const std::vector<void*>& eps_slots) {
+  if (depth < 1 || depth > 3) fail(BP_ERR_CONFIG, "residual ring depth must be 1..3");
+  BP_CUDA(cudaSetDevice(device_));
+  BP_CUDA(cudaStreamSynchronize(stream_));
+  const size_t te = prec_ == BP_PREC_F64 ? 8 : 4;
+  xs_.assign(static_cast<size_t>(depth), nullptr);
+  es_.assign(static_cast<size_t>(depth), nullptr);
+  ring_external_ = !x_slots.empty();
+  if (ring_external_ && (static_cast<int>(x_slots.size()) != depth ||
+                         (is_last() && static_cast<int>(eps_slots.size()) != depth)))
+    fail(BP_ERR_CONFIG, "ring slots must match the ring depth");
+  for (int k = 0; k < depth; ++k) {
+    if (ring_external_) {
+      xs_[static_cast<size_t>(k)] = x_slots[static_cast<size_t>(k)];
+      if (is_last()) es_[static_cast<size_t>(k)] = eps_slots[static_cast<size_t>(k)];
+      continue;
+    }
+    xown_[k].reserve(static_cast<size_t>(max_tokens) * h_ * te);
+    xs_[static_cast<size_t>(k)] = xown_[k].p;
+    if (is_last()) {
+      eown_[k].reserve(static_cast<size_t>(max_tokens) * C_ * te);
+      es_[static_cast<size_t>(k)] = eown_[k].p;
+    }
+  }
+  for (int k = depth; k < 3; ++k) { xown_[k].release(); eown_[k].release(); }
+  ring_tokens_ = max_tokens;
+}
+
 void Stage::ensure_workspace(int64_t tokens, int64_t capture, bool new_cache, int use_prev) {
   const bool bf = prec_ == BP_PREC_BF16;
   const size_t te = prec_ == BP_PREC_F64 ? 8 : 4;
   const size_t me = bf ? 2 : te;
   const size_t S = static_cast<size_t>(tokens), P = static_cast<size_t>(capture);
   const size_t H = static_cast<size_t>(h_), nl = static_cast<size_t>(end_ - begin_);
+  if (tokens > ring_tokens_) {
+    if (ring_external_) fail(BP_ERR_DIMENSION, "pass exceeds the caller-supplied residual ring");
+    set_ring(std::max<int>(1, ring_depth()), tokens);
+  }
   if (tokens > cap_tokens_) {
-    x_.alloc(S * H * te);
     ln_.alloc(S * H * me);
     attn_.alloc(S * H * me);
     cq_.alloc(S * H * me);
     hmid_.alloc(S * static_cast<size_t>(F_) * me);
-    eps_.alloc(S * static_cast<size_t>(C_) * te);
     if (bf && is_first()) {
       ftab_.alloc((S / static_cast<size_t>(tpf_) + 1) * static_cast<size_t>(h_ / 2) * 32);
       lat32_.alloc(S * static_cast<size_t>(C_) * 4);
@@ -370,6 +401,8 @@ const void* Stage::forward(const StageInput& in) {
     fail(BP_ERR_CACHE, "host prefix not loaded");
   for (int f : in.capture_frames)
     if (f < 0 || f >= in.nframes) fail(BP_ERR_DIMENSION, "capture frame out of range");
+  if (xs_.empty()) set_ring(1, in.tokens);
+  if (in.slot < 0 || in.slot >= ring_depth()) fail(BP_ERR_INTERNAL, "residual ring slot out of range");
   switch (prec_) {
     case BP_PREC_F64: return forward_simt<double>(in);
     case BP_PREC_F32: return forward_simt<float>(in);
@@ -387,7 +420,7 @@ const void* Stage::forward_simt(const StageInput& in) {
   const bool new_rec = capturing && (in.mode == BP_CACHE_RECOMPUTE || in.record_inputs);
   ensure_workspace(S, P, new_cache, in.use_prev);
   cudaStream_t st = stream_;
-  T* x = x_.as<T>();
+  T* x = static_cast<T*>(xs_[static_cast<size_t>(in.slot)]);
   T* ln = ln_.as<T>();
   T* at = attn_.as<T>();
   T* cq = cq_.as<T>();
@@ -396,7 +429,10 @@ const void* Stage::forward_simt(const StageInput& in) {
     launch_embed<T>(static_cast<const double*>(in.payload), static_cast<const double*>(w_in_),
                     freq_.as<double>(), in.d_levels, in.d_frame_ids, S, C_, h_, tpf_, x, st);
   } else {
-    BP_CUDA(cudaMemcpyAsync(x, in.payload, static_cast<size_t>(S * H) * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    if (in.payload != x) {  // a receive that landed in the slot needs no copy
+      BP_CUDA(cudaMemcpyAsync(x, in.payload, static_cast<size_t>(S * H) * sizeof(T), cudaMemcpyDeviceToDevice, st));
+      ++input_copies_;
+    }
   }
   Entry nc, nr;
   T* qkv = qkv_.as<T>();
@@ -476,11 +512,12 @@ const void* Stage::forward_simt(const StageInput& in) {
   if (new_rec) { nr.valid = true; nr.tokens = P; rec_ = std::move(nr); }
   parity_ ^= 1;
   if (is_last()) {
-    launch_matmul<T>(x, H, static_cast<const T*>(w_out_), C_, static_cast<int>(S), C_, h_, eps_.as<T>(),
-                     C_, kEpiNone, nullptr, 0, st);
-    return eps_.p;
+    T* eps = static_cast<T*>(es_[static_cast<size_t>(in.slot)]);
+    launch_matmul<T>(x, H, static_cast<const T*>(w_out_), C_, static_cast<int>(S), C_, h_, eps, C_, kEpiNone, nullptr,
+                     0, st);
+    return eps;
   }
-  return x_.p;
+  return x;
 }
 
 const void* Stage::forward_bf16(const StageInput& in) {
@@ -492,7 +529,7 @@ const void* Stage::forward_bf16(const StageInput& in) {
   const bool new_rec = capturing && (in.mode == BP_CACHE_RECOMPUTE || in.record_inputs);
   ensure_workspace(S, P, new_cache, in.use_prev);
   cudaStream_t st = stream_;
-  float* x = x_.as<float>();
+  float* x = static_cast<float*>(xs_[static_cast<size_t>(in.slot)]);
   bf16* ln = ln_.as<bf16>();
   bf16* at = attn_.as<bf16>();
   bf16* cq = cq_.as<bf16>();
@@ -502,7 +539,10 @@ const void* Stage::forward_bf16(const StageInput& in) {
                       ttab_.as<double>(), ftab_.as<double>(), in.d_levels, in.d_frame_ids, S, C_, h_, tpf_,
                       lat32_.as<float>(), x, st);
   } else {
-    BP_CUDA(cudaMemcpyAsync(x, in.payload, static_cast<size_t>(S * H) * 4, cudaMemcpyDeviceToDevice, st));
+    if (in.payload != x) {  // a receive that landed in the slot needs no copy
+      BP_CUDA(cudaMemcpyAsync(x, in.payload, static_cast<size_t>(S * H) * 4, cudaMemcpyDeviceToDevice, st));
+      ++input_copies_;
+    }
   }
   const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(dh_)));
 
@@ -600,11 +640,11 @@ const void* Stage::forward_bf16(const StageInput& in) {
   if (new_rec) { nr.valid = true; nr.tokens = P; rec_ = std::move(nr); }
   parity_ ^= 1;
   if (is_last()) {
-    launch_gemm_f32_tile(x, H, static_cast<const float*>(w_out_), C_, static_cast<int>(S), C_, h_, eps_.as<float>(),
-                         C_, false, st);
-    return eps_.p;
+    float* eps = static_cast<float*>(es_[static_cast<size_t>(in.slot)]);
+    launch_gemm_f32_tile(x, H, static_cast<const float*>(w_out_), C_, static_cast<int>(S), C_, h_, eps, C_, false, st);
+    return eps;
   }
-  return x_.p;
+  return x;
 }
 
 void Stage::tag_entries(int64_t block_id, int level) {

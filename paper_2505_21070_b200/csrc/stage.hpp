@@ -25,6 +25,7 @@ struct StageInput {
   bool record_inputs = false;
   int mode = BP_CACHE_DISABLED;
   int use_prev = 0;                    // 0 none, 1 resident cache, 2 resident recording
+  int slot = 0;                        // residual-stream ring slot (see Stage::set_ring)
 };
 
 class Stage {
@@ -59,6 +60,21 @@ class Stage {
   void cache_rows(int layer, int which, double* host_out);  // fp64 download
   void bump_ulp(int layer, int which, int64_t index);
   std::string audit();  // cache_mismatch_report (model.cpp:171-199)
+
+  // Residual-stream ring for the multi-process executor: forward() runs in
+  // place on ring slot `in.slot` (the hidden state [tokens, h] in the
+  // activation dtype) and returns that slot (or eps slot `in.slot` on the
+  // last stage). A payload that already IS the slot (a receive landed there)
+  // is not copied, so a stage boundary costs no device copies: receive into
+  // the slot, run the layers in place, send from the slot. Slots are either
+  // the stage's own (depth slots of max_tokens rows) or supplied by the
+  // caller (NCCL-registered / IPC-exported memory, >= max_tokens rows each).
+  void set_ring(int depth, int64_t max_tokens, const std::vector<void*>& x_slots = {},
+                const std::vector<void*>& eps_slots = {});
+  void* x_slot(int k) const { return xs_[static_cast<size_t>(k)]; }
+  void* eps_slot(int k) const { return es_[static_cast<size_t>(k)]; }
+  int ring_depth() const { return static_cast<int>(xs_.size()); }
+  int64_t input_copies() const { return input_copies_; }  // payloads copied into the ring (not received in place)
 
   void set_context(const double* host, int64_t rows, int64_t cols);
   // use_prev 3 (host K|V) / 4 (host recorded inputs), fp64 device arrays, layer-major
@@ -128,7 +144,12 @@ class Stage {
 
   // workspace
   int64_t cap_tokens_ = 0, cap_capture_ = 0;
-  DevBuf x_, ln_, attn_, cq_, hmid_, eps_, kvp_, lnp_;
+  DevBuf ln_, attn_, cq_, hmid_, kvp_, lnp_;
+  DevBuf xown_[3], eown_[3];       // own residual / eps ring slots
+  std::vector<void*> xs_, es_;     // the ring in use (own or caller-supplied)
+  bool ring_external_ = false;
+  int64_t input_copies_ = 0;
+  int64_t ring_tokens_ = 0;
   DevBuf qkv_;             // [tokens][3h], reused by every layer
   DevBuf recbuf_[2];       // [L_local][capture][h] per parity (written before the old one is read)
   DevBuf cap_[2];          // KV feature cache [L_local][capture][2h]; the second buffer

@@ -302,6 +302,13 @@ void PipelineConfig::validate() const {
   model.validate();
   queue.validate();
   if (devices < 1) throw ConfigError("devices must be >= 1");
+  if (transport != Transport::kLoopback && world > 1) {
+    if (world != devices) throw ConfigError("multi-process transports need world == devices (one stage per process)");
+    if (rank < 0 || rank >= world) throw ConfigError("rank outside [0, world)");
+    if (bootstrap_dir.empty()) throw ConfigError("multi-process transports need a bootstrap_dir");
+  } else if (world != 1 || rank != 0) {
+    throw ConfigError("rank / world apply to the multi-process transports (nccl, ipc) only");
+  }
   if (model.layers % devices != 0 && !uneven_split)
     throw ConfigError("layers " + std::to_string(model.layers) + " not divisible by devices " + std::to_string(devices));
 }
@@ -334,7 +341,7 @@ bp_pipeline_desc pipe_desc(const PipelineConfig& c) {
   d.record_trace = c.record_trace;
   d.check_cache = c.check_cache;
   d.precision = static_cast<int32_t>(c.model.precision);
-  d.transport = BP_TRANSPORT_LOOPBACK;
+  d.transport = c.devices > 1 && c.world > 1 ? static_cast<int32_t>(c.transport) : BP_TRANSPORT_LOOPBACK;
   d.uneven_split = c.uneven_split;
   return d;
 }
@@ -400,8 +407,17 @@ RunResult run_pipeline(const PipelineConfig& cfg) {
   RunResult r;
   ScheduleGuard s = make_schedule(d);
   bp_pipeline* p = nullptr;
-  ck(bp_pipeline_create(&d, 0, 1, cfg.model.device, nullptr, &p));
+  const bool multi = d.transport != BP_TRANSPORT_LOOPBACK;
+  std::vector<uint8_t> ids;
+  if (multi && d.transport == BP_TRANSPORT_NCCL) {
+    ids.resize(static_cast<size_t>(cfg.world) * 128);
+    ck(bp_bootstrap_nccl_ids(cfg.bootstrap_dir.c_str(), cfg.rank, cfg.world, cfg.bootstrap_timeout_ms, ids.data()));
+  }
+  ck(bp_pipeline_create(&d, multi ? cfg.rank : 0, multi ? cfg.world : 1, cfg.model.device,
+                        ids.empty() ? nullptr : ids.data(), &p));
   std::unique_ptr<bp_pipeline, bp_status (*)(bp_pipeline*)> pg(p, bp_pipeline_destroy);
+  if (multi && d.transport == BP_TRANSPORT_IPC)
+    ck(bp_bootstrap_ipc(p, cfg.bootstrap_dir.c_str(), cfg.rank, cfg.world, cfg.bootstrap_timeout_ms));
   Collector col{&r.blocks, {cfg.model.height, cfg.model.width, cfg.model.channels}};
   ck(bp_pipeline_run(p, on_emit, &col));
   bp_pipeline_stats st{};

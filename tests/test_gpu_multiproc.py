@@ -73,3 +73,37 @@ def test_nccl_pipeline_equals_serial_bitwise(bp, tmp_path, prec, n):
     got = run_ranks(dict(base, devices=n, transport="nccl", uneven_split=n == 3), n, tmp_path)
     for r in range(2):
         assert np.array_equal(got[f"run{r}"], ref), (prec, n, r)
+
+
+def run_ranks_nt(cfg, n, tmp_path, runs=2):
+    """The ranks as plain processes (no torch.distributed launcher, no torch in
+    the workers): file rendezvous through a fresh bootstrap directory."""
+    boot = tmp_path / "boot"
+    boot.mkdir()
+    prefix = str(tmp_path / "nt")
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(n), LOCAL_RANK="0")
+        procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "mp_worker_nt.py"), json.dumps(cfg),
+                                       prefix, str(boot), str(runs)], cwd=ROOT, env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.STDOUT, text=True))
+    logs = [p.communicate(timeout=600)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), "\n".join(l[-2000:] for l in logs)
+    stats = [json.load(open(f"{prefix}.rank{r}.json")) for r in range(n)]
+    return np.load(prefix + ".npz"), stats
+
+
+@pytest.mark.parametrize("transport,prec,n", [("ipc", "bf16", 2), ("ipc", "f64", 3), ("nccl", "bf16", 2)])
+def test_file_bootstrap_without_torch(bp, tmp_path, transport, prec, n):
+    """No PyTorch anywhere in the ranks; stage boundaries received in place
+    (zero device copies of hidden states); bitwise == the serial oracle."""
+    base = dict(G["mid"]["config"], precision=prec)
+    if n > 2:
+        base.update(steps=3, blocks=2, layers=3)
+    want = bp.serial_oracle(base)
+    ref = np.concatenate([b["frames"].ravel() for b in want["blocks"]])
+    got, stats = run_ranks_nt(dict(base, devices=n, transport=transport), n, tmp_path)
+    for r in range(2):
+        assert np.array_equal(got[f"run{r}"], ref)
+    assert all(not s["torch_loaded"] for s in stats)
+    assert all(s["boundary_copies"] == 0 for s in stats), stats

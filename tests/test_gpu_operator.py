@@ -177,3 +177,32 @@ def test_smoke_traffic_report_matches_engine(op):
         finally:
             p.close()
         assert rep["match"], rep
+
+
+@pytest.mark.parametrize("transport", ["ipc", "nccl"])
+def test_cli_multiprocess_run_equals_single_process(tmp_path, transport):
+    """The C++ host path end to end, no Python or PyTorch in the ranks: two
+    `blockpipe run --transport ... --rank r --world 2` processes (file
+    rendezvous in --bootstrap-dir) write latents.bin / schedule.csv /
+    transfers.json byte-identical to the single-process two-stage run."""
+    import subprocess
+    exe = os.path.join(ROOT, "paper_2505_21070_b200", "lib", "blockpipe")
+    common = ["run", "--devices", "2", "--layers", "4", "--hidden", "256", "--heads", "2", "--channels", "16",
+              "--height", "4", "--width", "6", "--context-len", "16", "--steps", "3", "--blocks", "3",
+              "--precision", "bf16", "--mode", "single"]
+    single = subprocess.run([exe, *common, "--out", str(tmp_path / "one")], capture_output=True, text=True, timeout=300)
+    assert single.returncode == 0, single.stderr
+    boot = tmp_path / "boot"
+    boot.mkdir()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, CUDA_MODULE_LOADING="EAGER")
+        if transport == "nccl":  # both ranks share GPU 0: NCCL treats them as separate hosts
+            env.update(NCCL_HOSTID=f"blockpipe-cli-{r}", NCCL_SOCKET_IFNAME="lo", NCCL_IB_DISABLE="1")
+        procs.append(subprocess.Popen([exe, *common, "--transport", transport, "--rank", str(r), "--world", "2",
+                                       "--bootstrap-dir", str(boot), "--out", str(tmp_path / "multi")],
+                                      env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+    logs = [p.communicate(timeout=600)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), logs
+    for f in ("latents.bin", "schedule.csv", "transfers.json"):
+        assert (tmp_path / "multi" / f).read_bytes() == (tmp_path / "one" / f).read_bytes(), f

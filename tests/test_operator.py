@@ -242,6 +242,9 @@ def test_noise_demo_overlap_signal(op):
     (["analyze", "costs", "--method", "gpipe"], 2),
     (["analyze", "bubble", "--format", "yaml"], 2),
     (["run", "--config", "/nonexistent/config.json"], 3),
+    (["run", "--transport", "nccl", "--world", "2", "--rank", "0", "--devices", "2"], 2),  # no --bootstrap-dir
+    (["run", "--rank", "1"], 2),
+    (["run", "--transport", "carrier-pigeon"], 2),
     (["--help"], 0),
     (["analyze", "--help"], 0),
 ])
