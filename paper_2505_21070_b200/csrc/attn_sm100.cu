@@ -3,24 +3,18 @@
 // HBM) ++ current block] without concatenating them in memory
 // (model.cpp:201-211, 302-318: vcat_rows(prefix, k) then attention()).
 //
-// Two implementations (launch_attn_tc variant):
-//   2 (default) k_attn_pp: two 128-row query tiles per CTA, 64-key K/V tiles,
-//     double-buffered S per tile, both softmax warpgroups running concurrently
-//     (see the comment above k_attn_pp).
-//   1 k_attn_tc: one 128-row query tile per CTA, Q and P as TMEM A operands:
-//
-//   warp 0      TMA producer: Q once, then K and V tiles of 128 keys into two
-//               separate 3-deep rings (K is freed as soon as S_j is computed)
-//   warp 1      MMA issuer (warp-converged, elect-in-PTX): S_j = Q K_j^T with Q
-//               staged in TMEM, O += P_{j-1} V_{j-1} with P in TMEM; S double-buffered
-//   warps 2..5  softmax: one thread per query row stages Q into TMEM, then per
-//               tile reads S from TMEM, online softmax in the log2 domain (1/8
-//               of exp2 on an FMA polynomial), writes P (bf16 pairs) over S in
-//               TMEM; O is rescaled in TMEM only when the row max grows by > 2^8;
-//               epilogue O / l -> bf16 -> global
-// Only K and V stream through shared memory (A operands come from TMEM).
+// Two kernels, both the ping-pong schedule of two 128-row query tiles over
+// 64-key K/V tiles with S double-buffered in TMEM (see k_attn_pp):
+//   k_attn_pp2  on a cta_group::2 CTA pair (M = 256 MMAs, each CTA staging
+//               half of every K / V tile): the self-attention (launch_attn_tc
+//               variant 4, the default);
+//   k_attn_pp   one CTA, O staged through smem and written by TMA bulk
+//               stores: the cross-attention over the 512-token context
+//               (variant 2), where the pair's cluster setup does not pay off.
 // Keys past a segment's end (a tile that straddles it) are masked; TMA
-// zero-fills the rows.
+// zero-fills the rows. Losing variants measured in round 1 (one query tile
+// per CTA with Q in TMEM; 128-key tiles with rows split over two softmax
+// warps) are recorded in DESIGN.md and no longer built.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -39,25 +33,10 @@ void launch_attn_simt(const AttnBf16Args& a, int64_t rows, cudaStream_t st);
 
 namespace {
 
-constexpr int kDh = 128, BQ = 128, BKV = 128;
+constexpr int kDh = 128, BQ = 128;
 constexpr uint32_t HALF = 128 * 64 * 2;      // [128 rows][64 bf16] swizzled TMA box
-constexpr uint32_t TILE = 2 * HALF;          // 32 KB
-constexpr int KST = 3;                       // K ring depth
-constexpr int VST = 3;                       // V ring depth
-constexpr uint32_t SMEM_Q = 0;
-constexpr uint32_t SMEM_K = SMEM_Q + TILE;
-constexpr uint32_t SMEM_V = SMEM_K + KST * TILE;
-constexpr uint32_t SMEM_BAR = SMEM_V + VST * TILE;
-constexpr uint32_t SMEM_BYTES = SMEM_BAR + 256 + 1024;  // mbarriers + TMEM slot + alignment
-constexpr int kThreads = 192;  // TMA warp, MMA warp, 4 softmax warps
+constexpr uint32_t TILE = 2 * HALF;          // 32 KB: one 128-row query tile
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P values up to 2^8 before O is rescaled
-// TMEM columns: S_0 [0,128), S_1 [128,256) (P_j overwrites the first 64
-// columns of S_j as packed bf16 pairs), O [256,384), Q [384,448).
-constexpr uint32_t TM_O = 256, TM_Q = 384;
-
-struct AttnMaps {
-  CUtensorMap q, k0, v0, k1, v1;
-};
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -65,254 +44,9 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x on the FMA pipe for x <= 8: round-to-integer via the 1.5*2^23 trick,
-// degree-3 minimax polynomial for 2^f on [-0.5, 0.5] (rel. error ~1e-4, far
-// below the bf16 rounding of P), exponent added with an integer shift.
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -127.f);
-  const float j = x + 12582912.f;
-  const float f = x - (j - 12582912.f);
-  const float p = fmaf(fmaf(fmaf(0.0555041086f, f, 0.2402264923f), f, 0.6931471806f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
-}
-
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
-}
-
-// Both MMAs take their A operand from TMEM (Q staged once; P written by the
-// softmax over its S buffer), so only K / V stream through shared memory.
-__global__ void __launch_bounds__(kThreads, 1)
-    k_attn_tc(const __grid_constant__ AttnMaps maps, int64_t rows, int64_t n0, int64_t n1, float scale_log2,
-              bf16* __restrict__ out, int64_t ldo) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
-  uint64_t* q_full = bars + 0;     // Q landed in smem (TMA)
-  uint64_t* q_tmem = bars + 1;     // Q staged into TMEM (128 softmax threads)
-  uint64_t* k_full = bars + 2;     // [KST]
-  uint64_t* k_empty = bars + 5;    // [KST] freed once S_j is computed
-  uint64_t* v_full = bars + 8;     // [VST]
-  uint64_t* v_empty = bars + 11;   // [VST] freed once PV_j is computed
-  uint64_t* s_full = bars + 14;    // [2]
-  uint64_t* p_full = bars + 16;    // [2] P_j written into TMEM (also frees S_j)
-  uint64_t* pv_done = bars + 18;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qtile = blockIdx.x, head = blockIdx.y;
-  const int t0 = static_cast<int>((n0 + BKV - 1) / BKV);
-  const int t1 = static_cast<int>((n1 + BKV - 1) / BKV);
-  const int T = t0 + t1;
-
-  if (warp == 0 && lane == 0) {
-    tc::tma_prefetch(&maps.q);
-    tc::tma_prefetch(&maps.k1);
-    tc::tma_prefetch(&maps.v1);
-    tc::mbar_init(q_full, 1);
-    tc::mbar_init(q_tmem, 128);
-    for (int s = 0; s < KST; ++s) {
-      tc::mbar_init(&k_full[s], 1);
-      tc::mbar_init(&k_empty[s], 1);
-    }
-    for (int s = 0; s < VST; ++s) {
-      tc::mbar_init(&v_full[s], 1);
-      tc::mbar_init(&v_empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      tc::mbar_init(&s_full[s], 1);
-      tc::mbar_init(&p_full[s], 128);
-    }
-    tc::mbar_init(pv_done, 1);
-    tc::fence_barrier_init();
-  }
-  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    // ---- TMA producer: Q, then K_j / V_j into their rings -----------------------------
-    tc::mbar_arrive_expect_tx_elect(q_full, TILE);
-    tc::tma_load_2d_elect(smem + SMEM_Q, &maps.q, q_full, head * kDh, qtile * BQ);
-    tc::tma_load_2d_elect(smem + SMEM_Q + HALF, &maps.q, q_full, head * kDh + 64, qtile * BQ);
-    for (int j = 0; j < T; ++j) {
-      const bool seg0 = j < t0;
-      const int row0 = (seg0 ? j : j - t0) * BKV;
-      const int ks = j % KST, vs = j % VST;
-      tc::mbar_wait(&k_empty[ks], ((j / KST) & 1) ^ 1);
-      uint8_t* kd = smem + SMEM_K + ks * TILE;
-      const CUtensorMap* mk = seg0 ? &maps.k0 : &maps.k1;
-      tc::mbar_arrive_expect_tx_elect(&k_full[ks], TILE);
-      tc::tma_load_2d_elect(kd, mk, &k_full[ks], head * kDh, row0);
-      tc::tma_load_2d_elect(kd + HALF, mk, &k_full[ks], head * kDh + 64, row0);
-      tc::mbar_wait(&v_empty[vs], ((j / VST) & 1) ^ 1);
-      uint8_t* vd = smem + SMEM_V + vs * TILE;
-      const CUtensorMap* mv = seg0 ? &maps.v0 : &maps.v1;
-      tc::mbar_arrive_expect_tx_elect(&v_full[vs], TILE);
-      tc::tma_load_2d_elect(vd, mv, &v_full[vs], head * kDh, row0);
-      tc::tma_load_2d_elect(vd + HALF, mv, &v_full[vs], head * kDh + 64, row0);
-    }
-  } else if (warp == 1) {
-    // ---- MMA issuer: S_0, S_1, PV_0, S_2, PV_1, ... (tensor core runs them in order) ----
-    constexpr uint32_t idesc_s = tc::idesc_bf16(BQ, BKV, 0, 0);   // Q (TMEM) x K^T (smem, K-major)
-    constexpr uint32_t idesc_o = tc::idesc_bf16(BQ, kDh, 0, 1);   // P (TMEM) x V (smem, MN-major)
-    tc::mbar_wait(q_tmem, 0);
-    tc::fence_after_sync();
-    auto issue_pv = [&](int jj) {
-      const int vs = jj % VST;
-      tc::mbar_wait(&v_full[vs], (jj / VST) & 1);
-      tc::mbar_wait(&p_full[jj & 1], (jj >> 1) & 1);
-      tc::fence_after_sync();
-      const uint32_t v_addr = tc::smem_u32(smem + SMEM_V + vs * TILE);
-      const uint32_t p_tm = tmem + static_cast<uint32_t>((jj & 1) * BKV);
-#pragma unroll
-      for (int kk = 0; kk < BKV / 16; ++kk) {
-        // V tile [keys][d]: MN-major (d contiguous); 16 keys = two 8-row groups
-        const uint64_t bd = tc::desc_sw128(v_addr + kk * 2048, 1024, HALF);
-        tc::mma_bf16_ts_elect(tmem + TM_O, p_tm + kk * 8, bd, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
-      }
-      tc::mma_commit_elect(pv_done);
-      tc::mma_commit_elect(&v_empty[vs]);
-    };
-    for (int j = 0; j < T; ++j) {
-      const int ks = j % KST;
-      tc::mbar_wait(&k_full[ks], (j / KST) & 1);
-      if (j >= 2) tc::mbar_wait(&p_full[j & 1], ((j >> 1) - 1) & 1);  // S_{j-2} buffer consumed
-      tc::fence_after_sync();
-      const uint32_t k_addr = tc::smem_u32(smem + SMEM_K + ks * TILE);
-      const uint32_t d = tmem + static_cast<uint32_t>((j & 1) * BKV);
-#pragma unroll
-      for (int kk = 0; kk < kDh / 16; ++kk) {
-        const uint64_t bd = tc::desc_sw128(k_addr + (kk >> 2) * HALF + (kk & 3) * 32, 1024, 16);
-        tc::mma_bf16_ts_elect(d, tmem + TM_Q + kk * 8, bd, idesc_s, kk > 0 ? 1u : 0u);
-      }
-      tc::mma_commit_elect(&s_full[j & 1]);
-      tc::mma_commit_elect(&k_empty[ks]);
-      if (j >= 1) issue_pv(j - 1);
-    }
-    if (T >= 1) issue_pv(T - 1);
-  } else {
-    // ---- softmax + epilogue: thread <-> query row <-> TMEM lane ---------------------------
-    const int qq = warp & 3;
-    const int r = qq * 32 + lane;
-    const uint32_t lane_off = static_cast<uint32_t>(qq * 32) << 16;
-    {  // stage Q row r into TMEM columns [TM_Q, TM_Q + 64): packed bf16 pairs along d
-      tc::mbar_wait(q_full, 0);
-      const uint32_t q_row = tc::smem_u32(smem + SMEM_Q) + static_cast<uint32_t>(r * 128);
-      uint32_t qa[32], qb[32];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(qa[4 * c]), "=r"(qa[4 * c + 1]), "=r"(qa[4 * c + 2]), "=r"(qa[4 * c + 3])
-                     : "r"(q_row + ((c ^ (r & 7)) << 4)));
-        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(qb[4 * c]), "=r"(qb[4 * c + 1]), "=r"(qb[4 * c + 2]), "=r"(qb[4 * c + 3])
-                     : "r"(q_row + HALF + ((c ^ (r & 7)) << 4)));
-      }
-      tc::tmem_st32(tmem + lane_off + TM_Q, qa);
-      tc::tmem_st32(tmem + lane_off + TM_Q + 32, qb);
-      tc::tmem_st_wait();
-      tc::fence_before_sync();
-      tc::mbar_arrive(q_tmem);
-    }
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < T; ++j) {
-      const int s = j & 1;
-      const bool seg0 = j < t0;
-      const int64_t seg_n = seg0 ? n0 : n1;
-      const int row0 = (seg0 ? j : j - t0) * BKV;
-      const int valid = static_cast<int>(seg_n - row0 < BKV ? seg_n - row0 : BKV);
-      const uint32_t tm_s = tmem + lane_off + static_cast<uint32_t>(s * BKV);
-      tc::mbar_wait(&s_full[s], (j >> 1) & 1);
-      tc::fence_after_sync();
-      uint32_t sr[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        tc::tmem_ld32(tm_s + static_cast<uint32_t>(c * 32), *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-      tc::tmem_ld_wait();
-      if (valid < BKV) {  // keys past the segment end (only a segment's last tile)
-#pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
-      }
-      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int c = 0; c < 128; ++c) m4[c & 3] = fmaxf(m4[c & 3], __uint_as_float(sr[c]));
-      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;  // scale > 0
-      const bool need = mx > m_used + kRescaleThreshold;
-      const float m_new = need ? mx : m_used;
-      const float corr = need ? ex2(m_used - m_new) : 1.f;  // 0 on the first tile
-      const float neg_m = -m_new;
-      uint32_t pk[64];
-      float ls0 = 0.f, ls1 = 0.f;
-#pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const float x0 = fmaf(__uint_as_float(sr[2 * c]), scale_log2, neg_m);
-        const float x1 = fmaf(__uint_as_float(sr[2 * c + 1]), scale_log2, neg_m);
-        // 1 pair in 8 on the FMA pipe, the rest on MUFU (balances the two pipes)
-        const float p0 = (c & 7) == 7 ? ex2_poly(x0) : ex2(x0);
-        const float p1 = (c & 7) == 7 ? ex2_poly(x1) : ex2(x1);
-        ls0 += p0;
-        ls1 += p1;
-        pk[c] = pack_bf16(p0, p1);
-      }
-      l = l * corr + (ls0 + ls1);
-      m_used = m_new;
-      // O is stable once PV_{j-1} completed; only rescales need to wait for it
-      if (j >= 1 && __any_sync(0xffffffffu, need)) {
-        tc::mbar_wait(pv_done, (j - 1) & 1);
-        tc::fence_after_sync();
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          const uint32_t ta = tmem + lane_off + TM_O + static_cast<uint32_t>(c * 32);
-          tc::tmem_ld32(ta, o);
-          tc::tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
-          tc::tmem_st32(ta, o);
-        }
-      }
-      // P_j (bf16 pairs along keys) over the first 64 columns of S_j
-      tc::tmem_st32(tm_s, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-      tc::tmem_st32(tm_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
-      tc::tmem_st_wait();
-      tc::fence_before_sync();
-      tc::mbar_arrive(&p_full[s]);
-    }
-    // epilogue: O / l
-    if (T >= 1) {
-      tc::mbar_wait(pv_done, (T - 1) & 1);
-      tc::fence_after_sync();
-    }
-    const int64_t row = static_cast<int64_t>(qtile) * BQ + r;
-    const float inv_l = 1.f / l;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t o[32];
-      tc::tmem_ld32(tmem + lane_off + TM_O + static_cast<uint32_t>(c * 32), o);
-      tc::tmem_ld_wait();
-      if (row < rows) {
-        uint4* dst = reinterpret_cast<uint4*>(out + row * ldo + head * kDh + c * 32);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          dst[v] = make_uint4(pack_bf16(__uint_as_float(o[8 * v]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l),
-                              pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l),
-                              pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l),
-                              pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l));
-        }
-      }
-    }
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 1) {
-    tc::fence_after_sync();
-    tc::tmem_dealloc<512>(tmem);
-  }
 }
 
 // ============================================================================
@@ -640,7 +374,7 @@ struct AttnMapsP2 {
 };
 
 // kPoly8: exp2 pairs in 8 evaluated on the FMA pipe
-template <int kPoly8, bool kTmaEpi = false>
+template <int kPoly8>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     k_attn_pp2(const __grid_constant__ AttnMapsP2 maps, int64_t rows, int64_t n0, int64_t n1, float scale_log2,
                bf16* __restrict__ out, int64_t ldo) {
@@ -843,36 +577,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     }
     const int64_t row = static_cast<int64_t>(qpair) * 2 * BQ + x * BQ + r;
     const float inv_l = 1.f / (l2.x + l2.y);
-    if (kTmaEpi) {
-      // O / l as bf16 into this tile's Q buffer (every QK^T completed before its
-      // last PV) in the output map's swizzled [128][64] layout, then TMA stores
-      uint8_t* stage_o = smem + P2_Q + x * TILE;
-      const uint32_t so = tc::smem_u32(stage_o);
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t o[32];
-        tc::tmem_ld32(tm_o + static_cast<uint32_t>(c * 32), o);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const uint32_t unit = static_cast<uint32_t>((c & 1) * 4 + v);
-          tc::st_shared_v4(so + static_cast<uint32_t>((c >> 1) * HALF + r * 128) + ((unit ^ static_cast<uint32_t>(r & 7)) << 4),
-                           pack_bf16(__uint_as_float(o[8 * v]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l),
-                           pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l),
-                           pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l),
-                           pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l));
-        }
-      }
-      tc::fence_proxy_async_smem();
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + x) : "memory");  // this tile's 128 softmax threads
-      if (qq == 0 && lane == 0) {
-        const int qrow = qpair * 2 * BQ + x * BQ;
-        tc::tma_store_2d(&maps.o, stage_o, head * kDh, qrow);
-        tc::tma_store_2d(&maps.o, stage_o + HALF, head * kDh + 64, qrow);
-        tc::bulk_commit_group();
-        tc::bulk_wait_group_read<0>();
-      }
-    } else
 #pragma unroll 1
     for (int c = 0; c < 4; ++c) {
       uint32_t o[32];
@@ -896,294 +600,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
   if (warp == 1) {
     tc::fence_after_sync();
     tc::tmem_dealloc_cg2<512>(tmem);
-  }
-}
-
-// ============================================================================
-// Variant 3: two query tiles per CTA, 128-key tiles, one S buffer per tile,
-// each S row split across two softmax warps
-// ============================================================================
-// TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512). QK^T is an SS
-// MMA at N = 128, which runs at the tcgen05 floor (8 KB of smem per 64-cycle
-// step, tools/micro/mma_floor.cu); P_x(j) overwrites the first 64 columns of
-// S_x as packed bf16 and feeds PV as the TMEM A operand. The tensor core runs
-//   PV_A(j) QK_A(j+1) PV_B(j) QK_B(j+1) ...
-// so softmax A(j+1) overlaps PV_B(j) + QK_B(j+1) and vice versa; the commit
-// that publishes S_x(j+1) also covers PV_x(j), so an O rescale never waits.
-// The softmax of one tile is latency-bound with one warp per SM sub-partition,
-// so each row is split over two warps that share its TMEM lane quarter: half
-// h owns keys [64h, 64h+64) and O columns [64h, 64h+64); the halves swap
-// their row maxima through shared memory (one 64-thread named barrier per
-// tile, which also orders every S load of the tile before any P store).
-// 640 threads: warpgroup 0 = TMA warp, MMA warp, two idle warps (registers
-// released with setmaxnreg.dec); warpgroups 1-2 = tile A halves 0/1,
-// warpgroups 3-4 = tile B halves 0/1.
-constexpr int FA_BK = 128;
-constexpr int FA_KST = 2, FA_VST = 2;
-constexpr uint32_t FA_Q = 0;                          // Q_A, Q_B (32 KB each)
-constexpr uint32_t FA_K = FA_Q + 2 * TILE;
-constexpr uint32_t FA_V = FA_K + FA_KST * TILE;
-constexpr uint32_t FA_RED = FA_V + FA_VST * TILE;     // [parity][tile][half][128 rows] fp32
-constexpr uint32_t FA_BAR = FA_RED + 2 * 2 * 2 * 128 * 4;
-constexpr uint32_t FA_SMEM_BYTES = FA_BAR + 256 + 1024;
-constexpr int FA_THREADS = 640;
-static_assert(FA_SMEM_BYTES <= 232448, "variant-3 attention exceeds the 227 KB smem limit");
-
-__device__ __forceinline__ void named_bar_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-__global__ void __launch_bounds__(FA_THREADS, 1)
-    k_attn_fa(const __grid_constant__ AttnMaps maps, int64_t rows, int64_t n0, int64_t n1, float scale_log2,
-              bf16* __restrict__ out, int64_t ldo) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + FA_BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;              // [FA_KST]
-  uint64_t* k_empty = k_full + FA_KST;      // [FA_KST]
-  uint64_t* v_full = k_empty + FA_KST;      // [FA_VST]
-  uint64_t* v_empty = v_full + FA_VST;      // [FA_VST]
-  uint64_t* s_full = v_empty + FA_VST;      // [tile]
-  uint64_t* p_full = s_full + 2;            // [tile] (256 arrivals)
-  uint64_t* o_full = p_full + 2;            // [tile] final PV done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
-  float* red = reinterpret_cast<float*>(smem + FA_RED);
-
-  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const int qpair = blockIdx.x, head = blockIdx.y;
-  const int t0 = static_cast<int>((n0 + FA_BK - 1) / FA_BK);
-  const int t1 = static_cast<int>((n1 + FA_BK - 1) / FA_BK);
-  const int T = t0 + t1;
-
-  if (warp == 0 && lane == 0) {
-    tc::tma_prefetch(&maps.q);
-    tc::tma_prefetch(&maps.k1);
-    tc::tma_prefetch(&maps.v1);
-    tc::mbar_init(q_full, 1);
-    for (int s = 0; s < FA_KST; ++s) {
-      tc::mbar_init(&k_full[s], 1);
-      tc::mbar_init(&k_empty[s], 1);
-    }
-    for (int s = 0; s < FA_VST; ++s) {
-      tc::mbar_init(&v_full[s], 1);
-      tc::mbar_init(&v_empty[s], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&p_full[i], 256);
-      tc::mbar_init(&o_full[i], 1);
-    }
-    tc::fence_barrier_init();
-  }
-  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp < 4) {
-    tc::setmaxnreg_dec<32>();
-    if (warp == 0) {
-      // ---- TMA producer -----------------------------------------------------------------
-      tc::mbar_arrive_expect_tx_elect(q_full, 2 * TILE);
-      for (int x = 0; x < 2; ++x) {
-        const int qrow = qpair * 2 * BQ + x * BQ;
-        tc::tma_load_2d_elect(smem + FA_Q + x * TILE, &maps.q, q_full, head * kDh, qrow);
-        tc::tma_load_2d_elect(smem + FA_Q + x * TILE + HALF, &maps.q, q_full, head * kDh + 64, qrow);
-      }
-      for (int j = 0; j < T; ++j) {
-        const bool seg0 = j < t0;
-        const int row0 = (seg0 ? j : j - t0) * FA_BK;
-        const int ks = j % FA_KST, vs = j % FA_VST;
-        tc::mbar_wait(&k_empty[ks], ((j / FA_KST) & 1) ^ 1);
-        uint8_t* kd = smem + FA_K + ks * TILE;
-        const CUtensorMap* mk = seg0 ? &maps.k0 : &maps.k1;
-        tc::mbar_arrive_expect_tx_elect(&k_full[ks], TILE);
-        tc::tma_load_2d_elect(kd, mk, &k_full[ks], head * kDh, row0);
-        tc::tma_load_2d_elect(kd + HALF, mk, &k_full[ks], head * kDh + 64, row0);
-        tc::mbar_wait(&v_empty[vs], ((j / FA_VST) & 1) ^ 1);
-        uint8_t* vd = smem + FA_V + vs * TILE;
-        const CUtensorMap* mv = seg0 ? &maps.v0 : &maps.v1;
-        tc::mbar_arrive_expect_tx_elect(&v_full[vs], TILE);
-        tc::tma_load_2d_elect(vd, mv, &v_full[vs], head * kDh, row0);
-        tc::tma_load_2d_elect(vd + HALF, mv, &v_full[vs], head * kDh + 64, row0);
-      }
-    } else if (warp == 1) {
-      // ---- MMA issuer ---------------------------------------------------------------------
-      constexpr uint32_t idesc_s = tc::idesc_bf16(BQ, FA_BK, 0, 0);  // Q x K^T, both K-major smem
-      constexpr uint32_t idesc_o = tc::idesc_bf16(BQ, kDh, 0, 1);    // P (TMEM) x V (smem, MN-major)
-      const uint32_t q_base = tc::smem_u32(smem + FA_Q);
-      auto qk = [&](int x, int j) {
-        const uint32_t k_addr = tc::smem_u32(smem + FA_K + (j % FA_KST) * TILE);
-        tc::mma_ss_k128_elect<HALF / 16, HALF / 16>(tmem + static_cast<uint32_t>(x * FA_BK),
-                                                    tc::desc_sw128(q_base + x * TILE, 1024, 16),
-                                                    tc::desc_sw128(k_addr, 1024, 16), idesc_s, 0u);
-      };
-      auto pv = [&](int x, int j) {
-        const uint32_t v_addr = tc::smem_u32(smem + FA_V + (j % FA_VST) * TILE);
-        const uint32_t o = tmem + 256u + static_cast<uint32_t>(x * kDh);
-        const uint32_t p = tmem + static_cast<uint32_t>(x * FA_BK);
-        // keys [0,64) then [64,128): 64 rows x 128 B = 8 KB further into each d-half
-        tc::mma_ts_k64_elect<2048 / 16>(o, p, tc::desc_sw128(v_addr, 1024, HALF), idesc_o, j > 0 ? 1u : 0u);
-        tc::mma_ts_k64_elect<2048 / 16>(o, p + 32, tc::desc_sw128(v_addr + 8192, 1024, HALF), idesc_o, 1u);
-      };
-      tc::mbar_wait(q_full, 0);
-      if (T > 0) {
-        tc::mbar_wait(&k_full[0], 0);
-        tc::fence_after_sync();
-        qk(0, 0);
-        tc::mma_commit_elect(&s_full[0]);
-        qk(1, 0);
-        tc::mma_commit_elect(&s_full[1]);
-        tc::mma_commit_elect(&k_empty[0]);
-      }
-      for (int j = 0; j < T; ++j) {
-        const bool more = j + 1 < T;
-        tc::mbar_wait(&v_full[j % FA_VST], (j / FA_VST) & 1);
-        tc::mbar_wait(&p_full[0], j & 1);
-        tc::fence_after_sync();
-        pv(0, j);
-        if (more) {
-          tc::mbar_wait(&k_full[(j + 1) % FA_KST], ((j + 1) / FA_KST) & 1);
-          tc::fence_after_sync();
-          qk(0, j + 1);  // in-order after PV_A(j), which reads P_A(j) from the same columns
-          tc::mma_commit_elect(&s_full[0]);
-        } else {
-          tc::mma_commit_elect(&o_full[0]);
-        }
-        tc::mbar_wait(&p_full[1], j & 1);
-        tc::fence_after_sync();
-        pv(1, j);
-        tc::mma_commit_elect(&v_empty[j % FA_VST]);
-        if (more) {
-          qk(1, j + 1);
-          tc::mma_commit_elect(&s_full[1]);
-          tc::mma_commit_elect(&k_empty[(j + 1) % FA_KST]);
-        } else {
-          tc::mma_commit_elect(&o_full[1]);
-        }
-      }
-    }
-  } else {
-    tc::setmaxnreg_inc<112>();  // pool = 640 x 96 at launch: 32 + 4 x 112 = 480
-    // ---- softmax + epilogue: tile x, key half hf, row r (TMEM lane) ---------------------------
-    const int x = (warp - 4) >> 3;
-    const int hf = ((warp - 4) >> 2) & 1;
-    const int qq = warp & 3;
-    const int r = qq * 32 + lane;
-    const int bar_id = 1 + x * 4 + qq;  // the two warps of this tile and lane quarter
-    const uint32_t lane_off = static_cast<uint32_t>(qq * 32) << 16;
-    const uint32_t tm_s = tmem + lane_off + static_cast<uint32_t>(x * FA_BK);
-    const uint32_t tm_o = tmem + lane_off + 256u + static_cast<uint32_t>(x * kDh + hf * 64);
-    const float2 sc2 = make_float2(scale_log2, scale_log2);
-    float m_used = -INFINITY;
-    float2 l2 = make_float2(0.f, 0.f);
-    const int n0i = static_cast<int>(n0), n1i = static_cast<int>(n1);
-    for (int j = 0; j < T; ++j) {
-      const bool seg0 = j < t0;
-      const int row0 = (seg0 ? j : j - t0) * FA_BK;
-      const int rem = (seg0 ? n0i : n1i) - row0 - hf * 64;  // valid keys in this half
-      tc::mbar_wait(&s_full[x], j & 1);
-      tc::fence_after_sync();
-      uint32_t sr[64];
-      tc::tmem_ld32(tm_s + static_cast<uint32_t>(hf * 64), *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tc::tmem_ld32(tm_s + static_cast<uint32_t>(hf * 64 + 32), *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      tc::tmem_ld_wait();
-      if (rem < 64) {  // keys past the segment end (a segment's last tile)
-#pragma unroll
-        for (int c = 0; c < 64; ++c)
-          if (c >= rem) sr[c] = __float_as_uint(-INFINITY);
-      }
-      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int c = 0; c < 64; c += 8) {
-        m4[0] = max3f(m4[0], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
-        m4[1] = max3f(m4[1], __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
-        m4[2] = max3f(m4[2], __uint_as_float(sr[c + 4]), __uint_as_float(sr[c + 5]));
-        m4[3] = max3f(m4[3], __uint_as_float(sr[c + 6]), __uint_as_float(sr[c + 7]));
-      }
-      // swap half-row maxima; the barrier also orders both halves' S loads
-      // before either half's P store (P of half 1 lands in S columns of half 0)
-      float* slot = red + ((j & 1) * 2 + x) * 256;
-      slot[hf * 128 + r] = max3f(m4[0], m4[1], fmaxf(m4[2], m4[3]));
-      tc::fence_before_sync();
-      named_bar_sync(bar_id, 64);
-      tc::fence_after_sync();
-      const float mx = fmaxf(slot[r], slot[128 + r]) * scale_log2;  // scale > 0
-      const bool need = mx > m_used + kRescaleThreshold;
-      const float m_new = need ? mx : m_used;
-      const float corr = need ? ex2(m_used - m_new) : 1.f;  // 0 on the first tile
-      const float2 neg_m2 = make_float2(-m_new, -m_new);
-      float2 ls_a = make_float2(0.f, 0.f), ls_b = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int k = ch * 16 + c;
-          const float2 xv = __ffma2_rn(make_float2(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1])), sc2,
-                                       neg_m2);
-          const float2 p = (c & 3) == 3 ? ex2_poly2(xv) : make_float2(ex2(xv.x), ex2(xv.y));
-          if (c & 1) ls_b = __fadd2_rn(ls_b, p);
-          else ls_a = __fadd2_rn(ls_a, p);
-          pk[c] = pack_bf16(p.x, p.y);
-        }
-        tc::tmem_st16(tm_s + static_cast<uint32_t>(hf * 32 + ch * 16), pk);
-      }
-      l2 = __ffma2_rn(l2, make_float2(corr, corr), __fadd2_rn(ls_a, ls_b));
-      m_used = m_new;
-      // O holds PV_x(j-1): the commit that published S_x(j) covers it
-      if (j >= 1 && __any_sync(0xffffffffu, need)) {
-#pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          uint32_t o[32];
-          const uint32_t ta = tm_o + static_cast<uint32_t>(c * 32);
-          tc::tmem_ld32(ta, o);
-          tc::tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
-          tc::tmem_st32(ta, o);
-        }
-      }
-      tc::tmem_st_wait();
-      tc::fence_before_sync();
-      tc::mbar_arrive(&p_full[x]);
-    }
-    // row sum over both halves, through the parity slot tile T-1 did not use
-    // (its last readers passed the barrier of tile T-1 before anyone gets here)
-    float* ls = red + (((T & 1) * 2) + x) * 256;
-    ls[hf * 128 + r] = l2.x + l2.y;
-    named_bar_sync(bar_id, 64);
-    const float l = ls[r] + ls[128 + r];
-    if (T >= 1) {
-      tc::mbar_wait(&o_full[x], 0);
-      tc::fence_after_sync();
-    }
-    const int64_t row = static_cast<int64_t>(qpair) * 2 * BQ + x * BQ + r;
-    const float inv_l = 1.f / l;
-#pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
-      uint32_t o[32];
-      tc::tmem_ld32(tm_o + static_cast<uint32_t>(c * 32), o);
-      tc::tmem_ld_wait();
-      if (row < rows) {
-        uint4* dst = reinterpret_cast<uint4*>(out + row * ldo + head * kDh + hf * 64 + c * 32);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          dst[v] = make_uint4(pack_bf16(__uint_as_float(o[8 * v]) * inv_l, __uint_as_float(o[8 * v + 1]) * inv_l),
-                              pack_bf16(__uint_as_float(o[8 * v + 2]) * inv_l, __uint_as_float(o[8 * v + 3]) * inv_l),
-                              pack_bf16(__uint_as_float(o[8 * v + 4]) * inv_l, __uint_as_float(o[8 * v + 5]) * inv_l),
-                              pack_bf16(__uint_as_float(o[8 * v + 6]) * inv_l, __uint_as_float(o[8 * v + 7]) * inv_l));
-        }
-      }
-    }
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 1) {
-    tc::fence_after_sync();
-    tc::tmem_dealloc<512>(tmem);
   }
 }
 
@@ -1225,91 +641,40 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     launch_attn_simt(a, rows, st);
     return;
   }
-  set_smem_attr(k_attn_tc, SMEM_BYTES);
-  set_smem_attr(k_attn_pp<0>, PP_SMEM_BYTES);
-  set_smem_attr(k_attn_pp<1>, PP_SMEM_BYTES);
-  set_smem_attr(k_attn_pp<2>, PP_SMEM_BYTES);
-  set_smem_attr(k_attn_fa, FA_SMEM_BYTES);
-  set_smem_attr(k_attn_pp2<0>, P2_SMEM_BYTES);
-  set_smem_attr(k_attn_pp2<1>, P2_SMEM_BYTES);
-  set_smem_attr(k_attn_pp2<2>, P2_SMEM_BYTES);
-  set_smem_attr(k_attn_pp2<1, true>, P2_SMEM_BYTES);
-  AttnMaps maps;
-  maps.q = map_for(a.q, rows, H, a.ldq);
-  maps.k1 = map_for(a.k1, a.n1, H, a.ldk1);
-  maps.v1 = map_for(a.v1, a.n1, H, a.ldv1);
-  if (a.n0 > 0) {
-    maps.k0 = map_for(a.k0, a.n0, H, a.ldk0);
-    maps.v0 = map_for(a.v0, a.n0, H, a.ldv0);
-  } else {
-    maps.k0 = maps.k1;
-    maps.v0 = maps.v1;
-  }
+  if ((reinterpret_cast<uintptr_t>(a.out) | static_cast<uintptr_t>(a.ldo * 2)) % 16)
+    fail(BP_ERR_INTERNAL, "attention output must be 16-byte aligned");
   const float scale_log2 = a.scale * 1.4426950408889634f;
-  if (variant == 4) {  // k_attn_pp on a CTA pair (cta_group::2)
+  // K / V tensor maps of one segment; without a prefix the unused segment
+  // maps alias the current block's
+  auto seg_maps = [&](uint32_t k_box, uint32_t v_box, CUtensorMap* k0, CUtensorMap* v0, CUtensorMap* k1,
+                      CUtensorMap* v1) {
+    *k1 = map_for(a.k1, a.n1, H, a.ldk1, k_box);
+    *v1 = map_for(a.v1, a.n1, H, a.ldv1, v_box);
+    *k0 = a.n0 > 0 ? map_for(a.k0, a.n0, H, a.ldk0, k_box) : *k1;
+    *v0 = a.n0 > 0 ? map_for(a.v0, a.n0, H, a.ldv0, v_box) : *v1;
+  };
+  if (variant == 4) {  // k_attn_pp on a CTA pair (cta_group::2): each CTA stages 32 keys of K, half of V
+    set_smem_attr(k_attn_pp2<1>, P2_SMEM_BYTES);
     AttnMapsP2 pm;
-    pm.q = maps.q;
-    pm.k1 = map_for(a.k1, a.n1, H, a.ldk1, 32);
-    pm.v1 = map_for(a.v1, a.n1, H, a.ldv1, PBK);
-    if (a.n0 > 0) {
-      pm.k0 = map_for(a.k0, a.n0, H, a.ldk0, 32);
-      pm.v0 = map_for(a.v0, a.n0, H, a.ldv0, PBK);
-    } else {
-      pm.k0 = pm.k1;
-      pm.v0 = pm.v1;
-    }
+    pm.q = map_for(a.q, rows, H, a.ldq);
+    seg_maps(32, PBK, &pm.k0, &pm.v0, &pm.k1, &pm.v1);
+    pm.o = map_for(a.out, rows, H, a.ldo);
     const unsigned pairs = static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ));
     dim3 grid(pairs + (pairs & 1u), static_cast<unsigned>(a.heads));
-    // exp2 pairs in 8 on the FMA pipe (BP_ATTN_POLY overrides; default 1): the
-    // pair's softmax is latency-bound, so the polynomial pays only in small
-    // doses -- 1 in 8 beats all-MUFU (15.47-15.50 vs 15.68-15.69 s per video,
-    // same box twice) and 1 in 4 (16.22 s)
-    static const int poly2 = [] {
-      const char* e = std::getenv("BP_ATTN_POLY");
-      return e ? std::atoi(e) : 1;
-    }();
-    // epilogue: direct 16-byte stores (default) or smem + TMA stores
-    // (BP_ATTN_TMA_EPI=1): equal in the step (15.64-15.65 s either way), the
-    // direct stores 2-3% faster in isolation. The single-CTA kernel, which runs
-    // the short cross-attention, always stages through smem (0.48 -> 0.40 s).
-    static const bool tma_epi = [] {
-      const char* e = std::getenv("BP_ATTN_TMA_EPI");
-      return e && std::atoi(e) != 0;
-    }();
-    if ((reinterpret_cast<uintptr_t>(a.out) | static_cast<uintptr_t>(a.ldo * 2)) % 16)
-      fail(BP_ERR_INTERNAL, "attention output must be 16-byte aligned");
-    pm.o = map_for(a.out, rows, H, a.ldo);
-    auto kern = tma_epi ? k_attn_pp2<1, true> : (poly2 == 0 ? k_attn_pp2<0> : (poly2 == 2 ? k_attn_pp2<2> : k_attn_pp2<1>));
-    launch_pdl(kern, grid, dim3(PP_THREADS), P2_SMEM_BYTES, st, pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
-  } else if (variant == 3) {  // two Q tiles per CTA, 128-key tiles, one S buffer per tile
-    dim3 grid(static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(a.heads));
-    k_attn_fa<<<grid, FA_THREADS, FA_SMEM_BYTES, st>>>(maps, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
-  } else if (variant == 2) {  // ping-pong: 256 query rows per CTA, 64-key tiles
+    // one exp2 pair in 8 on the FMA pipe: the pair's softmax is latency-bound,
+    // so the polynomial pays only in small doses (1 in 8 beat all-MUFU and 1 in
+    // 4 in the power-capped step, round 1: 15.47 vs 15.68 vs 16.22 s / video)
+    launch_pdl(k_attn_pp2<1>, grid, dim3(PP_THREADS), P2_SMEM_BYTES, st, pm, rows, a.n0, a.n1, scale_log2, a.out,
+               a.ldo);
+  } else {  // single-CTA ping-pong: 256 query rows per CTA, 64-key tiles, TMA-store epilogue
+    set_smem_attr(k_attn_pp<1>, PP_SMEM_BYTES);
     AttnMapsPP pm;
-    pm.q = maps.q;
-    pm.k1 = map_for(a.k1, a.n1, H, a.ldk1, PBK);
-    pm.v1 = map_for(a.v1, a.n1, H, a.ldv1, PBK);
-    if (a.n0 > 0) {
-      pm.k0 = map_for(a.k0, a.n0, H, a.ldk0, PBK);
-      pm.v0 = map_for(a.v0, a.n0, H, a.ldv0, PBK);
-    } else {
-      pm.k0 = pm.k1;
-      pm.v0 = pm.v1;
-    }
-    if ((reinterpret_cast<uintptr_t>(a.out) | static_cast<uintptr_t>(a.ldo * 2)) % 16)
-      fail(BP_ERR_INTERNAL, "attention output must be 16-byte aligned");
+    pm.q = map_for(a.q, rows, H, a.ldq);
+    seg_maps(PBK, PBK, &pm.k0, &pm.v0, &pm.k1, &pm.v1);
     pm.o = map_for(a.out, rows, H, a.ldo);
     dim3 grid(static_cast<unsigned>((rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(a.heads));
-    // pairs of exp2 (out of 4) evaluated on the FMA pipe; BP_ATTN_POLY overrides (A/B runs)
-    static const int poly = [] {
-      const char* e = std::getenv("BP_ATTN_POLY");
-      return e ? std::atoi(e) : 1;
-    }();
-    auto kern = poly == 0 ? k_attn_pp<0> : (poly == 2 ? k_attn_pp<2> : k_attn_pp<1>);
-    launch_pdl(kern, grid, dim3(PP_THREADS), PP_SMEM_BYTES, st, pm, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
-  } else {
-    dim3 grid(static_cast<unsigned>((rows + BQ - 1) / BQ), static_cast<unsigned>(a.heads));
-    k_attn_tc<<<grid, kThreads, SMEM_BYTES, st>>>(maps, rows, a.n0, a.n1, scale_log2, a.out, a.ldo);
+    launch_pdl(k_attn_pp<1>, grid, dim3(PP_THREADS), PP_SMEM_BYTES, st, pm, rows, a.n0, a.n1, scale_log2, a.out,
+               a.ldo);
   }
   count_launch();
 }

@@ -1,15 +1,17 @@
 // tcgen05 GEMM for the DiT projections (K5a-K5f): C[M,N] = A[M,K] . W[N,K]^T
 // with bf16 operands, fp32 accumulation in TMEM and fused epilogues (bf16
-// store, erf-GELU, fp32 residual add). Two variants (launch_gemm_tc): the
-// default k_gemm_pair (2-CTA clusters sharing the weight tile, smem-transposed
-// epilogue; see its comment) and k_gemm_tc below. Persistent, one CTA per SM:
-//   warp 0      TMA producer (one elected lane) into a 4-stage smem ring
-//   warp 1      MMA issuer (one elected lane), 128x256x16 UMMA, TMEM alloc
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> global
+// store, erf-GELU, fp32 residual add by TMA reduce-add). One kernel,
+// k_gemm_pair: persistent 2-CTA clusters issuing one cta_group::2 MMA
+// (M = 256 x N = 256) per k-step (see its comment):
+//   warp 0      TMA producer (one elected lane) into a 6-stage smem ring
+//   warp 1      MMA issuer (leader CTA, one elected lane), TMEM alloc
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> smem -> global
 // Two 256-column TMEM accumulators let the epilogue of tile i overlap the
 // MMAs of tile i+1. K is consumed in a fixed ascending order and there is no
 // split-K, so every output row is computed identically wherever it sits in
-// M (the cached == recompute invariant).
+// M (the cached == recompute invariant). Losing variants of round
+// 1 (one CTA per tile; a multicast pair with two M = 128 MMAs per step) are
+// recorded in DESIGN.md and no longer built.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -28,10 +30,9 @@ namespace bp {
 
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int BM = 128, BN = 256, BK = 64;
 constexpr uint32_t A_BYTES = BM * BK * 2;
 constexpr uint32_t B_BYTES = BN * BK * 2;
-constexpr uint32_t SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
 constexpr int kThreads = 192;
 
 __device__ __forceinline__ float gelu_erf_f(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
@@ -62,161 +63,16 @@ __device__ __forceinline__ float2 gelu_erf_f2(float2 v) {
   return make_float2(v.x >= 0.f ? v.x - q.x : q.x, v.y >= 0.f ? v.y - q.y : q.y);
 }
 
-template <int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M, int N,
-              int K, void* __restrict__ Cv, int64_t ldc) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sa = smem;
-  uint8_t* sb = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sb + STAGES * B_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles = (N + BN - 1) / BN;
-  const int m_tiles = (M + BM - 1) / BM;
-  const int total = n_tiles * m_tiles;
-  const int num_k = (K + BK - 1) / BK;
-
-  if (warp == 0 && lane == 0) {
-    tc::tma_prefetch(&map_a);
-    tc::tma_prefetch(&map_b);
-    for (int s = 0; s < STAGES; ++s) {
-      tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], 128);
-    }
-    tc::fence_barrier_init();
-  }
-  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    // ---- TMA producer -----------------------------------------------------------
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const int m_blk = tile / n_tiles, n_blk = tile - m_blk * n_tiles;
-      for (int kb = 0; kb < num_k; ++kb) {
-        tc::mbar_wait(&empty[stage], phase ^ 1);
-        tc::mbar_arrive_expect_tx_elect(&full[stage], A_BYTES + B_BYTES);
-        tc::tma_load_2d_elect(sa + stage * A_BYTES, &map_a, &full[stage], kb * BK, m_blk * BM);
-        tc::tma_load_2d_elect(sb + stage * B_BYTES, &map_b, &full[stage], kb * BK, n_blk * BN);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-      }
-    }
-  } else if (warp == 1) {
-    // ---- MMA issuer ---------------------------------------------------------------
-    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc::fence_after_sync();
-      const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
-      for (int kb = 0; kb < num_k; ++kb) {
-        tc::mbar_wait(&full[stage], phase);
-        tc::fence_after_sync();
-        const uint32_t a0 = tc::smem_u32(sa + stage * A_BYTES);
-        const uint32_t b0 = tc::smem_u32(sb + stage * B_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint64_t ad = tc::desc_sw128(a0 + kk * 32, 1024, 16);
-          const uint64_t bd = tc::desc_sw128(b0 + kk * 32, 1024, 16);
-          tc::mma_bf16_ss_elect(d, ad, bd, idesc, (kb | kk) ? 1u : 0u);
-        }
-        tc::mma_commit_elect(&empty[stage]);  // smem slot free once these MMAs finish
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-      }
-      tc::mma_commit_elect(&tfull[acc]);  // accumulator ready
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
-    }
-  } else {
-    // ---- epilogue (warps 2..5 -> TMEM lane quarters 2,3,0,1) -----------------------------
-    const int q = warp & 3;
-    const int r_in = q * 32 + lane;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const int m_blk = tile / n_tiles, n_blk = tile - m_blk * n_tiles;
-      tc::mbar_wait(&tfull[acc], acc_phase);
-      tc::fence_after_sync();
-      const int row = m_blk * BM + r_in;
-      const bool row_ok = row < M;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tc::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c), r);
-        tc::tmem_ld_wait();
-        const int col = n_blk * BN + c;
-        if (!row_ok || col >= N) continue;
-        if (EPI == kGemmStoreBf16 || EPI == kGemmGeluBf16) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
-            if (EPI == kGemmGeluBf16) {
-              const float2 g = gelu_erf_f2(make_float2(x0, x1));
-              x0 = g.x;
-              x1 = g.y;
-            }
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
-            pk[i] = *reinterpret_cast<uint32_t*>(&h2);
-          }
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<bf16*>(Cv) + static_cast<int64_t>(row) * ldc + col);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
-        } else {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(Cv) + static_cast<int64_t>(row) * ldc + col);
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            float4 o = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                   __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-            if (EPI == kGemmResidualF32) {
-              const float4 old = dst[v];
-              o.x = old.x + o.x; o.y = old.y + o.y; o.z = old.z + o.z; o.w = old.w + o.w;
-            }
-            dst[v] = o;
-          }
-        }
-      }
-      tc::fence_before_sync();
-      tc::mbar_arrive(&tempty[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
-    }
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 1) {
-    tc::fence_after_sync();
-    tc::tmem_dealloc<512>(tmem_base);
-  }
-}
-
-// ---- cluster-pair variant -------------------------------------------------------------
+// ---- the cta_group::2 cluster pair ----------------------------------------------------
 // The two CTAs of a (2,1,1) cluster compute vertically adjacent 128x256 tiles
-// (m-blocks 2p, 2p+1) that share one weight tile. Each CTA loads its own A
-// tile and one half (128 rows) of the weight tile, multicast into both CTAs'
-// shared memory, so the L2->SM bytes per k-block and CTA drop from 48 KB to
-// 32 KB (the 128x256 tile alone needs ~96 B/cycle/SM at the MMA rate). A stage
-// is refilled only after both CTAs' MMAs consumed it: `empty` counts two
-// arrivals and every MMA commit is multicast to both CTAs. Row results do not
-// depend on which CTA computes them (same K order, no split-K), so cached ==
-// recompute still holds bitwise.
+// (m-blocks 2p, 2p+1) that share one weight tile, as ONE cta_group::2 MMA per
+// k-step, M = 256 (each CTA's 128 A rows) x N = 256 (each CTA stages its
+// 128-row half of the weight tile): 32 KB per stage and CTA, a 6-stage ring.
+// The leader CTA issues every MMA, both CTAs' TMA loads complete on the
+// leader's full barriers, every commit is multicast to both CTAs, and each
+// CTA's epilogue drains its own 128 accumulator rows and reports to the
+// leader's tempty barrier. Row results do not depend on which CTA computes
+// them (same K order, no split-K), so cached == recompute holds bitwise.
 //
 // Epilogue: each 32-row x 32-column chunk goes TMEM -> registers (thread =
 // row) -> a 4 KB per-warp smem slab (16-byte units XOR-swizzled by row) ->
@@ -224,29 +80,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 // 128-byte rows (4 rows fp32, 8 rows bf16) instead of 32 scattered 16-byte
 // pieces: the L1 work per tile drops 8x, which is what bounded the K = 1536
 // residual GEMMs.
-//
-// kCg2 (variant 3): the pair runs ONE cta_group::2 MMA per k-step, M = 256
-// (each CTA's 128 A rows) x N = 256 (each CTA stages its 128-row half of the
-// weight tile, no multicast): a stage is 32 KB instead of 48 KB, so the ring
-// holds 6 stages; the leader CTA issues every MMA, both CTAs' TMA loads
-// complete on the leader's full barriers, and each CTA's epilogue drains its
-// own 128 accumulator rows and reports to the leader's tempty barrier.
 constexpr uint32_t B_HALF = B_BYTES / 2;
-template <bool kCg2>
 struct PairLayout {
-  static constexpr int kStages = kCg2 ? 6 : STAGES;
-  static constexpr uint32_t kStageB = kCg2 ? B_HALF : B_BYTES;
+  static constexpr int kStages = 6;
+  static constexpr uint32_t kStageB = B_HALF;
   static constexpr uint32_t kStaging = (kStages * (A_BYTES + kStageB) + 256 + 1023) & ~1023u;  // after ring + mbarriers
   static constexpr uint32_t kSmem = kStaging + 2 * 4 * 4096 + 1024;  // two 4 KB slabs per epilogue warp
   static_assert(kSmem <= 232448, "pair GEMM exceeds the 227 KB smem limit");
 };
-constexpr uint32_t PAIR_SMEM_BYTES = PairLayout<false>::kSmem;
 
-template <int EPI, bool kCg2 = false>
+template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bh, int M, int N,
                 int K, void* __restrict__ Cv, int64_t ldc, const __grid_constant__ CUtensorMap map_c) {
-  using L = PairLayout<kCg2>;
+  using L = PairLayout;
   constexpr int kSt = L::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -273,18 +120,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc::tma_prefetch(&map_bh);
     for (int s = 0; s < kSt; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], kCg2 ? 1 : 2);  // the leader's MMA / both CTAs' MMAs
+      tc::mbar_init(&empty[s], 1);  // the leader's MMA commit (multicast)
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], kCg2 ? 8 : 128);  // cg2: one lane per epilogue warp of both CTAs
+      tc::mbar_init(&tempty[a], 8);  // one lane per epilogue warp of both CTAs
     }
     tc::fence_mbarrier_init_cluster();
   }
-  if (warp == 1) {
-    if (kCg2) tc::tmem_alloc_cg2<512>(tmem_slot);
-    else tc::tmem_alloc<512>(tmem_slot);
-  }
+  if (warp == 1) tc::tmem_alloc_cg2<512>(tmem_slot);
   tc::fence_before_sync();
   __syncthreads();
   tc::cluster_sync();  // barrier inits visible to the peer before any remote arrive / multicast
@@ -293,31 +137,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc::pdl_wait();  // A and the residual were produced by the previous kernel
 
   if (warp == 0) {
-    // ---- TMA producer: own A tile + own half of the shared weight tile (multicast) ----
+    // ---- TMA producer: own A tile + own half of the shared weight tile ----
     int stage = 0;
     uint32_t phase = 0;
     for (int pair = cluster; pair < total; pair += nclusters) {
       const int m_blk = (pair / n_tiles) * 2 + rank, n_blk = pair % n_tiles;
       for (int kb = 0; kb < num_k; ++kb) {
         tc::mbar_wait(&empty[stage], phase ^ 1);
-        if (kCg2) {  // own A rows + own weight half, both completing on the leader's barrier
-          const uint32_t lf = tc::mapa_shared(tc::smem_u32(&full[stage]), 0);
-          if (rank == 0) tc::mbar_arrive_expect_tx_elect(&full[stage], 2 * (A_BYTES + B_HALF));
-          tc::tma_load_2d_cg2_elect(sa + stage * A_BYTES, &map_a, lf, kb * BK, m_blk * BM);
-          tc::tma_load_2d_cg2_elect(sb + stage * L::kStageB, &map_bh, lf, kb * BK, n_blk * BN + rank * (BN / 2));
-        } else {
-          tc::mbar_arrive_expect_tx_elect(&full[stage], A_BYTES + B_BYTES);
-          tc::tma_load_2d_elect(sa + stage * A_BYTES, &map_a, &full[stage], kb * BK, m_blk * BM);
-          tc::tma_load_2d_multicast_elect(sb + stage * B_BYTES + rank * B_HALF, &map_bh, &full[stage], kb * BK,
-                                          n_blk * BN + rank * (BN / 2), kBoth);
-        }
+        // own A rows + own weight half, both completing on the leader's barrier
+        const uint32_t lf = tc::mapa_shared(tc::smem_u32(&full[stage]), 0);
+        if (rank == 0) tc::mbar_arrive_expect_tx_elect(&full[stage], 2 * (A_BYTES + B_HALF));
+        tc::tma_load_2d_cg2_elect(sa + stage * A_BYTES, &map_a, lf, kb * BK, m_blk * BM);
+        tc::tma_load_2d_cg2_elect(sb + stage * L::kStageB, &map_bh, lf, kb * BK, n_blk * BN + rank * (BN / 2));
         if (++stage == kSt) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer (cg2: the leader only) --------------------------------------------------
-    if (!kCg2 || rank == 0) {
-      constexpr uint32_t idesc = tc::idesc_bf16(kCg2 ? 2 * BM : BM, BN, 0, 0);
+    // ---- MMA issuer (the leader only) -------------------------------------------------------
+    if (rank == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(2 * BM, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -331,18 +169,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc::fence_after_sync();
           const uint32_t a0 = tc::smem_u32(sa + stage * A_BYTES);
           const uint32_t b0 = tc::smem_u32(sb + stage * L::kStageB);
-          if (kCg2) {
-            tc::mma_ss_k64_cg2_elect(d, tc::desc_sw128(a0, 1024, 16), tc::desc_sw128(b0, 1024, 16), idesc,
-                                     kb ? 1u : 0u);
-            tc::mma_commit_cg2_multicast_elect(&empty[stage], kBoth);
-          } else {
-            tc::mma_ss_k64_elect(d, tc::desc_sw128(a0, 1024, 16), tc::desc_sw128(b0, 1024, 16), idesc, kb ? 1u : 0u);
-            tc::mma_commit_multicast_elect(&empty[stage], kBoth);  // frees the stage in both CTAs
-          }
+          tc::mma_ss_k64_cg2_elect(d, tc::desc_sw128(a0, 1024, 16), tc::desc_sw128(b0, 1024, 16), idesc,
+                                   kb ? 1u : 0u);
+          tc::mma_commit_cg2_multicast_elect(&empty[stage], kBoth);  // frees the stage in both CTAs
           if (++stage == kSt) { stage = 0; phase ^= 1; }
         }
-        if (kCg2) tc::mma_commit_cg2_multicast_elect(&tfull[acc], kBoth);
-        else tc::mma_commit_elect(&tfull[acc]);
+        tc::mma_commit_cg2_multicast_elect(&tfull[acc], kBoth);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -442,12 +274,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         chunk(c + 32, old);
       }
       tc::fence_before_sync();
-      if (kCg2) {  // the leader's MMA reuses the accumulator once both CTAs drained it
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive_cluster(tc::mapa_shared(tc::smem_u32(&tempty[acc]), 0));
-      } else {
-        tc::mbar_arrive(&tempty[acc]);
-      }
+      __syncwarp();  // the leader's MMA reuses the accumulator once both CTAs drained it
+      if (lane == 0) tc::mbar_arrive_cluster(tc::mapa_shared(tc::smem_u32(&tempty[acc]), 0));
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -458,8 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc::cluster_sync();  // the peer may still multicast into / arrive on this CTA's shared memory until here
   if (warp == 1) {
     tc::fence_after_sync();
-    if (kCg2) tc::tmem_dealloc_cg2<512>(tmem_base);
-    else tc::tmem_dealloc<512>(tmem_base);
+    tc::tmem_dealloc_cg2<512>(tmem_base);
   }
 }
 
@@ -486,24 +313,15 @@ std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 
 std::atomic<int> g_sm_reserve{0};
 
-template <int EPI, bool kCg2 = false>
+template <int EPI>
 void launch_pair(const CUtensorMap& ma, const CUtensorMap& mbh, int M, int N, int K, void* C, int64_t ldc,
                  const CUtensorMap& mc, cudaStream_t st) {
-  set_smem_attr(k_gemm_pair<EPI, kCg2>, PairLayout<kCg2>::kSmem);
+  set_smem_attr(k_gemm_pair<EPI>, PairLayout::kSmem);
   const int pairs = (((M + BM - 1) / BM + 1) / 2) * ((N + BN - 1) / BN);
   const int avail = (kNumSms - g_sm_reserve.load(std::memory_order_relaxed)) / 2;
   const int clusters = pairs < avail ? pairs : avail;
-  launch_pdl(k_gemm_pair<EPI, kCg2>, dim3(2 * clusters), dim3(kThreads), PairLayout<kCg2>::kSmem, st, ma, mbh, M, N, K,
+  launch_pdl(k_gemm_pair<EPI>, dim3(2 * clusters), dim3(kThreads), PairLayout::kSmem, st, ma, mbh, M, N, K,
              C, ldc, mc);
-}
-
-template <int EPI>
-void launch_epi(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, void* C, int64_t ldc,
-                cudaStream_t st) {
-  set_smem_attr(k_gemm_tc<EPI>, SMEM_BYTES);
-  const int total = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = total < kNumSms ? total : kNumSms;
-  k_gemm_tc<EPI><<<grid, kThreads, SMEM_BYTES, st>>>(ma, mb, M, N, K, C, ldc);
 }
 
 }  // namespace
@@ -576,43 +394,25 @@ int sm_reserve() { return g_sm_reserve.load(); }
 
 void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C, int64_t ldc, int epi,
                     cudaStream_t st, int variant) {
+  (void)variant;  // one tcgen05 implementation (the SIMT check path is variant 0, see kernels_bf16.cu)
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15)
     fail(BP_ERR_INTERNAL, "GEMM operands must be 16-byte aligned");
   if ((lda * 2) % 16 || (K * 2) % 16 || N % 32 || ldc % 8)
     fail(BP_ERR_INTERNAL, "GEMM strides must be 16-byte multiples and N % 32 == 0");
   const CUtensorMap ma = cached_map(A, static_cast<uint64_t>(M), static_cast<uint64_t>(K), static_cast<uint64_t>(lda), BM, BK);
-  if (variant == 2 || variant == 3) {  // cluster pair sharing the weight tile (128-row weight boxes)
-    const CUtensorMap mbh =
-        cached_map(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(K), BN / 2, BK);
-    CUtensorMap mc = mbh;  // unused except by the residual epilogue
-    if (epi == kGemmResidualF32) {
-      if ((reinterpret_cast<uintptr_t>(C) & 15) || (ldc * 4) % 16) fail(BP_ERR_INTERNAL, "residual C must be 16-byte aligned");
-      mc = cached_map_f32(C, static_cast<uint64_t>(M), static_cast<uint64_t>(N), static_cast<uint64_t>(ldc), 32, 32);
-    }
-    if (variant == 3) {  // one cta_group::2 MMA (M = 256) per k-step
-      switch (epi) {
-        case kGemmStoreBf16: launch_pair<kGemmStoreBf16, true>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-        case kGemmGeluBf16: launch_pair<kGemmGeluBf16, true>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-        case kGemmResidualF32: launch_pair<kGemmResidualF32, true>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-        default: launch_pair<kGemmStoreF32, true>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-      }
-    } else {
-      switch (epi) {
-        case kGemmStoreBf16: launch_pair<kGemmStoreBf16>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-        case kGemmGeluBf16: launch_pair<kGemmGeluBf16>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-        case kGemmResidualF32: launch_pair<kGemmResidualF32>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-        default: launch_pair<kGemmStoreF32>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-      }
-    }
-    count_launch();
-    return;
+  // each CTA of the pair stages one 128-row half of the 256-row weight tile
+  const CUtensorMap mbh =
+      cached_map(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(K), BN / 2, BK);
+  CUtensorMap mc = mbh;  // unused except by the residual epilogue
+  if (epi == kGemmResidualF32) {
+    if ((reinterpret_cast<uintptr_t>(C) & 15) || (ldc * 4) % 16) fail(BP_ERR_INTERNAL, "residual C must be 16-byte aligned");
+    mc = cached_map_f32(C, static_cast<uint64_t>(M), static_cast<uint64_t>(N), static_cast<uint64_t>(ldc), 32, 32);
   }
-  const CUtensorMap mb = cached_map(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(K), BN, BK);
   switch (epi) {
-    case kGemmStoreBf16: launch_epi<kGemmStoreBf16>(ma, mb, M, N, K, C, ldc, st); break;
-    case kGemmGeluBf16: launch_epi<kGemmGeluBf16>(ma, mb, M, N, K, C, ldc, st); break;
-    case kGemmResidualF32: launch_epi<kGemmResidualF32>(ma, mb, M, N, K, C, ldc, st); break;
-    default: launch_epi<kGemmStoreF32>(ma, mb, M, N, K, C, ldc, st); break;
+    case kGemmStoreBf16: launch_pair<kGemmStoreBf16>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+    case kGemmGeluBf16: launch_pair<kGemmGeluBf16>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+    case kGemmResidualF32: launch_pair<kGemmResidualF32>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+    default: launch_pair<kGemmStoreF32>(ma, mbh, M, N, K, C, ldc, mc, st); break;
   }
   count_launch();
 }

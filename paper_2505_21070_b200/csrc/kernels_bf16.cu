@@ -326,22 +326,12 @@ void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int
 void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int variant);
 
 namespace {
-// GEMM: 0 = SIMT check path, 1 = tcgen05 one CTA per tile, 2 = tcgen05 cluster
-// pair sharing the weight tile, 3 = cta_group::2 pair (M = 256 MMAs). BP_GEMM_IMPL
-// overrides the default.
-int default_gemm_impl() {
-  const char* e = std::getenv("BP_GEMM_IMPL");
-  return e ? std::atoi(e) : 3;
-}
-int g_gemm_impl = default_gemm_impl();
-// 0 = SIMT check path, 1 = tcgen05 one Q tile/CTA, 2 = tcgen05 ping-pong, 3 = 128-key
-// tiles with one S buffer per tile, 4 = the ping-pong on a cta_group::2 pair.
-// BP_ATTN_IMPL overrides the default (A/B runs of the whole suite).
-int default_attn_impl() {
-  const char* e = std::getenv("BP_ATTN_IMPL");
-  return e ? std::atoi(e) : 4;
-}
-int g_attn_impl = default_attn_impl();
+// GEMM: 0 = the SIMT check path, otherwise the tcgen05 cta_group::2 pair.
+// Attention: 0 = SIMT check path, 2 = the single-CTA ping-pong kernel,
+// 4 = the ping-pong on a cta_group::2 pair (default). The kernel tests switch
+// them through bp_set_kernel_impl (libbp_cuda_test.so).
+int g_gemm_impl = 3;
+int g_attn_impl = 4;
 }  // namespace
 
 void set_gemm_impl(int impl) { g_gemm_impl = impl; }
@@ -366,14 +356,8 @@ void launch_attn_bf16_cross(const AttnBf16Args& a, int64_t rows, cudaStream_t st
   if (rows <= 0) return;
   // cross-attention over the 512-token context (8 key tiles) runs the
   // single-CTA ping-pong (variant 2): the pair's cluster setup does not pay
-  // off there (0.48 vs 0.51 s of cross-attention per video). BP_CROSS_IMPL
-  // overrides (-1: the self-attention variant).
-  static const int cross_impl = [] {
-    const char* e = std::getenv("BP_CROSS_IMPL");
-    return e ? std::atoi(e) : 2;
-  }();
-  const int impl = (cross_impl >= 0 && g_attn_impl >= 1) ? cross_impl : g_attn_impl;
-  if (impl >= 1) launch_attn_tc(a, rows, st, impl);
+  // off there (0.48 vs 0.51 s of cross-attention per video, round 1)
+  if (g_attn_impl >= 1) launch_attn_tc(a, rows, st, 2);
   else launch_attn_simt(a, rows, st);
 }
 

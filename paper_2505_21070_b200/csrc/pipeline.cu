@@ -653,8 +653,7 @@ void* Pipeline::alloc_ring_buffer(size_t bytes) {
 // staging, with identical results.
 void Pipeline::register_buffer(ncclComm_t comm, void* p, size_t bytes) {
   if (!comm || !p || d_.transport != BP_TRANSPORT_NCCL || !bp::nccl().CommRegister) return;
-  if (std::find(nccl_mem_.begin(), nccl_mem_.end(), p) == nccl_mem_.end() &&
-      std::getenv("BP_NCCL_REGISTER_ALL") == nullptr)
+  if (std::find(nccl_mem_.begin(), nccl_mem_.end(), p) == nccl_mem_.end())
     return;  // only cuMem (ncclMemAlloc) buffers qualify for NVLink zero-copy
   void* h = nullptr;
   if (bp::nccl().CommRegister(comm, p, bytes, &h) == ncclSuccess && h) {

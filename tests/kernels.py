@@ -93,6 +93,6 @@ def ref_attn(q, k, v, heads, dh, scale):
     return out
 
 
-# the library's default attention implementation (kernels_bf16.cu), restored after A/B tests
-DEFAULT_ATTN_IMPL = int(os.environ.get("BP_ATTN_IMPL", "4"))
-DEFAULT_GEMM_IMPL = int(os.environ.get("BP_GEMM_IMPL", "3"))
+# the library's default implementations (kernels_bf16.cu), restored after A/B tests
+DEFAULT_ATTN_IMPL = 4
+DEFAULT_GEMM_IMPL = 3

@@ -17,9 +17,9 @@ def lib(bp):
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 512, 128), (1000, 1536, 1536), (257, 4608, 256),
                                    (64, 96, 64), (130, 8960, 128)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
-@pytest.mark.parametrize("impl", [1, 2, 3])
+@pytest.mark.parametrize("impl", [3])
 def test_gemm_tcgen05(lib, M, N, K, epi, impl):
-    """impl 1: one CTA per 128x256 tile; impl 2: 2-CTA cluster sharing the weight tile (multicast)."""
+    """The cta_group::2 pair GEMM (one M = 256 MMA per k-step) vs fp64 numpy and the SIMT check kernel."""
     rng = np.random.default_rng(M * 7 + N + K + epi)
     A = to_bf16_bits(rng.standard_normal((M, K)))
     W = to_bf16_bits(rng.standard_normal((N, K)) / np.sqrt(K))
@@ -45,7 +45,7 @@ def test_gemm_tcgen05(lib, M, N, K, epi, impl):
     assert np.linalg.norm(g - c) / np.linalg.norm(c) < (5e-3 if epi in (0, 1) else 1e-5)
 
 
-@pytest.mark.parametrize("impl", [1, 2, 3])
+@pytest.mark.parametrize("impl", [3])
 def test_gemm_row_position_invariance(lib, impl):
     """A row's result does not depend on its M position (cached == recompute),
     nor on which GEMM implementation or cluster CTA computed it."""
@@ -59,21 +59,6 @@ def test_gemm_row_position_invariance(lib, impl):
     assert np.array_equal(full[333:333 + 97], part)
 
 
-@pytest.mark.parametrize("epi", [0, 2])
-def test_gemm_implementations_bitwise_equal(lib, epi):
-    """Both tcgen05 GEMMs run the same MMA sequence per tile: identical bits."""
-    rng = np.random.default_rng(11 + epi)
-    A = to_bf16_bits(rng.standard_normal((1000, 512)))
-    W = to_bf16_bits(rng.standard_normal((1536, 512)) / 20)
-    C0 = np.zeros((1000, 1536), dtype=np.uint16) if epi == 0 else rng.standard_normal((1000, 1536)).astype(np.float32)
-    out = []
-    for impl in (1, 2):
-        lib.bp_set_kernel_impl(impl, DEFAULT_ATTN_IMPL)
-        out.append(gemm(lib, A, W, C0, epi))
-    lib.bp_set_kernel_impl(DEFAULT_GEMM_IMPL, DEFAULT_ATTN_IMPL)
-    assert np.array_equal(out[0], out[1])
-
-
 def test_gemm_bench(lib):
     ms = __import__("ctypes").c_double()
     for (M, N, K) in [(18720, 4608, 1536), (18720, 8960, 1536), (18720, 1536, 8960)]:
@@ -82,14 +67,14 @@ def test_gemm_bench(lib):
         print(f"gemm {M}x{N}x{K}: {ms.value:.3f} ms  {tf:.0f} TFLOP/s")
 
 
-@pytest.mark.parametrize("impl", [1, 2, 3, 4])
+@pytest.mark.parametrize("impl", [2, 4])
 @pytest.mark.parametrize("rows,n0,n1,heads", [(128, 0, 128, 1), (300, 0, 300, 2), (300, 200, 300, 2),
                                               (257, 256, 129, 2), (96, 0, 512, 3), (1000, 640, 1000, 1),
                                               (513, 65, 63, 2), (256, 0, 1, 1), (40, 7, 100, 2),
                                               (512, 0, 1024, 2), (256, 512, 1024, 1), (300, 0, 512, 1)])
 def test_attention_tcgen05(lib, rows, n0, n1, heads, impl):
-    """impl 1: one 128-row Q tile per CTA; impl 2: ping-pong over two Q tiles, 64-key tiles;
-    impl 3: two Q tiles, 128-key tiles, one S buffer per tile; impl 4: impl 2 on a CTA pair."""
+    """impl 2: ping-pong over two Q tiles, 64-key tiles (the cross-attention kernel);
+    impl 4: the same schedule on a cta_group::2 CTA pair (the self-attention kernel)."""
     dh = 128
     rng = np.random.default_rng(rows + n0 * 3 + n1 + heads)
     H = heads * dh

@@ -1,8 +1,8 @@
 """Kernel micro-benchmarks through the self-test hooks (include/bp_cuda_test.h),
 used for A/B runs and ncu captures:
     python tools/bench_kernels.py attn|gemm|all [iters]
-The attention implementation follows BP_ATTN_IMPL (1 = one Q tile per CTA,
-2 = ping-pong over two Q tiles)."""
+Attention: the default launchers (self-attention: the cta_group::2 pair
+kernel; "cross": the stage's cross-attention launcher)."""
 import ctypes
 import os
 import sys
@@ -17,7 +17,7 @@ what = sys.argv[1] if len(sys.argv) > 1 else "attn"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 only = sys.argv[3] if len(sys.argv) > 3 else ""  # substring filter on the case tag
 ms = ctypes.c_double()
-impl = os.environ.get("BP_ATTN_IMPL", "4")
+impl = "default"
 if what in ("attn", "all"):
     # (rows, heads, dh, prefix n0, block n1): prefix pass, plain pass, cross-attention
     for rows, n0, n1, tag in ((18720, 6240, 18720, "self+prefix"), (18720, 0, 18720, "self"),
