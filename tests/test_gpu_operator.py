@@ -190,7 +190,12 @@ def test_cli_multiprocess_run_equals_single_process(tmp_path, transport):
     common = ["run", "--devices", "2", "--layers", "4", "--hidden", "256", "--heads", "2", "--channels", "16",
               "--height", "4", "--width", "6", "--context-len", "16", "--steps", "3", "--blocks", "3",
               "--precision", "bf16", "--mode", "single"]
-    single = subprocess.run([exe, *common, "--out", str(tmp_path / "one")], capture_output=True, text=True, timeout=300)
+    # the config echo in schedule.csv carries out_dir (artifacts.cpp), so both
+    # runs write to a relative "out" under their own working directory
+    (tmp_path / "one").mkdir()
+    (tmp_path / "multi").mkdir()
+    single = subprocess.run([exe, *common, "--out", "out"], capture_output=True, text=True, timeout=300,
+                            cwd=str(tmp_path / "one"))
     assert single.returncode == 0, single.stderr
     boot = tmp_path / "boot"
     boot.mkdir()
@@ -200,9 +205,10 @@ def test_cli_multiprocess_run_equals_single_process(tmp_path, transport):
         if transport == "nccl":  # both ranks share GPU 0: NCCL treats them as separate hosts
             env.update(NCCL_HOSTID=f"blockpipe-cli-{r}", NCCL_SOCKET_IFNAME="lo", NCCL_IB_DISABLE="1")
         procs.append(subprocess.Popen([exe, *common, "--transport", transport, "--rank", str(r), "--world", "2",
-                                       "--bootstrap-dir", str(boot), "--out", str(tmp_path / "multi")],
-                                      env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+                                       "--bootstrap-dir", str(boot), "--out", "out"],
+                                      env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                                      cwd=str(tmp_path / "multi")))
     logs = [p.communicate(timeout=600)[0] for p in procs]
     assert all(p.returncode == 0 for p in procs), logs
     for f in ("latents.bin", "schedule.csv", "transfers.json"):
-        assert (tmp_path / "multi" / f).read_bytes() == (tmp_path / "one" / f).read_bytes(), f
+        assert (tmp_path / "multi" / "out" / f).read_bytes() == (tmp_path / "one" / "out" / f).read_bytes(), f
