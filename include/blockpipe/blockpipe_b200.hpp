@@ -89,6 +89,7 @@ enum class Precision { kF64 = 0, kF32 = 1, kBF16 = 2 };
 struct ModelConfig {
   int layers = 4, hidden = 16, heads = 2, channels = 2, height = 2, width = 2, context_len = 4;
   int ffn = 0;                        // extension: 0 => 4 * hidden
+  bool wan_block = false;             // extension: the optional non-parity Wan2.1-style block (bp_block WAN)
   Precision precision = Precision::kF64;  // extension
   int device = 0;                     // extension
   int tokens_per_frame() const { return height * width; }

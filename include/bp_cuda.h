@@ -73,10 +73,20 @@ typedef enum {
  * written and polled by one-warp stream-ordered kernels. */
 typedef enum { BP_TRANSPORT_LOOPBACK = 0, BP_TRANSPORT_NCCL = 1, BP_TRANSPORT_IPC = 2 } bp_transport;
 
+/* Block variant. REFERENCE is the reference's block (LayerNorm + ln_affine,
+ * additive sinusoidal position / timestep embeddings, model.cpp:32-43,
+ * 155-169, 227-336) and the only one parity is judged on. WAN is an opt-in,
+ * non-parity extension: the Wan2.1 DiT block north_star names (adaLN
+ * modulation from a per-frame timestep MLP, gated residuals, RMS-normalised
+ * Q/K with 3D RoPE, tanh-GELU FFN, oracle/wan_oracle.py).
+ * WAN supports the resident K/V cache and no cache, not the recompute route. */
+typedef enum { BP_BLOCK_REFERENCE = 0, BP_BLOCK_WAN = 1 } bp_block;
+
 /* ModelConfig (model.hpp:21-32) + the defaulted FFN width extension. */
 typedef struct {
   int32_t layers, hidden, heads, channels, height, width, context_len;
-  int32_t ffn; /* 0 => 4*hidden, the reference's fixed width (model.cpp:98-99) */
+  int32_t ffn;   /* 0 => 4*hidden, the reference's fixed width (model.cpp:98-99) */
+  int32_t block; /* bp_block; 0 = the reference block */
 } bp_model_desc;
 
 /* PipelineConfig (engine.hpp:24-38) + QueueParams (block_queue.hpp:36-43). */

@@ -17,9 +17,15 @@ extern "C" {
 BP_API bp_status bp_set_kernel_impl(int32_t gemm_impl, int32_t attn_impl);
 
 /* C[M,N] (+)= A[M,K] . W[N,K]^T on the device, host buffers. A, W are bf16
- * bit patterns; C is bf16 (epi 0/1) or fp32 (epi 2/3), row stride ldc. */
+ * bit patterns; C is bf16 (epi 0/1/5) or fp32 (epi 2/3), row stride ldc. */
 BP_API bp_status bp_selftest_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int32_t epi,
                            const uint16_t* A, int64_t lda, const uint16_t* W, void* C, int64_t ldc);
+
+/* C[M,N] += gate[r / grp_rows][:] * (A . W^T) (fp32 C, the Wan gated residual
+ * epilogue); gate holds ngroups fp32 rows of N. */
+BP_API bp_status bp_selftest_gemm_gated(int32_t device, int32_t M, int32_t N, int32_t K, const uint16_t* A, int64_t lda,
+                                 const uint16_t* W, float* C, int64_t ldc, const float* gate, int32_t grp_rows,
+                                 int32_t ngroups);
 
 /* Attention of q rows against [k0/v0 (n0 rows) ++ k1/v1 (n1 rows)], bf16 bit
  * patterns, all with row stride heads*dh; out bf16 [rows, heads*dh]. */

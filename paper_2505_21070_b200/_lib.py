@@ -45,7 +45,7 @@ P = C.POINTER
 
 class ModelDesc(C.Structure):
     _fields_ = [("layers", i32), ("hidden", i32), ("heads", i32), ("channels", i32),
-                ("height", i32), ("width", i32), ("context_len", i32), ("ffn", i32)]
+                ("height", i32), ("width", i32), ("context_len", i32), ("ffn", i32), ("block", i32)]
 
 
 class PipelineDesc(C.Structure):

@@ -15,6 +15,7 @@ CACHE = {"off": 0, "on": 1, "recompute": 2}
 STRATEGIES = {"coordinated": 0, "complete-shuffle": 1, "subset": 2, "fresh": 3, "repeat": 4}
 PRECISIONS = {"f64": 0, "f32": 1, "bf16": 2}
 TRANSPORTS = {"loopback": 0, "nccl": 1, "ipc": 2}
+BLOCKS = {"reference": 0, "wan": 1}  # bp_block
 
 
 @dataclasses.dataclass
@@ -44,6 +45,7 @@ class PipelineConfig:
     check_cache: bool = False
     # B200 extensions
     ffn: int = 0                   # 0 => 4*hidden (model.cpp:98-99)
+    block: str = "reference"       # "wan": the optional non-parity Wan2.1-style block
     precision: str = "f64"
     transport: str = "loopback"
     uneven_split: bool = False
@@ -77,6 +79,10 @@ class PipelineConfig:
                 cfg.strategy = v
             elif k == "fault_inject":
                 cfg.fault_inject = bool(v)
+            elif k == "block":
+                if v not in BLOCKS:
+                    raise errors.ConfigError(f"block must be reference or wan, got {v}")
+                cfg.block = v
             elif k in ("out_dir", "emit_first_surplus", "format"):
                 pass  # operator-surface keys (artifacts / CLI), not part of the hot path
             elif k in {f.name for f in dataclasses.fields(cls)}:
@@ -86,8 +92,10 @@ class PipelineConfig:
         return cfg
 
     def model_desc(self) -> ModelDesc:
+        if self.block not in BLOCKS:
+            raise errors.ConfigError(f"block must be reference or wan, got {self.block}")
         return ModelDesc(self.layers, self.hidden, self.heads, self.channels, self.height,
-                         self.width, self.context_len, self.ffn)
+                         self.width, self.context_len, self.ffn, BLOCKS[self.block])
 
     def to_desc(self) -> PipelineDesc:
         d = PipelineDesc()

@@ -63,6 +63,22 @@ __device__ __forceinline__ float2 gelu_erf_f2(float2 v) {
   return make_float2(v.x >= 0.f ? v.x - q.x : q.x, v.y >= 0.f ? v.y - q.y : q.y);
 }
 
+// tanh-GELU (Wan FFN) on a pair: 0.5 x (1 + tanh(u)) = x / (1 + 2^(-2 u log2 e)),
+// u = sqrt(2/pi) (x + 0.044715 x^3); the exponential and the reciprocal on MUFU.
+__device__ __forceinline__ float2 gelu_tanh_f2(float2 v) {
+  const float2 v2 = __fmul2_rn(v, v);
+  const float2 inner = __ffma2_rn(v2, make_float2(0.044715f, 0.044715f), make_float2(1.f, 1.f));
+  // -2 sqrt(2/pi) log2(e) = -2.3022082
+  const float2 arg = __fmul2_rn(__fmul2_rn(v, inner), make_float2(-2.3022082f, -2.3022082f));
+  float2 e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(arg.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(arg.y));
+  const float2 den = __fadd2_rn(e, make_float2(1.f, 1.f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(den.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(den.y));
+  return __fmul2_rn(v, r);
+}
+
 // ---- the cta_group::2 cluster pair ----------------------------------------------------
 // The two CTAs of a (2,1,1) cluster compute vertically adjacent 128x256 tiles
 // (m-blocks 2p, 2p+1) that share one weight tile, as ONE cta_group::2 MMA per
@@ -92,7 +108,8 @@ struct PairLayout {
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bh, int M, int N,
-                int K, void* __restrict__ Cv, int64_t ldc, const __grid_constant__ CUtensorMap map_c) {
+                int K, void* __restrict__ Cv, int64_t ldc, const __grid_constant__ CUtensorMap map_c,
+                const GemmGate gate) {
   using L = PairLayout;
   constexpr int kSt = L::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -197,10 +214,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c), r);
         tc::tmem_ld_wait();
         const int col0 = n_blk * BN + c;
-        if (EPI == kGemmResidualF32) {
+        if (EPI == kGemmResidualF32 || EPI == kGemmResidualGatedF32) {
           // x += acc through a TMA reduce-add: the 32x32 fp32 chunk goes to a
           // 128B-swizzled slab (the tensor map's layout) and L2 performs the
           // read-modify-write, so the epilogue never waits on residual loads.
+          if (EPI == kGemmResidualGatedF32) {  // Wan: x += gate[frame] * acc
+            const int grow = row0 + lane < M ? row0 + lane : M - 1;
+            const float4* g4 = reinterpret_cast<const float4*>(
+                gate.gate + static_cast<int64_t>(grow / gate.grp_rows) * gate.grp_stride + col0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const float4 gv = col0 + 4 * u < N ? g4[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+              r[4 * u] = __float_as_uint(__uint_as_float(r[4 * u]) * gv.x);
+              r[4 * u + 1] = __float_as_uint(__uint_as_float(r[4 * u + 1]) * gv.y);
+              r[4 * u + 2] = __float_as_uint(__uint_as_float(r[4 * u + 2]) * gv.z);
+              r[4 * u + 3] = __float_as_uint(__uint_as_float(r[4 * u + 3]) * gv.w);
+            }
+          }
           const uint32_t sl = slab + static_cast<uint32_t>(red_buf * 4096);
           tc::bulk_wait_group_read<1>();  // the slab's previous reduce has read it
           __syncwarp();
@@ -218,13 +248,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           (void)old;
           return;
         }
-        if (EPI == kGemmStoreBf16 || EPI == kGemmGeluBf16) {
+        if (EPI == kGemmStoreBf16 || EPI == kGemmGeluBf16 || EPI == kGemmGeluTanhBf16) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
             if (EPI == kGemmGeluBf16) {
               const float2 g = gelu_erf_f2(make_float2(x0, x1));
+              x0 = g.x;
+              x1 = g.y;
+            } else if (EPI == kGemmGeluTanhBf16) {
+              const float2 g = gelu_tanh_f2(make_float2(x0, x1));
               x0 = g.x;
               x1 = g.y;
             }
@@ -279,7 +313,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (EPI == kGemmResidualF32) tc::bulk_wait_group<0>();  // this lane's reduce-adds are complete
+    if (EPI == kGemmResidualF32 || EPI == kGemmResidualGatedF32)
+      tc::bulk_wait_group<0>();  // this lane's reduce-adds are complete
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -315,13 +350,13 @@ std::atomic<int> g_sm_reserve{0};
 
 template <int EPI>
 void launch_pair(const CUtensorMap& ma, const CUtensorMap& mbh, int M, int N, int K, void* C, int64_t ldc,
-                 const CUtensorMap& mc, cudaStream_t st) {
+                 const CUtensorMap& mc, cudaStream_t st, const GemmGate& gate) {
   set_smem_attr(k_gemm_pair<EPI>, PairLayout::kSmem);
   const int pairs = (((M + BM - 1) / BM + 1) / 2) * ((N + BN - 1) / BN);
   const int avail = (kNumSms - g_sm_reserve.load(std::memory_order_relaxed)) / 2;
   const int clusters = pairs < avail ? pairs : avail;
   launch_pdl(k_gemm_pair<EPI>, dim3(2 * clusters), dim3(kThreads), PairLayout::kSmem, st, ma, mbh, M, N, K,
-             C, ldc, mc);
+             C, ldc, mc, gate);
 }
 
 }  // namespace
@@ -393,26 +428,31 @@ void set_sm_reserve(int sms) {
 int sm_reserve() { return g_sm_reserve.load(); }
 
 void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C, int64_t ldc, int epi,
-                    cudaStream_t st, int variant) {
-  (void)variant;  // one tcgen05 implementation (the SIMT check path is variant 0, see kernels_bf16.cu)
+                    cudaStream_t st, const GemmGate& gate) {
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(W)) & 15)
     fail(BP_ERR_INTERNAL, "GEMM operands must be 16-byte aligned");
   if ((lda * 2) % 16 || (K * 2) % 16 || N % 32 || ldc % 8)
     fail(BP_ERR_INTERNAL, "GEMM strides must be 16-byte multiples and N % 32 == 0");
+  const bool resid = epi == kGemmResidualF32 || epi == kGemmResidualGatedF32;
+  if (epi == kGemmResidualGatedF32 &&
+      ((reinterpret_cast<uintptr_t>(gate.gate) & 15) || gate.grp_stride % 4 || gate.grp_rows < 1))
+    fail(BP_ERR_INTERNAL, "gate table must be 16-byte aligned");
   const CUtensorMap ma = cached_map(A, static_cast<uint64_t>(M), static_cast<uint64_t>(K), static_cast<uint64_t>(lda), BM, BK);
   // each CTA of the pair stages one 128-row half of the 256-row weight tile
   const CUtensorMap mbh =
       cached_map(W, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(K), BN / 2, BK);
-  CUtensorMap mc = mbh;  // unused except by the residual epilogue
-  if (epi == kGemmResidualF32) {
+  CUtensorMap mc = mbh;  // unused except by the residual epilogues
+  if (resid) {
     if ((reinterpret_cast<uintptr_t>(C) & 15) || (ldc * 4) % 16) fail(BP_ERR_INTERNAL, "residual C must be 16-byte aligned");
     mc = cached_map_f32(C, static_cast<uint64_t>(M), static_cast<uint64_t>(N), static_cast<uint64_t>(ldc), 32, 32);
   }
   switch (epi) {
-    case kGemmStoreBf16: launch_pair<kGemmStoreBf16>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-    case kGemmGeluBf16: launch_pair<kGemmGeluBf16>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-    case kGemmResidualF32: launch_pair<kGemmResidualF32>(ma, mbh, M, N, K, C, ldc, mc, st); break;
-    default: launch_pair<kGemmStoreF32>(ma, mbh, M, N, K, C, ldc, mc, st); break;
+    case kGemmStoreBf16: launch_pair<kGemmStoreBf16>(ma, mbh, M, N, K, C, ldc, mc, st, gate); break;
+    case kGemmGeluBf16: launch_pair<kGemmGeluBf16>(ma, mbh, M, N, K, C, ldc, mc, st, gate); break;
+    case kGemmResidualF32: launch_pair<kGemmResidualF32>(ma, mbh, M, N, K, C, ldc, mc, st, gate); break;
+    case kGemmResidualGatedF32: launch_pair<kGemmResidualGatedF32>(ma, mbh, M, N, K, C, ldc, mc, st, gate); break;
+    case kGemmGeluTanhBf16: launch_pair<kGemmGeluTanhBf16>(ma, mbh, M, N, K, C, ldc, mc, st, gate); break;
+    default: launch_pair<kGemmStoreF32>(ma, mbh, M, N, K, C, ldc, mc, st, gate); break;
   }
   count_launch();
 }

@@ -18,7 +18,8 @@ namespace bp {
 __global__ void __launch_bounds__(256) k_ln_bf16(const float* __restrict__ x, int64_t ldx,
                                                  const float* __restrict__ g,
                                                  const float* __restrict__ b, int64_t rows, int n,
-                                                 bf16* __restrict__ y) {
+                                                 bf16* __restrict__ y, int grp_rows, int64_t grp_stride,
+                                                 float eps) {
   const int lane = threadIdx.x & 31;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= rows) return;
@@ -39,9 +40,10 @@ __global__ void __launch_bounds__(256) k_ln_bf16(const float* __restrict__ x, in
     q += (a * a + bb * bb) + (c * c + d * d);
   }
   for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-  const float inv = 1.0f / sqrtf(q / static_cast<float>(n) + 1e-5f);
-  const float4* g4 = reinterpret_cast<const float4*>(g);
-  const float4* b4 = reinterpret_cast<const float4*>(b);
+  const float inv = 1.0f / sqrtf(q / static_cast<float>(n) + eps);
+  const int64_t go = grp_stride ? (r / grp_rows) * grp_stride : 0;  // per-group (frame) affine: Wan modulation
+  const float4* g4 = reinterpret_cast<const float4*>(g + go);
+  const float4* b4 = reinterpret_cast<const float4*>(b + go);
   __nv_bfloat162* y2 = reinterpret_cast<__nv_bfloat162*>(y + r * n);
   for (int j = lane; j < n4; j += 32) {
     const float4 v = x4[j], gg = g4[j], bbv = b4[j];
@@ -60,7 +62,8 @@ __global__ void __launch_bounds__(256) k_ln_bf16(const float* __restrict__ x, in
 template <int NV>
 __global__ void __launch_bounds__(256) k_ln_bf16_reg(const float* __restrict__ x, int64_t ldx,
                                                      const float* __restrict__ g, const float* __restrict__ b,
-                                                     int64_t rows, int n, bf16* __restrict__ y) {
+                                                     int64_t rows, int n, bf16* __restrict__ y, int grp_rows,
+                                                     int64_t grp_stride, float eps) {
   // launched as a programmatic dependent of the residual GEMM: the CTAs are
   // resident before it ends and start reading x as soon as its writes land
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -83,9 +86,10 @@ __global__ void __launch_bounds__(256) k_ln_bf16_reg(const float* __restrict__ x
     q += (a * a + bb * bb) + (c * c + d * d);
   }
   for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-  const float inv = 1.0f / sqrtf(q / static_cast<float>(n) + 1e-5f);
-  const float4* g4 = reinterpret_cast<const float4*>(g);
-  const float4* b4 = reinterpret_cast<const float4*>(b);
+  const float inv = 1.0f / sqrtf(q / static_cast<float>(n) + eps);
+  const int64_t go = grp_stride ? (r / grp_rows) * grp_stride : 0;  // per-group (frame) affine: Wan modulation
+  const float4* g4 = reinterpret_cast<const float4*>(g + go);
+  const float4* b4 = reinterpret_cast<const float4*>(b + go);
   uint2* y2 = reinterpret_cast<uint2*>(y + r * n);
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
@@ -100,13 +104,14 @@ __global__ void __launch_bounds__(256) k_ln_bf16_reg(const float* __restrict__ x
   }
 }
 
-void launch_ln_bf16(const float* x, int64_t ldx, const float* g, const float* b, int64_t rows,
-                    int n, bf16* y, cudaStream_t st) {
+void launch_ln_bf16_grp(const float* x, int64_t ldx, const float* g, const float* b, int grp_rows,
+                        int64_t grp_stride, float eps, int64_t rows, int n, bf16* y, cudaStream_t st) {
   if (rows <= 0) return;
-  if (n % 4 != 0 || ldx % 4 != 0) fail(BP_ERR_CONFIG, "bf16 path needs hidden % 4 == 0");
+  if (n % 4 != 0 || ldx % 4 != 0 || grp_stride % 4 != 0) fail(BP_ERR_CONFIG, "bf16 path needs hidden % 4 == 0");
+  if (grp_stride && grp_rows < 1) fail(BP_ERR_INTERNAL, "LayerNorm groups need grp_rows >= 1");
   const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
   auto pdl = [&](auto kern) {  // programmatic dependent launch (overlaps the launch with the producer's tail)
-    launch_pdl(kern, dim3(blocks), dim3(256), 0, st, x, ldx, g, b, rows, n, y);
+    launch_pdl(kern, dim3(blocks), dim3(256), 0, st, x, ldx, g, b, rows, n, y, grp_rows, grp_stride, eps);
   };
   switch (n) {  // register-resident rows for the hidden sizes in use (Wan 1.3B / 14B, test models)
     case 128: pdl(k_ln_bf16_reg<1>); break;
@@ -114,9 +119,14 @@ void launch_ln_bf16(const float* x, int64_t ldx, const float* g, const float* b,
     case 512: pdl(k_ln_bf16_reg<4>); break;
     case 1536: pdl(k_ln_bf16_reg<12>); break;
     case 5120: pdl(k_ln_bf16_reg<40>); break;
-    default: k_ln_bf16<<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y); break;
+    default: k_ln_bf16<<<blocks, 256, 0, st>>>(x, ldx, g, b, rows, n, y, grp_rows, grp_stride, eps); break;
   }
   count_launch();
+}
+
+void launch_ln_bf16(const float* x, int64_t ldx, const float* g, const float* b, int64_t rows,
+                    int n, bf16* y, cudaStream_t st) {
+  launch_ln_bf16_grp(x, ldx, g, b, 1, 0, 1e-5f, rows, n, y, st);  // ln_affine, eps 1e-5 (model.cpp:13)
 }
 
 // ---- embeddings for the fp32 residual stream (bf16 / f32 modes) ----------------------
@@ -210,7 +220,7 @@ __device__ __forceinline__ float gelu_erf(float v) {
 // ---- SIMT check GEMM: C = A . W^T, fp32 accumulate, k ascending --------------------
 __global__ void __launch_bounds__(256) k_gemm_simt(const bf16* __restrict__ A, int64_t lda,
                                                    const bf16* __restrict__ W, int M, int N, int K,
-                                                   void* __restrict__ Cv, int64_t ldc, int epi) {
+                                                   void* __restrict__ Cv, int64_t ldc, int epi, GemmGate gate) {
   constexpr int BM = 64, BN = 64, BK = 16;
   __shared__ float As[BK][BM + 1];
   __shared__ float Ws[BK][BN + 1];
@@ -244,15 +254,19 @@ __global__ void __launch_bounds__(256) k_gemm_simt(const bf16* __restrict__ A, i
       if (epi == kGemmStoreBf16) static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(v);
       else if (epi == kGemmGeluBf16) static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(gelu_erf(v));
       else if (epi == kGemmResidualF32) static_cast<float*>(Cv)[o] += v;
+      else if (epi == kGemmResidualGatedF32)
+        static_cast<float*>(Cv)[o] += gate.gate[(gm / gate.grp_rows) * gate.grp_stride + gn] * v;
+      else if (epi == kGemmGeluTanhBf16)
+        static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(0.5f * v * (1.f + tanhf(0.7978845608f * (v + 0.044715f * v * v * v))));
       else static_cast<float*>(Cv)[o] = v;
     }
   }
 }
 
 void launch_gemm_simt(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C,
-                      int64_t ldc, int epi, cudaStream_t st) {
+                      int64_t ldc, int epi, cudaStream_t st, const GemmGate& gate) {
   dim3 grid((N + 63) / 64, (M + 63) / 64);
-  k_gemm_simt<<<grid, 256, 0, st>>>(A, lda, W, M, N, K, C, ldc, epi);
+  k_gemm_simt<<<grid, 256, 0, st>>>(A, lda, W, M, N, K, C, ldc, epi, gate);
   count_launch();
 }
 
@@ -322,7 +336,7 @@ void launch_attn_simt(const AttnBf16Args& a, int64_t rows, cudaStream_t st) {
 namespace bp {
 
 void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C, int64_t ldc,
-                    int epi, cudaStream_t st, int variant);
+                    int epi, cudaStream_t st, const GemmGate& gate);
 void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int variant);
 
 namespace {
@@ -340,10 +354,12 @@ void set_attn_impl(int impl) { g_attn_impl = impl; }
 int attn_impl() { return g_attn_impl; }
 
 void launch_gemm_bf16(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C, int64_t ldc,
-                      int epi, cudaStream_t st) {
+                      int epi, cudaStream_t st, const GemmGate& gate) {
   if (M <= 0 || N <= 0) return;
-  if (g_gemm_impl >= 1) launch_gemm_tc(A, lda, W, M, N, K, C, ldc, epi, st, g_gemm_impl);
-  else launch_gemm_simt(A, lda, W, M, N, K, C, ldc, epi, st);
+  if (epi == kGemmResidualGatedF32 && (!gate.gate || gate.grp_rows < 1))
+    fail(BP_ERR_INTERNAL, "gated residual GEMM needs a gate table");
+  if (g_gemm_impl >= 1) launch_gemm_tc(A, lda, W, M, N, K, C, ldc, epi, st, gate);
+  else launch_gemm_simt(A, lda, W, M, N, K, C, ldc, epi, st, gate);
 }
 
 void launch_attn_bf16(const AttnBf16Args& a, int64_t rows, cudaStream_t st) {

@@ -25,16 +25,30 @@ void launch_gemm_f32_tile(const float* A, int64_t lda, const float* B, int64_t l
                           int64_t ldc, bool residual, cudaStream_t st);
 void launch_ln_bf16(const float* x, int64_t ldx, const float* g, const float* b, int64_t rows,
                     int n, bf16* y, cudaStream_t st);
+// Same with a per-group affine (row r uses g/b + (r / grp_rows) * grp_stride;
+// grp_stride 0: one vector) and a given epsilon: the Wan block's modulated
+// LayerNorm (gain 1 + scale, bias shift per frame).
+void launch_ln_bf16_grp(const float* x, int64_t ldx, const float* g, const float* b, int grp_rows,
+                        int64_t grp_stride, float eps, int64_t rows, int n, bf16* y, cudaStream_t st);
 
 enum GemmEpi {
   kGemmStoreBf16 = 0,    // C bf16 = acc
   kGemmGeluBf16 = 1,     // C bf16 = gelu_erf(acc)           (ffn_sublayer, model.cpp:221-225)
   kGemmResidualF32 = 2,  // C fp32 = C + acc (x += sublayer)  (forward_chunk, model.cpp:325-331)
-  kGemmStoreF32 = 3      // C fp32 = acc
+  kGemmStoreF32 = 3,     // C fp32 = acc
+  kGemmResidualGatedF32 = 4,  // C fp32 = C + gate[row group] * acc (Wan gated residual)
+  kGemmGeluTanhBf16 = 5       // C bf16 = gelu_tanh(acc)           (Wan FFN)
+};
+// Per-row-group gate of kGemmResidualGatedF32: row r scales by
+// gate + (r / grp_rows) * grp_stride (one fp32 vector of N per group).
+struct GemmGate {
+  const float* gate = nullptr;
+  int grp_rows = 1;
+  int64_t grp_stride = 0;
 };
 // C[M,N] = A[M,K] (bf16, row stride lda) x W[N,K]^T (bf16, K-major weights).
 void launch_gemm_bf16(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C,
-                      int64_t ldc, int epi, cudaStream_t st);
+                      int64_t ldc, int epi, cudaStream_t st, const GemmGate& gate = GemmGate{});
 // Which GEMM implementation launch_gemm_bf16 uses: 1 = tcgen05 (default), 0 = SIMT check path.
 void set_gemm_impl(int impl);
 // SMs the persistent GEMM grids leave free (0 by default): the NCCL executor

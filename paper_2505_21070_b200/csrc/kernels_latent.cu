@@ -103,7 +103,8 @@ __global__ void k_elementwise(int op, const double* __restrict__ a, const double
                               double* __restrict__ out) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = op == 0 ? __dadd_rn(a[i], b[i]) : op == 1 ? __dsub_rn(a[i], b[i]) : __dmul_rn(a[i], s);
+    out[i] = op == 0 ? __dadd_rn(a[i], b[i]) : op == 1 ? __dsub_rn(a[i], b[i]) : op == 3 ? __dadd_rn(a[i], s)
+                                                                        : __dmul_rn(a[i], s);
 }
 
 void launch_elementwise(int op, const double* a, const double* b, int64_t n, double s, double* out, cudaStream_t st) {

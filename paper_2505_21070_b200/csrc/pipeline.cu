@@ -199,17 +199,8 @@ Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, c
         device_, d.model, d.seed_model, d.seed_context, sched.begins[static_cast<size_t>(j)],
         sched.ends[static_cast<size_t>(j)], d.precision, st_);
   }
-  if (rank_ == 0) {
-    const int M = d.num_b + d.num_c / 2;
-    pool_.alloc(static_cast<size_t>(M) * hwc_ * 8);
-    flags_.alloc(static_cast<size_t>(M) * M * 4);
-    int64_t at = 0;
-    for (const SchedBlock& b : sched.blocks) {
-      block_off_.push_back(at);
-      at += 3 * b.frames * hwc_;  // three state versions (current, previous, one older)
-    }
-    latents_.alloc(static_cast<size_t>(at) * 8);
-    payload_.alloc(static_cast<size_t>(sched.max_tokens) * C_ * 8);
+  {  // per-pass frame levels / ids (static schedule): rank 0 embeds with them; with the
+     // Wan block every stage needs them (modulation, RoPE)
     std::vector<int32_t> lv;
     std::vector<int64_t> fi;
     for (const SchedPass& p : sched.passes) {
@@ -221,6 +212,18 @@ Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, c
     pass_ids_.alloc(std::max<size_t>(fi.size(), 1) * 8);
     BP_CUDA(cudaMemcpy(pass_levels_.p, lv.data(), lv.size() * 4, cudaMemcpyHostToDevice));
     BP_CUDA(cudaMemcpy(pass_ids_.p, fi.data(), fi.size() * 8, cudaMemcpyHostToDevice));
+  }
+  if (rank_ == 0) {
+    const int M = d.num_b + d.num_c / 2;
+    pool_.alloc(static_cast<size_t>(M) * hwc_ * 8);
+    flags_.alloc(static_cast<size_t>(M) * M * 4);
+    int64_t at = 0;
+    for (const SchedBlock& b : sched.blocks) {
+      block_off_.push_back(at);
+      at += 3 * b.frames * hwc_;  // three state versions (current, previous, one older)
+    }
+    latents_.alloc(static_cast<size_t>(at) * 8);
+    payload_.alloc(static_cast<size_t>(sched.max_tokens) * C_ * 8);
     for (int64_t id : sched.emission) {
       double* h = nullptr;
       const size_t n = static_cast<size_t>(sched.blocks[static_cast<size_t>(id - 1)].frames * hwc_);
@@ -432,10 +435,8 @@ void Pipeline::emit_block(const SchedBlock& b, cudaStream_t st, bool to_host) {
 void Pipeline::before_stage(const SchedPass& p, int j, Stage& s, StageInput* in) {
   in->tokens = p.tokens;
   in->nframes = static_cast<int>(p.frame_levels.size());
-  if (rank_ == 0) {
-    in->d_levels = pass_levels_.as<int32_t>() + pass_off_[static_cast<size_t>(p.index)];
-    in->d_frame_ids = pass_ids_.as<int64_t>() + pass_off_[static_cast<size_t>(p.index)];
-  }
+  in->d_levels = pass_levels_.as<int32_t>() + pass_off_[static_cast<size_t>(p.index)];
+  in->d_frame_ids = pass_ids_.as<int64_t>() + pass_off_[static_cast<size_t>(p.index)];
   in->capture_frames = p.capture_frames;
   in->mode = d_.cache_mode;
   in->record_inputs = d_.check_cache && d_.cache_mode == BP_CACHE_CACHED;

@@ -73,6 +73,9 @@ void validate_model(const bp_model_desc& m) {
   if (m.height < 1 || m.width < 1) fail(BP_ERR_CONFIG, "token grid must be at least 1x1");
   if (m.context_len < 1) fail(BP_ERR_CONFIG, "context_len must be >= 1");
   if (m.ffn < 0) fail(BP_ERR_CONFIG, "ffn must be >= 0");
+  if (m.block != BP_BLOCK_REFERENCE && m.block != BP_BLOCK_WAN) fail(BP_ERR_CONFIG, "block must be reference or wan");
+  if (m.block == BP_BLOCK_WAN && ((m.hidden / m.heads) < 6 || (m.hidden / m.heads) % 2 != 0))
+    fail(BP_ERR_CONFIG, "wan block needs an even head dim of at least 6 (3D RoPE)");
 }
 
 namespace {
@@ -146,6 +149,8 @@ Schedule build_schedule(const bp_pipeline_desc& d) {
   if (d.order != BP_ORDER_REVERSE && d.order != BP_ORDER_SEQUENTIAL)
     fail(BP_ERR_CONFIG, "unknown order");
   if (d.cache_mode < 0 || d.cache_mode > 2) fail(BP_ERR_CONFIG, "unknown cache mode");
+  if (d.model.block == BP_BLOCK_WAN && (d.cache_mode == BP_CACHE_RECOMPUTE || d.check_cache))
+    fail(BP_ERR_CONFIG, "wan block supports cache modes on / off without the recompute audit");
 
   Schedule s;
   s.desc = d;

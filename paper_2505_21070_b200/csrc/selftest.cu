@@ -34,7 +34,8 @@ bp_status bp_selftest_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int3
                            int64_t lda, const uint16_t* W, void* C, int64_t ldc) {
   return bp::guarded([&] {
     BP_CUDA(cudaSetDevice(device));
-    const size_t cb = (epi == bp::kGemmStoreBf16 || epi == bp::kGemmGeluBf16) ? 2 : 4;
+    if (epi == bp::kGemmResidualGatedF32) bp::fail(BP_ERR_CONFIG, "gated epilogue: use bp_selftest_gemm_gated");
+    const size_t cb = (epi == bp::kGemmStoreBf16 || epi == bp::kGemmGeluBf16 || epi == bp::kGemmGeluTanhBf16) ? 2 : 4;
     bp::DevBuf da, dw, dc;
     da.alloc(static_cast<size_t>(M) * lda * 2);
     dw.alloc(static_cast<size_t>(N) * K * 2);
@@ -45,6 +46,27 @@ bp_status bp_selftest_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int3
     bp::launch_gemm_bf16(da.as<bp::bf16>(), lda, dw.as<bp::bf16>(), M, N, K, dc.p, ldc, epi, nullptr);
     BP_CUDA(cudaDeviceSynchronize());
     BP_CUDA(cudaMemcpy(C, dc.p, static_cast<size_t>(M) * ldc * cb, cudaMemcpyDeviceToHost));
+  });
+}
+
+bp_status bp_selftest_gemm_gated(int32_t device, int32_t M, int32_t N, int32_t K, const uint16_t* A, int64_t lda,
+                                 const uint16_t* W, float* C, int64_t ldc, const float* gate, int32_t grp_rows,
+                                 int32_t ngroups) {
+  return bp::guarded([&] {
+    BP_CUDA(cudaSetDevice(device));
+    bp::DevBuf da, dw, dc, dg;
+    da.alloc(static_cast<size_t>(M) * lda * 2);
+    dw.alloc(static_cast<size_t>(N) * K * 2);
+    dc.alloc(static_cast<size_t>(M) * ldc * 4);
+    dg.alloc(static_cast<size_t>(ngroups) * N * 4);
+    BP_CUDA(cudaMemcpy(da.p, A, static_cast<size_t>(M) * lda * 2, cudaMemcpyHostToDevice));
+    BP_CUDA(cudaMemcpy(dw.p, W, static_cast<size_t>(N) * K * 2, cudaMemcpyHostToDevice));
+    BP_CUDA(cudaMemcpy(dc.p, C, static_cast<size_t>(M) * ldc * 4, cudaMemcpyHostToDevice));
+    BP_CUDA(cudaMemcpy(dg.p, gate, static_cast<size_t>(ngroups) * N * 4, cudaMemcpyHostToDevice));
+    bp::launch_gemm_bf16(da.as<bp::bf16>(), lda, dw.as<bp::bf16>(), M, N, K, dc.p, ldc, bp::kGemmResidualGatedF32,
+                         nullptr, bp::GemmGate{dg.as<float>(), grp_rows, N});
+    BP_CUDA(cudaDeviceSynchronize());
+    BP_CUDA(cudaMemcpy(C, dc.p, static_cast<size_t>(M) * ldc * 4, cudaMemcpyDeviceToHost));
   });
 }
 
@@ -94,7 +116,8 @@ bp_status bp_selftest_attn_cross(int32_t device, int64_t rows, int32_t heads, in
 bp_status bp_bench_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int32_t epi, int32_t iters, double* ms) {
   return bp::guarded([&] {
     BP_CUDA(cudaSetDevice(device));
-    const size_t cb = (epi == bp::kGemmStoreBf16 || epi == bp::kGemmGeluBf16) ? 2 : 4;
+    if (epi == bp::kGemmResidualGatedF32) bp::fail(BP_ERR_CONFIG, "gated epilogue: use bp_selftest_gemm_gated");
+    const size_t cb = (epi == bp::kGemmStoreBf16 || epi == bp::kGemmGeluBf16 || epi == bp::kGemmGeluTanhBf16) ? 2 : 4;
     bp::DevBuf da, dw, dc;
     da.alloc(static_cast<size_t>(M) * K * 2);
     dw.alloc(static_cast<size_t>(N) * K * 2);

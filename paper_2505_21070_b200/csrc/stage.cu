@@ -7,6 +7,7 @@
 
 #include "kernels_bf16.cuh"
 #include "kernels_simt.cuh"
+#include "kernels_wan.cuh"
 #include "schedule.hpp"
 
 namespace bp {
@@ -18,6 +19,12 @@ enum Role : uint64_t {
   kWq = 0, kWk, kWv, kWo, kCq, kCk, kCv, kCo, kW1, kW2,
   kLn1G, kLn1B, kLn2G, kLn2B, kLn3G, kLn3B,
   kPatchify = 100, kHead = 101
+};
+// Wan-block roles (oracle/wan_oracle.py): per layer, and global ones keyed by
+// layer = L like kPatchify / kHead.
+enum WanRole : uint64_t {
+  kWanMod = 200, kWanQn, kWanKn, kWanCqn, kWanCkn,
+  kWanT1 = 210, kWanTb1, kWanT2, kWanTb2, kWanTp, kWanTpb, kWanHmod
 };
 
 size_t align256(size_t n) { return (n + 255) & ~static_cast<size_t>(255); }
@@ -39,6 +46,9 @@ Stage::Stage(int device, const bp_model_desc& m, uint64_t seed_model, uint64_t s
   C_ = m.channels;
   tpf_ = m.height * m.width;
   Lc_ = m.context_len;
+  wan_ = m.block == BP_BLOCK_WAN;
+  wan_rope_split(dh_, &wnt_, &wnh_);
+  if (wan_ && prec_ == BP_PREC_BF16 && F_ < 2 * h_) fail(BP_ERR_CONFIG, "wan block on the bf16 path needs ffn >= 2 hidden");
   if (prec_ == BP_PREC_BF16) {
     if (h_ % 64 != 0 || F_ % 64 != 0) fail(BP_ERR_CONFIG, "bf16 path needs hidden and ffn multiples of 64");
     if (dh_ % 16 != 0 || dh_ > 256) fail(BP_ERR_CONFIG, "bf16 path needs head dim % 16 == 0 and <= 256");
@@ -85,6 +95,19 @@ void Stage::build_weights(uint64_t seed_model, uint64_t seed_context) {
   size_t off_in = 0, off_out = 0;
   if (is_first()) { off_in = at; at += align256(static_cast<size_t>(C_) * h_ * 8); }
   if (is_last()) { off_out = at; at += align256(static_cast<size_t>(h_) * C_ * te); }
+  // Wan block: per-layer vectors [nl][10h], the timestep MLP, the head modulation (T)
+  const size_t H1 = static_cast<size_t>(h_);
+  size_t off_wanv = 0, off_t1 = 0, off_tb1 = 0, off_t2 = 0, off_tb2 = 0, off_tp = 0, off_tpb = 0, off_hmod = 0;
+  if (wan_) {
+    off_wanv = at; at += align256(static_cast<size_t>(nl) * 10 * H1 * te);
+    off_t1 = at; at += align256(kWanFreqDim * H1 * te);
+    off_tb1 = at; at += align256(H1 * te);
+    off_t2 = at; at += align256(H1 * H1 * te);
+    off_tb2 = at; at += align256(H1 * te);
+    off_tp = at; at += align256(6 * H1 * H1 * te);
+    off_tpb = at; at += align256(6 * H1 * te);
+    off_hmod = at; at += align256(2 * H1 * te);
+  }
   weights_.alloc(at);
   char* base = weights_.as<char>();
   lw_.resize(static_cast<size_t>(nl));
@@ -96,10 +119,16 @@ void Stage::build_weights(uint64_t seed_model, uint64_t seed_context) {
   }
   if (is_first()) w_in_ = base + off_in;
   if (is_last()) w_out_ = base + off_out;
+  if (wan_) {
+    wanv_ = base + off_wanv;
+    for (int l = 0; l < nl; ++l) lw_[static_cast<size_t>(l)].wan = base + off_wanv + static_cast<size_t>(l) * 10 * H1 * te;
+    wg_ = WanGlobal{base + off_t1, base + off_tb1, base + off_t2, base + off_tb2, base + off_tp, base + off_tpb,
+                    base + off_hmod};
+  }
 
   // Scratch: fp64 draw buffer, context, and the cross K|V weights for hoisting.
   const size_t max_numel = std::max({hF, hh, static_cast<size_t>(Lc_) * h_,
-                                     static_cast<size_t>(C_) * h_});
+                                     static_cast<size_t>(C_) * h_, wan_ ? 6 * hh : size_t{0}});
   DevBuf gen, ctx64;
   gen.alloc(max_numel * 8);
   ctx64.alloc(static_cast<size_t>(Lc_) * h_ * 8);
@@ -148,6 +177,41 @@ void Stage::build_weights(uint64_t seed_model, uint64_t seed_context) {
       draw(layer, r, H, H);
       place_side(w.ln, H, static_cast<int64_t>(r - kLn1G) * H);
     }
+    if (wan_) {  // [mod 6h | gq | gk | gcq | gck]; RMSNorm gains are 1 + draw
+      draw(layer, kWanMod, 6 * H, H);
+      place_side(w.wan, 6 * H, 0);
+      for (uint64_t r = kWanQn; r <= kWanCkn; ++r) {
+        draw(layer, r, H, H);
+        launch_elementwise(3, g, nullptr, H, 1.0, g, st);
+        place_side(w.wan, H, (6 + static_cast<int64_t>(r - kWanQn)) * H);
+      }
+    }
+  }
+  if (wan_) {  // the per-frame timestep MLP (every stage computes it) and the head modulation
+    const uint64_t L = static_cast<uint64_t>(m_.layers);
+    const int64_t H = h_;
+    draw(L, kWanT1, kWanFreqDim * H, kWanFreqDim); place_side(wg_.t1, kWanFreqDim * H, 0);
+    draw(L, kWanTb1, H, kWanFreqDim); place_side(wg_.tb1, H, 0);
+    draw(L, kWanT2, H * H, H); place_side(wg_.t2, H * H, 0);
+    draw(L, kWanTb2, H, H); place_side(wg_.tb2, H, 0);
+    draw(L, kWanTp, 6 * H * H, H); place_side(wg_.tp, 6 * H * H, 0);
+    draw(L, kWanTpb, 6 * H, H); place_side(wg_.tpb, 6 * H, 0);
+    draw(L, kWanHmod, 2 * H, H); place_side(wg_.hmod, 2 * H, 0);
+    if (prec_ == BP_PREC_BF16) {  // static RoPE tables of the token grid: (cos, sin)(pos * 10000^(-j / nh))
+      std::vector<float2> yt(static_cast<size_t>(m_.height) * wnh_), xt(static_cast<size_t>(m_.width) * wnh_);
+      for (int p = 0; p < std::max(m_.height, m_.width); ++p)
+        for (int j = 0; j < wnh_; ++j) {
+          const double a = p * std::pow(10000.0, -static_cast<double>(j) / wnh_);
+          const float2 cs = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+          if (p < m_.height) yt[static_cast<size_t>(p) * wnh_ + j] = cs;
+          if (p < m_.width) xt[static_cast<size_t>(p) * wnh_ + j] = cs;
+        }
+      wytab_.alloc(std::max<size_t>(yt.size(), 1) * sizeof(float2));
+      wxtab_.alloc(std::max<size_t>(xt.size(), 1) * sizeof(float2));
+      BP_CUDA(cudaMemcpyAsync(wytab_.p, yt.data(), yt.size() * sizeof(float2), cudaMemcpyHostToDevice, st));
+      BP_CUDA(cudaMemcpyAsync(wxtab_.p, xt.data(), xt.size() * sizeof(float2), cudaMemcpyHostToDevice, st));
+      BP_CUDA(cudaStreamSynchronize(st));  // the host vectors go out of scope
+    }
   }
   hoist_context(ctx64.as<double>());
   if (is_first()) {
@@ -166,6 +230,10 @@ void Stage::build_weights(uint64_t seed_model, uint64_t seed_context) {
   for (size_t i = 0; i < fr.size(); ++i) fr[i] = std::pow(10000.0, -2.0 * static_cast<double>(i) / h_);
   freq_.alloc(fr.size() * 8);
   BP_CUDA(cudaMemcpyAsync(freq_.p, fr.data(), fr.size() * 8, cudaMemcpyHostToDevice, st));
+  if (is_first() && prec_ == BP_PREC_F32 && wan_) {
+    winT_.alloc(static_cast<size_t>(C_) * h_ * 4);
+    launch_convert<double, float>(static_cast<const double*>(w_in_), winT_.as<float>(), static_cast<int64_t>(C_) * h_, st);
+  }
   if (is_first() && prec_ == BP_PREC_BF16) {
     w_in32_.alloc(static_cast<size_t>(C_) * h_ * 4);
     launch_convert<double, float>(static_cast<const double*>(w_in_), w_in32_.as<float>(),
@@ -201,15 +269,25 @@ void Stage::hoist_context(const double* ctx64) {
       if (prec_ == BP_PREC_F64) launch_place<double>(g, H, H, ckvT.as<double>() + off, 2 * H, 0, st);
       else launch_place<float>(g, H, H, ckvT.as<float>() + off, 2 * H, 0, st);
     }
+    // Wan block: the context keys are RMS-normalised (gain gck), no RoPE
     if (prec_ == BP_PREC_F64) {
       launch_matmul<double>(ctxT.as<double>(), H, ckvT.as<double>(), 2 * H, Lc_, 2 * h_, h_,
                             static_cast<double*>(w.ctx_kv), 2 * H, kEpiNone, nullptr, 0, st);
+      if (wan_)
+        launch_wan_qk<double>(static_cast<double*>(w.ctx_kv), 2 * H, Lc_, h_, heads_,
+                              static_cast<const double*>(w.wan) + 9 * H, 1, 0, nullptr, 1, 1, 0, st);
     } else if (prec_ == BP_PREC_F32) {
       launch_matmul<float>(ctxT.as<float>(), H, ckvT.as<float>(), 2 * H, Lc_, 2 * h_, h_,
                            static_cast<float*>(w.ctx_kv), 2 * H, kEpiNone, nullptr, 0, st);
+      if (wan_)
+        launch_wan_qk<float>(static_cast<float*>(w.ctx_kv), 2 * H, Lc_, h_, heads_,
+                             static_cast<const float*>(w.wan) + 9 * H, 1, 0, nullptr, 1, 1, 0, st);
     } else {
       launch_matmul<float>(ctxT.as<float>(), H, ckvT.as<float>(), 2 * H, Lc_, 2 * h_, h_, kvT.as<float>(), 2 * H,
                            kEpiNone, nullptr, 0, st);
+      if (wan_)
+        launch_wan_qk<float>(kvT.as<float>(), 2 * H, Lc_, h_, heads_, static_cast<const float*>(w.wan) + 9 * H, 1, 0,
+                             nullptr, 1, 1, 0, st);
       launch_convert<float, double>(kvT.as<float>(), g, static_cast<int64_t>(Lc_) * 2 * H, st);
       launch_place<bf16>(g, Lc_, 2 * H, static_cast<bf16*>(w.ctx_kv), 2 * H, 0, st);
     }
@@ -403,11 +481,278 @@ const void* Stage::forward(const StageInput& in) {
     if (f < 0 || f >= in.nframes) fail(BP_ERR_DIMENSION, "capture frame out of range");
   if (xs_.empty()) set_ring(1, in.tokens);
   if (in.slot < 0 || in.slot >= ring_depth()) fail(BP_ERR_INTERNAL, "residual ring slot out of range");
+  if (wan_) {
+    if (in.use_prev == 2 || in.use_prev == 4 || in.mode == BP_CACHE_RECOMPUTE || in.record_inputs)
+      fail(BP_ERR_CONFIG, "wan block supports the resident K/V cache and no cache, not the recompute route");
+    if (in.nframes > 0 && (!in.d_levels || !in.d_frame_ids))
+      fail(BP_ERR_CONFIG, "wan block needs the pass's frame levels and ids on every stage");
+    switch (prec_) {
+      case BP_PREC_F64: return forward_wan_simt<double>(in);
+      case BP_PREC_F32: return forward_wan_simt<float>(in);
+      default: return forward_wan_bf16(in);
+    }
+  }
   switch (prec_) {
     case BP_PREC_F64: return forward_simt<double>(in);
     case BP_PREC_F32: return forward_simt<float>(in);
     default: return forward_bf16(in);
   }
+}
+
+// ---- optional Wan2.1-style block (bp_block WAN; oracle/wan_oracle.py) ----------------------
+// Per pass: the timestep MLP for the pass's frames (e, e0 = SiLU(e) W_tp + b_tp)
+// and the modulation tables modt[l][f] = mod_l + e0_f (1 + scale chunks), the
+// head's hmt[f] = head_mod + e_f, and (bf16) the temporal RoPE table.
+template <typename T>
+void Stage::wan_pass_setup(const StageInput& in) {
+  const int nf = in.nframes, nl = end_ - begin_;
+  const int64_t H = h_;
+  const size_t sz = sizeof(T);
+  cudaStream_t st = stream_;
+  wsin_.reserve(static_cast<size_t>(nf) * kWanFreqDim * sz + 16);
+  wa_.reserve(static_cast<size_t>(nf) * H * sz + 16);
+  we_.reserve(static_cast<size_t>(nf) * H * sz + 16);
+  wes_.reserve(static_cast<size_t>(nf) * H * sz + 16);
+  we0_.reserve(static_cast<size_t>(nf) * 6 * H * sz + 16);
+  wmodt_.reserve(static_cast<size_t>(nl) * nf * 6 * H * sz + 16);
+  launch_wan_sinus<T>(in.d_levels, nf, wsin_.as<T>(), st);
+  launch_matmul<T>(wsin_.as<T>(), kWanFreqDim, static_cast<const T*>(wg_.t1), H, nf, h_, kWanFreqDim, wa_.as<T>(), H,
+                   kEpiNone, nullptr, 0, st);
+  launch_bias_act<T>(wa_.as<T>(), nf, h_, static_cast<const T*>(wg_.tb1), 1, nullptr, st);
+  launch_matmul<T>(wa_.as<T>(), H, static_cast<const T*>(wg_.t2), H, nf, h_, h_, we_.as<T>(), H, kEpiNone, nullptr, 0,
+                   st);
+  launch_bias_act<T>(we_.as<T>(), nf, h_, static_cast<const T*>(wg_.tb2), 0, wes_.as<T>(), st);
+  launch_matmul<T>(wes_.as<T>(), H, static_cast<const T*>(wg_.tp), 6 * H, nf, 6 * h_, h_, we0_.as<T>(), 6 * H,
+                   kEpiNone, nullptr, 0, st);
+  launch_bias_act<T>(we0_.as<T>(), nf, 6 * h_, static_cast<const T*>(wg_.tpb), 0, nullptr, st);
+  launch_wan_modt<T>(static_cast<const T*>(wanv_), 10 * H, nl, we0_.as<T>(), 6 * H, nf, h_, 6, false,
+                     wmodt_.as<T>(), st);
+  if (is_last()) {
+    whmt_.reserve(static_cast<size_t>(nf) * 2 * H * sz + 16);
+    launch_wan_modt<T>(static_cast<const T*>(wg_.hmod), 0, 1, we_.as<T>(), H, nf, h_, 2, true, whmt_.as<T>(), st);
+  }
+  if (prec_ == BP_PREC_BF16) {
+    wttab_.reserve(static_cast<size_t>(nf) * wnt_ * sizeof(float2) + 16);
+    launch_wan_rope_frames(in.d_frame_ids, nf, wnt_, wttab_.as<float2>(), st);
+  }
+}
+
+template <typename T>
+const void* Stage::forward_wan_simt(const StageInput& in) {
+  const int64_t S = in.tokens, H = h_;
+  const int64_t P = static_cast<int64_t>(in.capture_frames.size()) * tpf_;
+  const int nl = end_ - begin_, nf = in.nframes;
+  const bool new_cache = P > 0 && in.mode == BP_CACHE_CACHED;
+  ensure_workspace(S, P, new_cache, in.use_prev);
+  cudaStream_t st = stream_;
+  T* x = static_cast<T*>(xs_[static_cast<size_t>(in.slot)]);
+  T* ln = ln_.as<T>();
+  T* at = attn_.as<T>();
+  T* tmp = cq_.as<T>();
+  T* hm = hmid_.as<T>();
+  if (is_first()) {  // x = latents W_in: positions enter through RoPE, time through the modulation
+    const T* lat = static_cast<const T*>(in.payload);
+    const T* win = static_cast<const T*>(w_in_);
+    if (prec_ == BP_PREC_F32) {
+      wlat_.reserve(static_cast<size_t>(S) * C_ * sizeof(T));
+      launch_convert<double, T>(static_cast<const double*>(in.payload), wlat_.as<T>(), S * C_, st);
+      lat = wlat_.as<T>();
+      win = winT_.as<T>();
+    }
+    launch_matmul<T>(lat, C_, win, H, static_cast<int>(S), h_, C_, x, H, kEpiNone, nullptr, 0, st);
+  } else if (in.payload != x) {
+    BP_CUDA(cudaMemcpyAsync(x, in.payload, static_cast<size_t>(S * H) * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    ++input_copies_;
+  }
+  wan_pass_setup<T>(in);
+  const int64_t mstride = 6 * H;  // modulation table: frame stride
+  Entry nc;
+  T* qkv = qkv_.as<T>();
+  for (int li = 0; li < nl; ++li) {
+    const LayerW& w = lw_[static_cast<size_t>(li)];
+    const T* lnw = static_cast<const T*>(w.ln);
+    const T* wv = static_cast<const T*>(w.wan);
+    const T* mt = wmodt_.as<T>() + static_cast<int64_t>(li) * nf * mstride;
+    launch_ln_mod<T>(x, H, mt + H, mt, tpf_, mstride, S, h_, kWanEps, ln, H, st);
+    AttnArgs<T> a{};
+    if (in.use_prev == 1) {
+      a.k0 = static_cast<const T*>(cache_.k[static_cast<size_t>(li)]);
+      a.v0 = static_cast<const T*>(cache_.v[static_cast<size_t>(li)]);
+      a.ldk0 = a.ldv0 = cache_.ld;
+      a.n0 = cache_.tokens;
+    } else if (in.use_prev == 3) {
+      a.k0 = hostpre_.as<T>() + static_cast<int64_t>(li) * host_rows_ * 2 * H;
+      a.v0 = a.k0 + H;
+      a.ldk0 = a.ldv0 = 2 * H;
+      a.n0 = host_rows_;
+    }
+    launch_matmul<T>(ln, H, static_cast<const T*>(w.wqkv), 3 * H, static_cast<int>(S), 3 * h_, h_, qkv, 3 * H,
+                     kEpiNone, nullptr, 0, st);
+    launch_wan_qk<T>(qkv, 3 * H, S, h_, heads_, wv + 6 * H, 2, H, in.d_frame_ids, tpf_, m_.width, 1, st);
+    a.q = qkv; a.ldq = 3 * H;
+    a.k1 = qkv + H; a.ldk1 = 3 * H;
+    a.v1 = qkv + 2 * H; a.ldv1 = 3 * H;
+    a.n1 = S;
+    a.out = at; a.ldo = H;
+    a.dh = dh_;
+    a.scale = static_cast<T>(1.0 / std::sqrt(static_cast<double>(dh_)));
+    launch_attention<T>(a, S, heads_, st);
+    if (new_cache) capture_kv(in, li, qkv, sizeof(T), &nc);
+    launch_matmul<T>(at, H, static_cast<const T*>(w.wo), H, static_cast<int>(S), h_, h_, tmp, H, kEpiNone, nullptr, 0,
+                     st);
+    launch_gate_residual<T>(x, tmp, mt + 2 * H, tpf_, mstride, S, h_, st);
+    launch_ln_mod<T>(x, H, lnw + 2 * H, lnw + 3 * H, 1, 0, S, h_, kWanEps, ln, H, st);
+    launch_matmul<T>(ln, H, static_cast<const T*>(w.cq), H, static_cast<int>(S), h_, h_, tmp, H, kEpiNone, nullptr, 0,
+                     st);
+    launch_wan_qk<T>(tmp, H, S, h_, heads_, wv + 8 * H, 1, 0, nullptr, tpf_, m_.width, 0, st);
+    AttnArgs<T> c{};
+    c.q = tmp; c.ldq = H;
+    c.k1 = static_cast<const T*>(w.ctx_kv); c.ldk1 = 2 * H;
+    c.v1 = static_cast<const T*>(w.ctx_kv) + H; c.ldv1 = 2 * H;
+    c.n1 = Lc_;
+    c.out = at; c.ldo = H;
+    c.dh = dh_;
+    c.scale = a.scale;
+    launch_attention<T>(c, S, heads_, st);
+    launch_matmul<T>(at, H, static_cast<const T*>(w.co), H, static_cast<int>(S), h_, h_, x, H, kEpiResidual, x, H,
+                     st);
+    launch_ln_mod<T>(x, H, mt + 4 * H, mt + 3 * H, tpf_, mstride, S, h_, kWanEps, ln, H, st);
+    launch_matmul<T>(ln, H, static_cast<const T*>(w.w1), F_, static_cast<int>(S), F_, h_, hm, F_, kEpiNone, nullptr,
+                     0, st);
+    launch_gelu_tanh<T>(hm, S * F_, st);
+    launch_matmul<T>(hm, F_, static_cast<const T*>(w.w2), H, static_cast<int>(S), h_, F_, tmp, H, kEpiNone, nullptr,
+                     0, st);
+    launch_gate_residual<T>(x, tmp, mt + 5 * H, tpf_, mstride, S, h_, st);
+  }
+  cache_ = Entry{};
+  if (new_cache) { nc.valid = true; nc.tokens = P; cache_ = std::move(nc); }
+  rec_ = Entry{};
+  parity_ ^= 1;
+  (void)nf;
+  if (is_last()) {
+    const T* hmt = whmt_.as<T>();
+    launch_ln_mod<T>(x, H, hmt + H, hmt, tpf_, 2 * H, S, h_, kWanEps, ln, H, st);
+    T* eps = static_cast<T*>(es_[static_cast<size_t>(in.slot)]);
+    launch_matmul<T>(ln, H, static_cast<const T*>(w_out_), C_, static_cast<int>(S), C_, h_, eps, C_, kEpiNone, nullptr,
+                     0, st);
+    return eps;
+  }
+  return x;
+}
+
+const void* Stage::forward_wan_bf16(const StageInput& in) {
+  const int64_t S = in.tokens, H = h_;
+  const int64_t P = static_cast<int64_t>(in.capture_frames.size()) * tpf_;
+  const int nl = end_ - begin_, nf = in.nframes;
+  const bool new_cache = P > 0 && in.mode == BP_CACHE_CACHED;
+  ensure_workspace(S, P, new_cache, in.use_prev);
+  cudaStream_t st = stream_;
+  float* x = static_cast<float*>(xs_[static_cast<size_t>(in.slot)]);
+  bf16* ln = ln_.as<bf16>();
+  bf16* at = attn_.as<bf16>();
+  bf16* cq = cq_.as<bf16>();
+  bf16* hm = hmid_.as<bf16>();
+  if (is_first()) {  // x = latents W_in (fp32): positions enter through RoPE, time through the modulation
+    launch_convert<double, float>(static_cast<const double*>(in.payload), lat32_.as<float>(), S * C_, st);
+    launch_gemm_f32_tile(lat32_.as<float>(), C_, w_in32_.as<float>(), H, static_cast<int>(S), h_, C_, x, H, false, st);
+  } else if (in.payload != x) {
+    BP_CUDA(cudaMemcpyAsync(x, in.payload, static_cast<size_t>(S * H) * 4, cudaMemcpyDeviceToDevice, st));
+    ++input_copies_;
+  }
+  wan_pass_setup<float>(in);
+  const int64_t mstride = 6 * H;
+  const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(dh_)));
+  const float eps_ln = static_cast<float>(kWanEps);
+  const float2* tt = wttab_.as<float2>();
+  const float2* yt = wytab_.as<float2>();
+  const float2* xt = wxtab_.as<float2>();
+  Entry nc;
+  bf16* qkv = qkv_.as<bf16>();
+  for (int li = 0; li < nl; ++li) {
+    const LayerW& w = lw_[static_cast<size_t>(li)];
+    const float* lnw = static_cast<const float*>(w.ln);
+    const float* wv = static_cast<const float*>(w.wan);
+    const float* mt = wmodt_.as<float>() + static_cast<int64_t>(li) * nf * mstride;
+    prof_mark(3, true);
+    launch_ln_bf16_grp(x, H, mt + H, mt, tpf_, mstride, eps_ln, S, h_, ln, st);  // LN(x) (1 + sc1) + sh1
+    prof_mark(3, false);
+    AttnBf16Args a{};
+    if (in.use_prev == 1) {
+      a.k0 = static_cast<const bf16*>(cache_.k[static_cast<size_t>(li)]);
+      a.v0 = static_cast<const bf16*>(cache_.v[static_cast<size_t>(li)]);
+      a.ldk0 = a.ldv0 = cache_.ld;
+      a.n0 = cache_.tokens;
+    } else if (in.use_prev == 3) {
+      a.k0 = hostpre_.as<bf16>() + static_cast<int64_t>(li) * host_rows_ * 2 * H;
+      a.v0 = a.k0 + H;
+      a.ldk0 = a.ldv0 = 2 * H;
+      a.n0 = host_rows_;
+    }
+    prof_mark(2, true);
+    launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.wqkv), static_cast<int>(S), 3 * h_, h_, qkv, 3 * H,
+                     kGemmStoreBf16, st);
+    prof_mark(2, false);
+    prof_mark(3, true);
+    launch_wan_qk_bf16(qkv, 3 * H, S, h_, heads_, wv + 6 * H, 2, H, tt, yt, xt, tpf_, m_.width, 1, st);
+    prof_mark(3, false);
+    a.q = qkv; a.ldq = 3 * H;
+    a.k1 = qkv + H; a.ldk1 = 3 * H;
+    a.v1 = qkv + 2 * H; a.ldv1 = 3 * H;
+    a.n1 = S;
+    a.out = at; a.ldo = H;
+    a.heads = heads_; a.dh = dh_; a.scale = scale;
+    prof_mark(0, true);
+    launch_attn_bf16(a, S, st);
+    prof_mark(0, false);
+    if (new_cache) capture_kv(in, li, qkv, 2, &nc);
+    prof_mark(2, true);
+    launch_gemm_bf16(at, H, static_cast<const bf16*>(w.wo), static_cast<int>(S), h_, h_, x, H, kGemmResidualGatedF32,
+                     st, GemmGate{mt + 2 * H, tpf_, mstride});
+    prof_mark(2, false);
+    prof_mark(3, true);
+    launch_ln_bf16_grp(x, H, lnw + 2 * H, lnw + 3 * H, 1, 0, eps_ln, S, h_, ln, st);
+    prof_mark(3, false);
+    prof_mark(2, true);
+    launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.cq), static_cast<int>(S), h_, h_, cq, H, kGemmStoreBf16, st);
+    prof_mark(2, false);
+    prof_mark(3, true);
+    launch_wan_qk_bf16(cq, H, S, h_, heads_, wv + 8 * H, 1, 0, tt, yt, xt, tpf_, m_.width, 0, st);
+    prof_mark(3, false);
+    AttnBf16Args c{};
+    c.q = cq; c.ldq = H;
+    c.k1 = static_cast<const bf16*>(w.ctx_kv); c.ldk1 = 2 * H;
+    c.v1 = static_cast<const bf16*>(w.ctx_kv) + H; c.ldv1 = 2 * H;
+    c.n1 = Lc_;
+    c.out = at; c.ldo = H;
+    c.heads = heads_; c.dh = dh_; c.scale = scale;
+    prof_mark(1, true);
+    launch_attn_bf16_cross(c, S, st);
+    prof_mark(1, false);
+    prof_mark(2, true);
+    launch_gemm_bf16(at, H, static_cast<const bf16*>(w.co), static_cast<int>(S), h_, h_, x, H, kGemmResidualF32, st);
+    prof_mark(2, false);
+    prof_mark(3, true);
+    launch_ln_bf16_grp(x, H, mt + 4 * H, mt + 3 * H, tpf_, mstride, eps_ln, S, h_, ln, st);  // LN(x) (1 + sc2) + sh2
+    prof_mark(3, false);
+    prof_mark(2, true);
+    launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.w1), static_cast<int>(S), F_, h_, hm, F_, kGemmGeluTanhBf16, st);
+    launch_gemm_bf16(hm, F_, static_cast<const bf16*>(w.w2), static_cast<int>(S), h_, F_, x, H, kGemmResidualGatedF32,
+                     st, GemmGate{mt + 5 * H, tpf_, mstride});
+    prof_mark(2, false);
+  }
+  cache_ = Entry{};
+  if (new_cache) { nc.valid = true; nc.tokens = P; cache_ = std::move(nc); }
+  rec_ = Entry{};
+  parity_ ^= 1;
+  if (is_last()) {
+    const float* hmt = whmt_.as<float>();
+    float* hx = reinterpret_cast<float*>(hmid_.p);  // [S, h] fp32 fits the [S, F] bf16 buffer (F >= 2h)
+    launch_ln_mod<float>(x, H, hmt + H, hmt, tpf_, 2 * H, S, h_, kWanEps, hx, H, st);
+    float* eps = static_cast<float*>(es_[static_cast<size_t>(in.slot)]);
+    launch_gemm_f32_tile(hx, H, static_cast<const float*>(w_out_), C_, static_cast<int>(S), C_, h_, eps, C_, false, st);
+    return eps;
+  }
+  return x;
 }
 
 template <typename T>
@@ -768,5 +1113,7 @@ void Stage::prof_collect(double ms[4], int64_t launches[4]) {
 
 template const void* Stage::forward_simt<double>(const StageInput&);
 template const void* Stage::forward_simt<float>(const StageInput&);
+template const void* Stage::forward_wan_simt<double>(const StageInput&);
+template const void* Stage::forward_wan_simt<float>(const StageInput&);
 
 }  // namespace bp

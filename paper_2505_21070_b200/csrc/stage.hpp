@@ -104,6 +104,7 @@ class Stage {
     void* w2 = nullptr;     // SIMT: [F, h]; bf16: [h, F]
     void* ln = nullptr;     // 6 x [h]: ln1 g,b ln2 g,b ln3 g,b (T; fp32 on bf16 path)
     void* ctx_kv = nullptr; // hoisted cross-attention K|V [Lc, 2h] (T; bf16 on bf16 path)
+    void* wan = nullptr;    // Wan block: [mod 6h | gq h | gk h | gcq h | gck h] (T; fp32 on bf16 path)
   };
   struct Entry {  // resident KVCacheEntry or RecomputeEntry
     bool valid = false;
@@ -116,6 +117,15 @@ class Stage {
 
   template <typename T> const void* forward_simt(const StageInput& in);
   const void* forward_bf16(const StageInput& in);
+  // Optional Wan2.1-style block (bp_block WAN, non-parity)
+  template <typename T> void wan_pass_setup(const StageInput& in);
+  template <typename T> const void* forward_wan_simt(const StageInput& in);
+  const void* forward_wan_bf16(const StageInput& in);
+  bool wan_ = false;
+  int wnt_ = 0, wnh_ = 0;  // RoPE pairs per head: temporal, height (= width)
+  void* wanv_ = nullptr;   // [L_local][10h] per-layer Wan vectors (LayerW::wan points into it)
+  struct WanGlobal { void *t1, *tb1, *t2, *tb2, *tp, *tpb, *hmod; } wg_{};
+  DevBuf wsin_, wa_, we_, wes_, we0_, wmodt_, whmt_, wttab_, wytab_, wxtab_, wlat_, winT_;
   void build_weights(uint64_t seed_model, uint64_t seed_context);
   void hoist_context(const double* ctx64_device);
   uint64_t seed_model_ = 0;

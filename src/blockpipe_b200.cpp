@@ -46,6 +46,7 @@ bp_model_desc desc_of(const ModelConfig& c) {
   d.width = c.width;
   d.context_len = c.context_len;
   d.ffn = c.ffn;
+  d.block = c.wan_block ? BP_BLOCK_WAN : BP_BLOCK_REFERENCE;
   return d;
 }
 

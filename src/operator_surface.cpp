@@ -236,6 +236,11 @@ const std::map<std::string, Setter>& setters() {
       // B200 extensions (precision of the tensor-core path)
       {"precision", [](RunConfig& c, const ojson& v) { c.pipe.model.precision = parse_precision(v.get<std::string>()); }},
       {"ffn", [](RunConfig& c, const ojson& v) { c.pipe.model.ffn = v.get<int>(); }},
+      {"block", [](RunConfig& c, const ojson& v) {
+         const std::string b = v.get<std::string>();
+         if (b != "reference" && b != "wan") throw ConfigError("block must be reference or wan");
+         c.pipe.model.wan_block = b == "wan";
+       }},
       {"uneven_split", [](RunConfig& c, const ojson& v) { c.pipe.uneven_split = v.get<bool>(); }},
   };
   return t;
@@ -306,6 +311,7 @@ ojson config_object(const RunConfig& cfg) {
   j["format"] = cfg.format;
   if (p.model.precision != Precision::kF64) j["precision"] = precision_token(p.model.precision);
   if (p.model.ffn != 0) j["ffn"] = p.model.ffn;
+  if (p.model.wan_block) j["block"] = "wan";
   if (p.uneven_split) j["uneven_split"] = true;
   return j;
 }

@@ -15,6 +15,8 @@ TEST_SIGS = {
     "bp_last_error": (C.c_char_p, []),
     "bp_set_kernel_impl": (i32, [i32, i32]),
     "bp_selftest_gemm": (i32, [i32, i32, i32, i32, i32, C.c_void_p, i64, C.c_void_p, C.c_void_p, i64]),
+    "bp_selftest_gemm_gated": (i32, [i32, i32, i32, i32, C.c_void_p, i64, C.c_void_p, C.c_void_p, i64, C.c_void_p,
+                                     i32, i32]),
     "bp_selftest_attn": (i32, [i32, i64, i32, i32, C.c_void_p, C.c_void_p, C.c_void_p, i64, C.c_void_p,
                                C.c_void_p, i64, C.c_float, C.c_void_p]),
     "bp_selftest_attn_cross": (i32, [i32, i64, i32, i32, C.c_void_p, C.c_void_p, C.c_void_p, i64, C.c_float,
