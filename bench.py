@@ -373,7 +373,9 @@ def workload_config(w, n, sched, args):
             "num_b": w["num_b"], "num_c": w["num_c"], "steps": w["steps"], "blocks": w["blocks"],
             "frames": w["frames"], "passes": sched.npasses, "prefix_passes": sched.npasses - sched.rounds,
             "parallelism": f"layer-pipeline x{n}" + (f" ({args.transport})" if n > 1 else ""),
-            "l2": "inputs larger than L2 (18720x1536 activations per pass)"}
+            "l2": "inputs larger than L2 (18720x1536 activations per pass)",
+            **({"block": "wan (optional non-parity Wan2.1-style block)"} if getattr(args, "block", "reference") == "wan"
+               else {})}
 
 
 def ln_kernel_roofline(device, tokens, hidden, peaks):
@@ -411,6 +413,9 @@ def main():
                                                                 "wan14b"],
                     help="wan13-301 (default, every N): configs[2]; wan13-81: configs[1]; wan13-1025: the "
                          "configs[3] video at any N; wan14b: the configs[4] sample leg")
+    ap.add_argument("--block", default="reference", choices=["reference", "wan"],
+                    help="reference (the parity block, default) or wan: the optional non-parity Wan2.1-style block "
+                         "(adaLN modulation, RMSNorm + 3D RoPE on Q/K, gated residuals; a labelled extra)")
     args = ap.parse_args()
     if args.workload == "wan14b":
         return run_wan14b(args)
@@ -437,7 +442,7 @@ def main():
     cfg = bp.PipelineConfig(devices=n, precision="bf16", layers=w["layers"], hidden=w["hidden"], heads=w["heads"],
                             ffn=w["ffn"], channels=w["channels"], height=w["height"], width=w["width"],
                             context_len=w["context_len"], num_b=w["num_b"], num_c=w["num_c"], steps=w["steps"],
-                            blocks=w["blocks"], uneven_split=True,
+                            blocks=w["blocks"], uneven_split=True, block=args.block,
                             transport=args.transport if n > 1 else "loopback")
     sched = bp.Schedule(cfg)
     fl_video, n_prefix = video_flops(w, sched)

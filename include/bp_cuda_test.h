@@ -48,6 +48,11 @@ BP_API bp_status bp_bench_attn(int32_t device, int64_t rows, int32_t heads, int3
  * (fp32 [rows, n] -> bf16, the bf16 path's k_ln_bf16_reg). */
 BP_API bp_status bp_bench_ln(int32_t device, int64_t rows, int32_t n, int32_t iters, double* ms);
 
+/* Device time (ms per launch) of the Wan block's bf16 Q/K RMSNorm + 3D RoPE
+ * kernel over a [rows, 3h] QKV buffer (q and k parts, in place). */
+BP_API bp_status bp_bench_wan_qk(int32_t device, int64_t rows, int32_t h, int32_t heads, int32_t height,
+                                 int32_t width, int32_t iters, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,6 +8,7 @@
 
 #include "device.cuh"
 #include "kernels_wan.cuh"
+#include "tc_common.cuh"
 
 namespace bp {
 
@@ -203,6 +204,74 @@ __global__ void __launch_bounds__(256) k_wan_qk_bf16(bf16* __restrict__ base, in
   }
 }
 
+// Register-resident version for h % 256 == 0 and 32 % (dh / 8) == 0 (NV =
+// h / 256 16-byte chunks per lane): one global read of the row; lane l's
+// chunks l + 32 i all sit at the same offset inside their heads (32 is a
+// multiple of the dh / 8 chunks per head), so its four rotary pairs' (cos,
+// sin) are looked up once per row. Launched as a programmatic dependent of
+// the QKV / cross-Q GEMM.
+template <int NV>
+__global__ void __launch_bounds__(256) k_wan_qk_bf16_reg(bf16* __restrict__ base, int64_t ld, int64_t rows, int h,
+                                                        int dh, const float* __restrict__ g, int nparts,
+                                                        int64_t part_stride, const float2* __restrict__ ttab,
+                                                        const float2* __restrict__ ytab,
+                                                        const float2* __restrict__ xtab, int tpf, int width,
+                                                        int rope) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (wid >= rows * nparts) return;
+  const int64_t r = wid / nparts;
+  const int p = static_cast<int>(wid % nparts);
+  uint4* v = reinterpret_cast<uint4*>(base + r * ld + p * part_stride);
+  const float* gp = g + static_cast<int64_t>(p) * h;
+  uint4 u[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) u[i] = v[lane + 32 * i];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __bfloat1622float2(b2[q]);
+      s = fmaf(f.x, f.x, fmaf(f.y, f.y, s));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float inv = rsqrtf(s / static_cast<float>(h) + static_cast<float>(kWanEps));
+  float2 cs[4] = {make_float2(1.f, 0.f), make_float2(1.f, 0.f), make_float2(1.f, 0.f), make_float2(1.f, 0.f)};
+  if (rope) {
+    int nt, nh;
+    wan_rope_split(dh, &nt, &nh);
+    const int tok = static_cast<int>(r % tpf);
+    const int yy = tok / width, xx = tok % width;
+    const int j0 = (lane % (dh >> 3)) * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q;
+      cs[q] = j < nt ? ttab[(r / tpf) * nt + j]
+                     : (j < nt + nh ? ytab[static_cast<int64_t>(yy) * nh + j - nt]
+                                    : xtab[static_cast<int64_t>(xx) * nh + j - nt - nh]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + 32 * i;
+    __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&u[i]);
+    const float4 g0 = *reinterpret_cast<const float4*>(gp + 8 * c);
+    const float4 g1 = *reinterpret_cast<const float4*>(gp + 8 * c + 4);
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __bfloat1622float2(b2[q]);
+      const float a = f.x * inv * gg[2 * q], b = f.y * inv * gg[2 * q + 1];
+      b2[q] = __floats2bfloat162_rn(a * cs[q].x - b * cs[q].y, a * cs[q].y + b * cs[q].x);
+    }
+    v[c] = u[i];
+  }
+}
+
 __global__ void k_wan_rope_frames(const int64_t* __restrict__ frame_ids, int nframes, int nt, float2* __restrict__ ttab) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nframes * nt) return;
@@ -279,8 +348,22 @@ void launch_wan_qk_bf16(bf16* base, int64_t ld, int64_t rows, int h, int heads, 
                         int width, int rope, cudaStream_t st) {
   if (rows <= 0) return;
   if (h % 8 != 0 || ld % 8 != 0 || part_stride % 8 != 0) fail(BP_ERR_CONFIG, "wan qk kernel needs 16-byte rows");
-  k_wan_qk_bf16<<<blocks_for(rows * nparts, 8), 256, 0, st>>>(base, ld, rows, h, h / heads, g, nparts, part_stride,
-                                                               ttab, ytab, xtab, tpf, width, rope);
+  const int dh = h / heads;
+  const unsigned blocks = blocks_for(rows * nparts, 8);
+  auto reg = [&](auto kern) {
+    launch_pdl(kern, dim3(blocks), dim3(256), 0, st, base, ld, rows, h, dh, g, nparts, part_stride, ttab, ytab, xtab,
+               tpf, width, rope);
+  };
+  const bool lanes_fit = dh % 8 == 0 && 32 % (dh / 8) == 0;
+  switch (lanes_fit ? h : 0) {  // register-resident rows for the widths in use (Wan 1.3B / 14B, test models)
+    case 256: reg(k_wan_qk_bf16_reg<1>); break;
+    case 512: reg(k_wan_qk_bf16_reg<2>); break;
+    case 1536: reg(k_wan_qk_bf16_reg<6>); break;
+    case 5120: reg(k_wan_qk_bf16_reg<20>); break;
+    default:
+      k_wan_qk_bf16<<<blocks, 256, 0, st>>>(base, ld, rows, h, dh, g, nparts, part_stride, ttab, ytab, xtab, tpf,
+                                            width, rope);
+  }
   count_launch();
 }
 

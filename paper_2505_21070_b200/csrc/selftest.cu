@@ -6,6 +6,7 @@
 #include "bp_cuda_test.h"
 #include "device.cuh"
 #include "kernels_bf16.cuh"
+#include "kernels_wan.cuh"
 
 namespace bp {
 __global__ void k_fill_rand_bf16(bf16* p, int64_t n, uint64_t seed, float scale) {
@@ -201,6 +202,48 @@ bp_status bp_bench_ln(int32_t device, int64_t rows, int32_t n, int32_t iters, do
     BP_CUDA(cudaEventCreate(&e1));
     BP_CUDA(cudaEventRecord(e0, st));
     for (int i = 0; i < iters; ++i) bp::launch_ln_bf16(x.as<float>(), n, gp, gp + n, rows, n, y.as<bp::bf16>(), st);
+    BP_CUDA(cudaEventRecord(e1, st));
+    BP_CUDA(cudaEventSynchronize(e1));
+    float t = 0;
+    BP_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *ms = t / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+  });
+}
+
+bp_status bp_bench_wan_qk(int32_t device, int64_t rows, int32_t h, int32_t heads, int32_t height, int32_t width,
+                          int32_t iters, double* ms) {
+  return bp::guarded([&] {
+    BP_CUDA(cudaSetDevice(device));
+    int nt, nh;
+    bp::wan_rope_split(h / heads, &nt, &nh);
+    const int tpf = height * width;
+    const int nf = static_cast<int>((rows + tpf - 1) / tpf);
+    bp::DevBuf qkv, g, tt, yt, xt;
+    qkv.alloc(static_cast<size_t>(rows) * 3 * h * 2);
+    g.alloc(static_cast<size_t>(2 * h) * 4);
+    tt.alloc(static_cast<size_t>(nf) * nt * 8 + 8);
+    yt.alloc(static_cast<size_t>(height) * nh * 8 + 8);
+    xt.alloc(static_cast<size_t>(width) * nh * 8 + 8);
+    bp::k_fill_rand_bf16<<<1024, 256>>>(qkv.as<bp::bf16>(), rows * 3 * h, 5, 2.0f);
+    BP_CUDA(cudaMemset(g.p, 0x3f, static_cast<size_t>(2 * h) * 4));
+    BP_CUDA(cudaMemset(tt.p, 0, tt.bytes));
+    BP_CUDA(cudaMemset(yt.p, 0, yt.bytes));
+    BP_CUDA(cudaMemset(xt.p, 0, xt.bytes));
+    cudaStream_t st;
+    BP_CUDA(cudaStreamCreate(&st));
+    auto go = [&] {
+      bp::launch_wan_qk_bf16(qkv.as<bp::bf16>(), 3 * h, rows, h, heads, g.as<float>(), 2, h, tt.as<float2>(),
+                             yt.as<float2>(), xt.as<float2>(), tpf, width, 1, st);
+    };
+    for (int i = 0; i < 3; ++i) go();
+    cudaEvent_t e0, e1;
+    BP_CUDA(cudaEventCreate(&e0));
+    BP_CUDA(cudaEventCreate(&e1));
+    BP_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; ++i) go();
     BP_CUDA(cudaEventRecord(e1, st));
     BP_CUDA(cudaEventSynchronize(e1));
     float t = 0;

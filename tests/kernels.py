@@ -24,6 +24,7 @@ TEST_SIGS = {
     "bp_bench_gemm": (i32, [i32, i32, i32, i32, i32, i32, C.POINTER(f64)]),
     "bp_bench_attn": (i32, [i32, i64, i32, i32, i64, i64, i32, C.POINTER(f64)]),
     "bp_bench_ln": (i32, [i32, i64, i32, i32, C.POINTER(f64)]),
+    "bp_bench_wan_qk": (i32, [i32, i64, i32, i32, i32, i32, i32, C.POINTER(f64)]),
 }
 _testlib = None
 

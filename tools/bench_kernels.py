@@ -34,3 +34,12 @@ if what in ("gemm", "all"):
             continue
         assert lib.bp_bench_gemm(0, m, n, k, epi, iters, ctypes.byref(ms)) == 0
         print(f"gemm {tag:10s} {m}x{n}x{k} ms {ms.value:.4f} TF {2 * m * n * k / ms.value / 1e9:.1f}")
+if what in ("wan", "all"):
+    # the Wan block's Q/K RMSNorm + 3D RoPE (bf16, in place on the QKV buffer):
+    # algorithmic bytes = q and k read once and written once
+    rows, h = 18720, 1536
+    assert lib.bp_bench_wan_qk(0, rows, h, 12, 30, 52, iters, ctypes.byref(ms)) == 0
+    gb = 4 * rows * h * 2 / 1e9
+    print(f"wan qk-norm+rope {rows}x{h} ms {ms.value:.4f} GB/s {gb / ms.value * 1e3:.0f}")
+    assert lib.bp_bench_ln(0, rows, h, iters, ctypes.byref(ms)) == 0
+    print(f"ln (modulated form shares it) {rows}x{h} ms {ms.value:.4f} GB/s {rows * h * 6 / ms.value / 1e6:.0f}")
