@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256) k_wan_qk_bf16(bf16* __restrict__ base, in
 // sin) are looked up once per row. Launched as a programmatic dependent of
 // the QKV / cross-Q GEMM.
 template <int NV>
-__global__ void __launch_bounds__(256) k_wan_qk_bf16_reg(bf16* __restrict__ base, int64_t ld, int64_t rows, int h,
+__global__ void __launch_bounds__(256, (NV > 8 ? 1 : 3)) k_wan_qk_bf16_reg(bf16* __restrict__ base, int64_t ld, int64_t rows, int h,
                                                         int dh, const float* __restrict__ g, int nparts,
                                                         int64_t part_stride, const float2* __restrict__ ttab,
                                                         const float2* __restrict__ ytab,
