@@ -230,8 +230,6 @@ Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, c
       BP_CUDA(cudaMallocHost(&h, n * 8));
       pinned_.push_back(h);
     }
-  } else {
-    // non-zero ranks need the per-pass frame metadata only on stage 0 (rank 0)
   }
   if (d.transport == BP_TRANSPORT_NCCL && N > 1) {
     // NCCL's p2p kernels (a send, a receive, rank 0's eps receive) need SMs
