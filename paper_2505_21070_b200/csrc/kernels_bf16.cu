@@ -341,8 +341,8 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
 
 namespace {
 // GEMM: 0 = the SIMT check path, otherwise the tcgen05 cta_group::2 pair.
-// Attention: 0 = SIMT check path, 2 = the single-CTA ping-pong kernel,
-// 4 = the ping-pong on a cta_group::2 pair (default). The kernel tests switch
+// Attention: 0 = SIMT check path, 2 = the persistent single-CTA ping-pong
+// (cross-attention), 4 = the ping-pong on a cta_group::2 pair (default). The kernel tests switch
 // them through bp_set_kernel_impl (libbp_cuda_test.so).
 int g_gemm_impl = 3;
 int g_attn_impl = 4;
@@ -371,8 +371,8 @@ void launch_attn_bf16(const AttnBf16Args& a, int64_t rows, cudaStream_t st) {
 void launch_attn_bf16_cross(const AttnBf16Args& a, int64_t rows, cudaStream_t st) {
   if (rows <= 0) return;
   // cross-attention over the 512-token context (8 key tiles) runs the
-  // single-CTA ping-pong (variant 2): the pair's cluster setup does not pay
-  // off there (0.48 vs 0.51 s of cross-attention per video, round 1)
+  // persistent single-CTA ping-pong k_attn_ps (variant 2): 959 TF/s isolated
+  // vs 670 for the pair kernel and 821 for one item per CTA (round 2)
   if (g_attn_impl >= 1) launch_attn_tc(a, rows, st, 2);
   else launch_attn_simt(a, rows, st);
 }

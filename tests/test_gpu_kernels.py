@@ -73,8 +73,9 @@ def test_gemm_bench(lib):
                                               (513, 65, 63, 2), (256, 0, 1, 1), (40, 7, 100, 2),
                                               (512, 0, 1024, 2), (256, 512, 1024, 1), (300, 0, 512, 1)])
 def test_attention_tcgen05(lib, rows, n0, n1, heads, impl):
-    """impl 2: ping-pong over two Q tiles, 64-key tiles (the cross-attention kernel);
-    impl 4: the same schedule on a cta_group::2 CTA pair (the self-attention kernel)."""
+    """impl 2: the persistent single-CTA ping-pong over (query pair, head) items,
+    64-key tiles (the cross-attention kernel, k_attn_ps); impl 4: the same
+    schedule on a cta_group::2 CTA pair (the self-attention kernel, k_attn_pp2)."""
     dh = 128
     rng = np.random.default_rng(rows + n0 * 3 + n1 + heads)
     H = heads * dh
@@ -112,7 +113,7 @@ def test_attention_boundary_sweep(lib):
     """Tile-boundary sweep of the default kernels: rows around the 128-row
     query tile and the 256-row CTA pair, both key segments around the 64-key
     tile (self-attention, k_attn_pp2), and the key count alone for the
-    cross-attention launcher (k_attn_pp)."""
+    cross-attention launcher (k_attn_ps)."""
     from kernels import attn_cross
     dh, heads = 128, 1
     edges = (63, 64, 65, 127, 128, 129)

@@ -39,7 +39,7 @@ def kernels():
         attn(lib, q, k0, v0, k1, v1, 2, 128, 0.088)
     q = to_bf16_bits(rng.standard_normal((300, H)))
     kc, vc = to_bf16_bits(rng.standard_normal((512, H))), to_bf16_bits(rng.standard_normal((512, H)))
-    attn_cross(lib, q, kc, vc, 2, 128, 0.088)  # k_attn_pp (cross-attention)
+    attn_cross(lib, q, kc, vc, 2, 128, 0.088)  # k_attn_ps (cross-attention, persistent)
     import ctypes
     ms = ctypes.c_double()
     assert lib.bp_bench_ln(0, 300, 1536, 1, ctypes.byref(ms)) == 0  # k_ln_bf16_reg
