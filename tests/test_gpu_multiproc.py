@@ -107,3 +107,17 @@ def test_file_bootstrap_without_torch(bp, tmp_path, transport, prec, n):
         assert np.array_equal(got[f"run{r}"], ref)
     assert all(not s["torch_loaded"] for s in stats)
     assert all(s["boundary_copies"] == 0 for s in stats), stats
+
+
+@pytest.mark.parametrize("prec", ["f64", "bf16"])
+def test_ipc_pipeline_wan_block_equals_serial(bp, tmp_path, prec):
+    """The optional Wan block through the multi-process executor: every
+    stage, not only the first, consumes the pass's frame levels (adaLN
+    modulation) and frame ids (RoPE), so ranks > 0 need the per-pass metadata;
+    two IPC processes equal the single-process serial run bitwise."""
+    base = dict(layers=4, hidden=256, heads=2, channels=16, height=4, width=6, context_len=16, num_b=2, num_c=4,
+                steps=3, blocks=2, mode="single", precision=prec, block="wan")
+    want = bp.serial_oracle(base)
+    ref = np.concatenate([b["frames"].ravel() for b in want["blocks"]])
+    got = run_ranks(dict(base, devices=2, transport="ipc"), 2, tmp_path, runs=1)
+    assert np.array_equal(got["run0"], ref), prec

@@ -1,8 +1,8 @@
 """Kernel micro-benchmarks through the self-test hooks (include/bp_cuda_test.h),
 used for A/B runs and ncu captures:
     python tools/bench_kernels.py attn|gemm|all [iters]
-Attention: the default launchers (self-attention: the cta_group::2 pair
-kernel; "cross": the stage's cross-attention launcher)."""
+Attention: the stage's kernels (self-attention: the cta_group::2 pair
+kernel k_attn_pp2; "cross": the persistent cross-attention kernel k_attn_ps)."""
 import ctypes
 import os
 import sys
@@ -24,7 +24,11 @@ if what in ("attn", "all"):
                               (18720, 0, 512, "cross")):
         if only not in tag:
             continue
+        # bp_bench_attn times the attention launcher of the current implementation
+        # id: 4 = the self-attention pair kernel, 2 = the cross-attention kernel
+        lib.bp_set_kernel_impl(3, 2 if tag == "cross" else 4)
         assert lib.bp_bench_attn(0, rows, 12, 128, n0, n1, iters, ctypes.byref(ms)) == 0
+        lib.bp_set_kernel_impl(3, 4)
         tf = 4 * rows * (n0 + n1) * 1536 / ms.value / 1e9
         print(f"attn impl={impl} {tag:12s} ms {ms.value:.4f} TF {tf:.1f}")
 if what in ("gemm", "all"):
