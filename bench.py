@@ -378,6 +378,29 @@ def workload_config(w, n, sched, args):
                else {})}
 
 
+def attn_isolated_roofline(device, w, sched, peaks):
+    """The dominant kernel timed alone (the burst peak is its denominator):
+    20 back-to-back k_attn_pp2 launches at the workload's prefix-pass shape
+    (q = S, kv = P + S), CUDA events on the launching stream, through the
+    kernel self-test library (same objects as libbp_cuda.so). Inside the step
+    the same kernel runs under the power cap and is judged against the
+    sustained peak (roofline.frac)."""
+    import ctypes
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from kernels import load_testlib
+    tpf = w["height"] * w["width"]
+    S, P = (w["num_b"] + w["num_c"] // 2) * tpf, (w["num_c"] // 2) * tpf
+    dh = w["hidden"] // w["heads"]
+    ms = ctypes.c_double()
+    if load_testlib().bp_bench_attn(device, S, w["heads"], dh, P, S, 20, ctypes.byref(ms)) != 0:
+        return None
+    tf = 4 * S * (P + S) * w["hidden"] / (ms.value * 1e-3) / 1e12
+    return {"achieved": tf, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": tf / peaks["bf16_tflops"],
+            "peak_kind": "measured burst (kernel timed alone)", "us_per_launch": ms.value * 1e3,
+            "shape": f"q {S} x kv {P}+{S}, {w['heads']} heads, dh {dh}",
+            "timing": "20 back-to-back launches after the timed videos, CUDA events on the launching stream"}
+
+
 def ln_kernel_roofline(device, tokens, hidden, peaks):
     """LayerNorm (the elementwise path's largest kernel) from kernel time:
     back-to-back launches on [tokens, hidden] fp32 -> bf16 (larger than L2),
@@ -570,7 +593,8 @@ def main():
                      "share_of_step": attn_s / prof_video_s,
                      "gemm_tflops": None if prof["gemm_ms"] <= 0 else
                      (fl_video - attn_fl) / (prof["gemm_ms"] / 1e3) / 1e12,
-                     "whole_step_frac": fl_video / s_video / 1e12 / peak},
+                     "whole_step_frac": fl_video / s_video / 1e12 / peak,
+                     "isolated": attn_isolated_roofline(local, w, sched, peaks)},
         # north_star: the elementwise path against HBM bandwidth, from kernel time
         "elementwise_roofline": ln_kernel_roofline(local, tokens_per_pass, w["hidden"], peaks),
         # where the device time of a video goes (CUDA events around each class of

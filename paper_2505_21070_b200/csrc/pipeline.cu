@@ -1,9 +1,10 @@
 // run_pipeline (engine.cpp:255-497) on B200s: the host replays the static
 // schedule (schedule.cpp); rank 0 owns the block latents, the noise pool
 // and the Euler updates; stage j runs on rank j (NCCL transport, one process
-// per GPU) or all stages share one GPU (loopback). Hidden states move
-// between stages with ncclSend/ncclRecv on dedicated streams, double-buffered
-// and event-chained to compute, so transfers overlap the next pass.
+// per GPU; NCCL or CUDA-IPC transport) or all stages share one GPU
+// (loopback). Hidden states move between stages on dedicated streams from and
+// into a 3-slot residual ring (no boundary copies), event-chained to compute,
+// so transfers overlap the next pass.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include "nccl_dl.hpp"
