@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_2505_21070_b200 as bp  # noqa: E402
 
-w = bench.WORKLOADS[1]
+w = bench.WORKLOADS["wan13-81"]
 cfg = bp.PipelineConfig(devices=1, precision="bf16", layers=w["layers"], hidden=w["hidden"], heads=w["heads"],
                         ffn=w["ffn"], channels=w["channels"], height=w["height"], width=w["width"],
                         context_len=w["context_len"], num_b=w["num_b"], num_c=w["num_c"], steps=w["steps"],
