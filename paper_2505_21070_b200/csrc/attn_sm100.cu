@@ -738,7 +738,8 @@ void launch_attn_tc(const AttnBf16Args& a, int64_t rows, cudaStream_t st, int va
     seg_maps(PBK, PBK, &pm.k0, &pm.v0, &pm.k1, &pm.v1);
     pm.o = map_for(a.out, rows, H, a.ldo);
     const int64_t items = ((rows + 2 * BQ - 1) / (2 * BQ)) * a.heads;
-    const unsigned grid = static_cast<unsigned>(items < kNumSms ? items : kNumSms);
+    const int64_t avail = kNumSms - sm_reserve();  // SMs left to NCCL's kernels (multi-process NCCL runs)
+    const unsigned grid = static_cast<unsigned>(items < avail ? items : avail);
     // 1 exp2 pair in 8 on the FMA pipe (0, 1, 2, 3 in 8 measured within 1%)
     launch_pdl(k_attn_ps<1>, dim3(grid), dim3(PP_THREADS), PS_SMEM_BYTES, st, pm, rows, a.n0, a.n1, a.heads,
                scale_log2, a.out, a.ldo);

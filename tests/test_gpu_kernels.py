@@ -69,13 +69,15 @@ def test_gemm_bench(lib):
 
 @pytest.mark.parametrize("impl", [2, 4])
 @pytest.mark.parametrize("rows,n0,n1,heads", [(128, 0, 128, 1), (300, 0, 300, 2), (300, 200, 300, 2),
+                                              (511, 0, 512, 3), (513, 0, 512, 2), (1300, 0, 512, 5),
                                               (257, 256, 129, 2), (96, 0, 512, 3), (1000, 640, 1000, 1),
                                               (513, 65, 63, 2), (256, 0, 1, 1), (40, 7, 100, 2),
                                               (512, 0, 1024, 2), (256, 512, 1024, 1), (300, 0, 512, 1)])
 def test_attention_tcgen05(lib, rows, n0, n1, heads, impl):
     """impl 2: the persistent single-CTA ping-pong over (query pair, head) items,
-    64-key tiles (the cross-attention kernel, k_attn_ps); impl 4: the same
-    schedule on a cta_group::2 CTA pair (the self-attention kernel, k_attn_pp2)."""
+    64-key tiles (the cross-attention kernel, k_attn_ps); impl 4: the
+    ping-pong on a cta_group::2 CTA pair, one query pair per CTA (the
+    self-attention kernel, k_attn_pp2)."""
     dh = 128
     rng = np.random.default_rng(rows + n0 * 3 + n1 + heads)
     H = heads * dh
