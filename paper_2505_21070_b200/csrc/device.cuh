@@ -3,6 +3,7 @@
 
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdint>
@@ -21,6 +22,16 @@ constexpr uint64_t kGoldenDev = 0x9E3779B97F4A7C15ULL;
     if (e_ != cudaSuccess)                                                              \
       ::bp::fail(BP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
   } while (0)
+
+// NVTX range for the host scope (pass / stage / sublayer structure of the
+// reference's run_pipeline and forward_chunk in nsys and `ncu --nvtx`
+// timelines); header-only NVTX3, a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Counts our own kernel launches (reported as gpu_launches by bench.py).
 extern std::atomic<int64_t> g_launches;

@@ -73,6 +73,7 @@ class Pipeline {
   std::vector<int64_t> pass_off_;              // offset into pass_levels_/pass_ids_
   std::vector<double*> pinned_;                // emission buffers
   bool fault_pending_ = false;
+  bool failed_ = false;  // a multi-process run threw (see ~Pipeline)
   int64_t launches_at_start_ = 0;
   // NCCL
   ncclComm_t comm_prev_ = nullptr, comm_next_ = nullptr, comm_eps_ = nullptr;
@@ -321,6 +322,16 @@ Pipeline::Pipeline(const bp_pipeline_desc& d, int rank, int world, int device, c
 
 Pipeline::~Pipeline() {
   cudaSetDevice(device_);
+  if (failed_) {
+    // a run failed part-way (a peer may be gone): abort the communicators
+    // first, so NCCL kernels still waiting on a peer return, and never touch
+    // the aborted handles again (ncclCommAbort on error)
+    for (ncclComm_t* c : {&comm_prev_, &comm_next_, &comm_eps_}) {
+      if (*c && bp::nccl().CommAbort) bp::nccl().CommAbort(*c);
+      if (bp::nccl().CommAbort) *c = nullptr;
+    }
+    nccl_regs_.clear();
+  }
   cudaDeviceSynchronize();
   if (d_.transport == BP_TRANSPORT_NCCL && d_.devices > 1) set_sm_reserve(0);
   for (char* q : opened_) cudaIpcCloseMemHandle(q);
@@ -556,8 +567,19 @@ void Pipeline::run(bp_emit_fn emit, void* user) {
   for (auto& s : stages_)
     if (s) s->set_profiling(profiling);
   if (ipc() && !ipc_ready_) fail(BP_ERR_CONFIG, "IPC transport: bp_ipc_connect has not been called");
-  if (multi()) run_nccl(emit, user);
-  else run_rank0_loopback(emit, user);
+  {
+    NvtxRange range("run_pipeline");
+    if (multi()) {
+      try {
+        run_nccl(emit, user);
+      } catch (...) {
+        failed_ = true;  // the destructor aborts the NCCL communicators instead of destroying them
+        throw;
+      }
+    } else {
+      run_rank0_loopback(emit, user);
+    }
+  }
   stats.attn_ms = stats.gemm_ms = stats.cross_ms = stats.ln_ms = 0.0;
   stats.attn_launches = stats.gemm_launches = stats.cross_launches = stats.ln_launches = 0;
   for (auto& s : stages_) {
@@ -601,7 +623,12 @@ void Pipeline::run_rank0_loopback(bp_emit_fn emit, void* user) {
       StageInput in;
       before_stage(p, j, s, &in);
       in.payload = cur;
-      cur = s.forward(in);
+      {
+        char name[48];
+        std::snprintf(name, sizeof name, "pass %lld stage %d", static_cast<long long>(p.index), j);
+        NvtxRange range(name);
+        cur = s.forward(in);
+      }
       after_stage(p, j, s);
       if (j + 1 < N) boundary += p.tokens * d_.model.hidden * static_cast<int64_t>(s.act_bytes());
     }
@@ -707,6 +734,9 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
     in.slot = static_cast<int>(p.index % kRing);
     const int64_t i = p.index;
     if (i >= kRing && (j == 0 || last)) BP_CUDA(cudaStreamWaitEvent(st_, slot_free(i - kRing), 0));
+    char name[48];
+    std::snprintf(name, sizeof name, "pass %lld stage %d", static_cast<long long>(i), j);
+    NvtxRange range(name);
     const void* out = s.forward(in);
     after_stage(p, j, s);
     BP_CUDA(cudaEventRecord(ev_fwd[i], st_));

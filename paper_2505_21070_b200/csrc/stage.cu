@@ -903,6 +903,7 @@ const void* Stage::forward_bf16(const StageInput& in) {
                          dst + static_cast<int64_t>(f) * tpf_ * H, H * 4, tpf_, H * 4, st);
       nr.rec.push_back(dst);
     }
+    nvtxRangePushA("self_attention_sublayer");  // model.cpp:201-211
     prof_mark(3, true);
     launch_ln_bf16(x, H, lnw, lnw + H, S, h_, ln, st);
     prof_mark(3, false);
@@ -948,6 +949,8 @@ const void* Stage::forward_bf16(const StageInput& in) {
     launch_gemm_bf16(at, H, static_cast<const bf16*>(w.wo), static_cast<int>(S), h_, h_, x, H,
                      kGemmResidualF32, st);
     prof_mark(2, false);
+    nvtxRangePop();
+    nvtxRangePushA("cross_attention_sublayer");  // model.cpp:213-219
     prof_mark(3, true);
     launch_ln_bf16(x, H, lnw + 2 * H, lnw + 3 * H, S, h_, ln, st);
     prof_mark(3, false);
@@ -969,6 +972,8 @@ const void* Stage::forward_bf16(const StageInput& in) {
     launch_gemm_bf16(at, H, static_cast<const bf16*>(w.co), static_cast<int>(S), h_, h_, x, H,
                      kGemmResidualF32, st);
     prof_mark(2, false);
+    nvtxRangePop();
+    nvtxRangePushA("ffn_sublayer");  // model.cpp:221-225
     prof_mark(3, true);
     launch_ln_bf16(x, H, lnw + 4 * H, lnw + 5 * H, S, h_, ln, st);
     prof_mark(3, false);
@@ -978,6 +983,7 @@ const void* Stage::forward_bf16(const StageInput& in) {
     launch_gemm_bf16(hm, F_, static_cast<const bf16*>(w.w2), static_cast<int>(S), h_, F_, x, H,
                      kGemmResidualF32, st);
     prof_mark(2, false);
+    nvtxRangePop();
   }
   cache_ = Entry{};
   if (new_cache) { nc.valid = true; nc.tokens = P; cache_ = std::move(nc); }
