@@ -78,3 +78,22 @@ def test_compute_entry_points_fail_loudly_without_gpu(bp):
     from paper_2505_21070_b200 import operator
     code, out, err = operator.cli_main(["run", "--out", "/tmp/bp_nogpu_run"])
     assert (code, out) == (1, "") and "no CUDA device" in err, err
+
+
+def test_integration_binding_stub_matches_the_abi():
+    """The ctypes stub INTEGRATION.md section 3 shows a maintainer has the
+    exact field layout of bp_pipeline_desc / bp_model_desc (the full binding
+    is paper_2505_21070_b200/_lib.py)."""
+    import ctypes as C
+    import re
+    from paper_2505_21070_b200 import _lib
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    code = text.split("## 3.")[1].split("```python")[1].split("```")[0]
+    defs = code[code.index("class ModelDesc"):code.index("EMIT =")]
+    ns = {"C": C}
+    exec(defs, ns)
+    for stub, real in ((ns["ModelDesc"], _lib.ModelDesc), (ns["PipelineDesc"], _lib.PipelineDesc)):
+        assert [f[0] for f in stub._fields_] == [f[0] for f in real._fields_]
+        assert C.sizeof(stub) == C.sizeof(real)
+    assert re.search(r"ModelDesc\(([^)]*)\)", code.split("EMIT =")[1]).group(1).count(",") + 1 == \
+        len(_lib.ModelDesc._fields_)
