@@ -272,6 +272,82 @@ __global__ void __launch_bounds__(256, (NV > 8 ? 1 : 3)) k_wan_qk_bf16_reg(bf16*
   }
 }
 
+// Both parts of a row (q and k, adjacent in the QKV buffer: part_stride ==
+// h) in one warp: twice the bytes in flight per warp, two independent
+// sum-of-squares chains, and the rotary (cos, sin) looked up once for both,
+// since q and k of a row share the token's position.
+template <int NV>
+__global__ void __launch_bounds__(256, 2) k_wan_qk2_bf16_reg(bf16* __restrict__ base, int64_t ld, int64_t rows, int h,
+                                                           int dh, const float* __restrict__ g,
+                                                           const float2* __restrict__ ttab,
+                                                           const float2* __restrict__ ytab,
+                                                           const float2* __restrict__ xtab, int tpf, int width,
+                                                           int rope) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int lane = threadIdx.x & 31;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  uint4* v = reinterpret_cast<uint4*>(base + r * ld);  // q chunks [0, h / 8), k chunks [h / 8, h / 4)
+  const int hc = h >> 3;
+  uint4 u[2][NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    u[0][i] = v[lane + 32 * i];
+    u[1][i] = v[hc + lane + 32 * i];
+  }
+  float s[2] = {0.f, 0.f};
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u[p][i]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(b2[q]);
+        s[p] = fmaf(f.x, f.x, fmaf(f.y, f.y, s[p]));
+      }
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    s[0] += __shfl_xor_sync(0xffffffffu, s[0], o);
+    s[1] += __shfl_xor_sync(0xffffffffu, s[1], o);
+  }
+  float2 cs[4] = {make_float2(1.f, 0.f), make_float2(1.f, 0.f), make_float2(1.f, 0.f), make_float2(1.f, 0.f)};
+  if (rope) {
+    int nt, nh;
+    wan_rope_split(dh, &nt, &nh);
+    const int tok = static_cast<int>(r % tpf);
+    const int yy = tok / width, xx = tok % width;
+    const int j0 = (lane % (dh >> 3)) * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q;
+      cs[q] = j < nt ? ttab[(r / tpf) * nt + j]
+                     : (j < nt + nh ? ytab[static_cast<int64_t>(yy) * nh + j - nt]
+                                    : xtab[static_cast<int64_t>(xx) * nh + j - nt - nh]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const float inv = rsqrtf(s[p] / static_cast<float>(h) + static_cast<float>(kWanEps));
+    const float* gp = g + static_cast<int64_t>(p) * h;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + 32 * i;
+      __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&u[p][i]);
+      const float4 g0 = *reinterpret_cast<const float4*>(gp + 8 * c);
+      const float4 g1 = *reinterpret_cast<const float4*>(gp + 8 * c + 4);
+      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(b2[q]);
+        const float a = f.x * inv * gg[2 * q], b = f.y * inv * gg[2 * q + 1];
+        b2[q] = __floats2bfloat162_rn(a * cs[q].x - b * cs[q].y, a * cs[q].y + b * cs[q].x);
+      }
+      v[p * hc + c] = u[p][i];
+    }
+  }
+}
+
 __global__ void k_wan_rope_frames(const int64_t* __restrict__ frame_ids, int nframes, int nt, float2* __restrict__ ttab) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nframes * nt) return;
@@ -355,6 +431,17 @@ void launch_wan_qk_bf16(bf16* base, int64_t ld, int64_t rows, int h, int heads, 
                tpf, width, rope);
   };
   const bool lanes_fit = dh % 8 == 0 && 32 % (dh / 8) == 0;
+  if (lanes_fit && nparts == 2 && part_stride == h && (h == 1536 || h == 256 || h == 512)) {
+    auto reg2 = [&](auto kern) {
+      launch_pdl(kern, dim3(blocks_for(rows, 8)), dim3(256), 0, st, base, ld, rows, h, dh, g, ttab, ytab, xtab, tpf,
+                 width, rope);
+    };
+    if (h == 1536) reg2(k_wan_qk2_bf16_reg<6>);
+    else if (h == 512) reg2(k_wan_qk2_bf16_reg<2>);
+    else reg2(k_wan_qk2_bf16_reg<1>);
+    count_launch();
+    return;
+  }
   switch (lanes_fit ? h : 0) {  // register-resident rows for the widths in use (Wan 1.3B / 14B, test models)
     case 256: reg(k_wan_qk_bf16_reg<1>); break;
     case 512: reg(k_wan_qk_bf16_reg<2>); break;

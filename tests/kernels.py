@@ -6,7 +6,7 @@ import os
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-TESTLIB_PATH = os.path.join(ROOT, "paper_2505_21070_b200", "lib", "libbp_cuda_test.so")
+TESTLIB_PATH = os.environ.get("BP_TESTLIB_PATH") or os.path.join(ROOT, "paper_2505_21070_b200", "lib", "libbp_cuda_test.so")
 
 i32, i64, f64 = C.c_int32, C.c_int64, C.c_double
 # kernel-level self-test hooks (include/bp_cuda_test.h), served by the test
