@@ -6,7 +6,8 @@
 part: "kernels" (tcgen05 GEMM epilogues, pair / single-CTA attention with and
 without a prefix segment, LayerNorm, through the kernel self-test library),
 "pipeline" (a bf16 and an fp32 two-stage loopback run of the mid config:
-embedding, capture copies, fp32 flash attention and tile GEMM, Euler steps),
+embedding, capture copies, fp32 flash attention and tile GEMM, Euler steps;
+and a bf16 run of the optional Wan block),
 or "all" (default). Shapes are small: the sanitizer instruments every access.
 """
 import os
@@ -52,6 +53,10 @@ def pipeline():
     for prec in ("bf16", "f32"):
         out = bp.run_pipeline(dict(base, precision=prec))
         assert all(np.isfinite(b["frames"]).all() for b in out["blocks"])
+    # the optional Wan block (dh = 128: modulated LayerNorm, the q/k RMSNorm +
+    # 3D RoPE kernel, gated-residual and tanh-GELU GEMM epilogues)
+    out = bp.run_pipeline(dict(base, precision="bf16", block="wan"))
+    assert all(np.isfinite(b["frames"]).all() for b in out["blocks"])
 
 
 if __name__ == "__main__":
