@@ -164,3 +164,25 @@ def test_cross_attention_production_launch(tlib):
     r = rel(got[sr], want)
     report(test="cross_attention_production_launch", q=rows, kv=n1, heads=heads, sampled_rows=len(sr), rel_l2=r)
     assert r < 1e-2, r
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(os.environ.get("BP_SLOW_PARITY") != "1",
+                    reason="the whole configs[1] video in fp32 takes ~10 min; set BP_SLOW_PARITY=1")
+def test_whole_configs1_video_bf16_vs_f32(bp):
+    """Error growth through the whole benchmarked video: configs[1] (30
+    layers, 3 blocks x 50 denoising steps, 150 passes, S = 18720, P = 6240)
+    in bf16 (the benchmarked path) against the fp32 verification path, per
+    emitted block (block 1 leaves the pipeline first, block 3 last)."""
+    base = dict(WAN13, layers=30, num_b=8, num_c=8, steps=50, blocks=3, devices=1)
+    t0 = time.time()
+    f32 = bp.run_pipeline(dict(base, precision="f32"))
+    t_f32 = time.time() - t0
+    b16 = bp.run_pipeline(dict(base, precision="bf16"))
+    per_block = [rel(x["frames"].ravel(), y["frames"].ravel()) for x, y in zip(b16["blocks"], f32["blocks"])]
+    la = np.concatenate([b["frames"].ravel() for b in b16["blocks"]])
+    lb = np.concatenate([b["frames"].ravel() for b in f32["blocks"]])
+    r_lat = rel(la, lb)
+    report(test="whole_video_bf16_vs_f32", workload="configs[1] 81 frames", layers=30, passes=150,
+           rel_l2_latents=r_lat, rel_l2_per_block=per_block, f32_run_s=round(t_f32, 1))
+    assert r_lat <= 2e-2, r_lat
