@@ -186,3 +186,27 @@ def test_whole_configs1_video_bf16_vs_f32(bp):
     report(test="whole_video_bf16_vs_f32", workload="configs[1] 81 frames", layers=30, passes=150,
            rel_l2_latents=r_lat, rel_l2_per_block=per_block, f32_run_s=round(t_f32, 1))
     assert r_lat <= 2e-2, r_lat
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(os.environ.get("BP_SLOW_PARITY") != "1",
+                    reason="40 layers of the 14B shape in fp32 take ~6 min; set BP_SLOW_PARITY=1")
+def test_wan14b_all_layers_bf16_vs_f32(bp):
+    """configs[4]'s shape through all 40 layers (h 5120, 40 heads, F 13824,
+    45 x 80 latent grid: S = 43200, P = 14400) for the bench's sample
+    schedule (2 blocks x 2 steps, 4 passes), bf16 against the fp32
+    verification path."""
+    base = dict(layers=40, hidden=5120, heads=40, ffn=13824, channels=64, height=45, width=80, context_len=512,
+                num_b=8, num_c=8, steps=2, blocks=2, devices=1, record_trace=True)
+    t0 = time.time()
+    f32 = bp.run_pipeline(dict(base, precision="f32"))
+    t_f32 = time.time() - t0
+    b16 = bp.run_pipeline(dict(base, precision="bf16"))
+    la = np.concatenate([b["frames"].ravel() for b in b16["blocks"]])
+    lb = np.concatenate([b["frames"].ravel() for b in f32["blocks"]])
+    r_lat = rel(la, lb)
+    r_eps = [rel(x["eps"], y["eps"]) for x, y in zip(b16["trace"], f32["trace"])]
+    report(test="wan14b_all_layers_bf16_vs_f32", layers=40, tokens=43200, prefix=14400, passes=len(r_eps),
+           rel_l2_latents=r_lat, rel_l2_eps_per_pass=r_eps, f32_run_s=round(t_f32, 1))
+    assert r_lat <= 2e-2, r_lat
+    assert max(r_eps) <= 3e-2, r_eps
