@@ -11,7 +11,13 @@ import sys
 
 import pytest
 
-pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+# The GPU pool has since closed compute-sanitizer (runs under it left GPUs
+# needing a reset), so these runs are opt-in: BP_RUN_SANITIZER=1 on a box
+# where the tool is allowed. The clean memcheck / racecheck / synccheck runs of
+# this round's kernels on B200 are recorded in profiles/r02_sanitizer.md.
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(os.environ.get("BP_RUN_SANITIZER") != "1",
+                                 reason="compute-sanitizer is closed on the GPU pool; set BP_RUN_SANITIZER=1 to run")]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
 
@@ -56,6 +62,8 @@ def sanitize(tool, *cmd, timeout=900):
                          capture_output=True, text=True, timeout=timeout, cwd=ROOT, env=env)
     text = out.stdout + out.stderr
     print(text[-3000:])
+    if "closed on this pool" in text:
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     return out.returncode, text
 
 
