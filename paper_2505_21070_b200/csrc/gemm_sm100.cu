@@ -34,10 +34,6 @@ constexpr int BM = 128, BN = 256, BK = 64;
 constexpr uint32_t A_BYTES = BM * BK * 2;
 constexpr uint32_t B_BYTES = BN * BK * 2;
 constexpr int kThreads = 192;
-#ifndef BP_GEMM_PREFETCH
-#define BP_GEMM_PREFETCH 0
-#endif
-constexpr int kGemmPrefetch = BP_GEMM_PREFETCH;  // k-steps of A prefetched into L2 ahead of the ring
 
 __device__ __forceinline__ float gelu_erf_f(float v) { return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f)); }
 
@@ -161,19 +157,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ---- TMA producer: own A tile + own half of the shared weight tile ----
     int stage = 0;
     uint32_t phase = 0;
-    // L2 prefetch of this CTA's A box kGemmPrefetch k-steps beyond the one being
-    // loaded (continuing into the next tile): a first touch of A that misses L2
-    // then costs an L2 hit inside the ring's window instead of an HBM round trip.
-    int pf_pair = cluster, pf_kb = 0;
-    for (int i = 0; i < kGemmPrefetch; ++i)
-      if (++pf_kb == num_k) { pf_kb = 0; pf_pair += nclusters; }
     for (int pair = cluster; pair < total; pair += nclusters) {
       const int m_blk = (pair / n_tiles) * 2 + rank, n_blk = pair % n_tiles;
       for (int kb = 0; kb < num_k; ++kb) {
-        if (kGemmPrefetch > 0) {
-          if (pf_pair < total) tc::tma_prefetch_l2_2d_elect(&map_a, pf_kb * BK, ((pf_pair / n_tiles) * 2 + rank) * BM);
-          if (++pf_kb == num_k) { pf_kb = 0; pf_pair += nclusters; }
-        }
         tc::mbar_wait(&empty[stage], phase ^ 1);
         // own A rows + own weight half, both completing on the leader's barrier
         const uint32_t lf = tc::mapa_shared(tc::smem_u32(&full[stage]), 0);

@@ -202,17 +202,6 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
     if (globaltimer_ns() - t0 > 5000000000ULL) __trap();
   }
 }
-// L2 prefetch of one 2-D TMA box (no shared memory, no barrier), one elected lane.
-__device__ __forceinline__ void tma_prefetch_l2_2d_elect(const CUtensorMap* map, int c0, int c1) {
-  asm volatile(
-      "{\n"
-      ".reg .pred e;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "@e cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n"
-      "}\n" ::"l"(reinterpret_cast<uint64_t>(map)),
-      "r"(c0), "r"(c1)
-      : "memory");
-}
 // 2-D TMA load into this CTA's shared memory whose complete_tx lands on the
 // mbarrier at shared::cluster address `bar_cluster` (the leader CTA's).
 __device__ __forceinline__ void tma_load_2d_cg2_elect(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
