@@ -321,6 +321,8 @@ typedef struct {
   int64_t boundary_copies;  /* device copies of hidden states at stage boundaries in the last
                                run (0 for the multi-process transports: received in place) */
   int64_t registered_buffers; /* stage-boundary buffers NCCL accepted for registration */
+  int64_t fused_sends;      /* hidden states this rank wrote into the next rank's receive slot
+                               from the last layer's residual GEMM epilogue (IPC, bf16) */
 } bp_pipeline_stats;
 BP_API bp_status bp_pipeline_get_stats(bp_pipeline* p, bp_pipeline_stats* out);
 /* Per-kernel-class timing with CUDA events on the launching stream (0/1). */

@@ -76,7 +76,7 @@ class PipelineStats(C.Structure):
                 ("boundary_bytes", i64), ("attn_ms", f64), ("gemm_ms", f64), ("cross_ms", f64),
                 ("attn_launches", i64), ("gemm_launches", i64), ("cross_launches", i64),
                 ("ln_ms", f64), ("ln_launches", i64), ("h2d_bytes", i64), ("d2h_bytes", i64),
-                ("boundary_copies", i64), ("registered_buffers", i64)]
+                ("boundary_copies", i64), ("registered_buffers", i64), ("fused_sends", i64)]
 
 
 EMIT_FN = C.CFUNCTYPE(None, C.c_void_p, i64, i64, P(f64), P(i32), i32, P(i64))

@@ -209,7 +209,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int pair = cluster; pair < total; pair += nclusters) {
       const int m_blk = (pair / n_tiles) * 2 + rank, n_blk = pair % n_tiles;
       const int row0 = m_blk * BM + q * 32;  // this warp's 32 rows
-      auto chunk = [&](int c, const float4 (&old)[8]) {
+      auto chunk = [&](int c) {
         uint32_t r[32];
         tc::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c), r);
         tc::tmem_ld_wait();
@@ -245,7 +245,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc::bulk_commit_group();
           }
           red_buf ^= 1;
-          (void)old;
           return;
         }
         if (EPI == kGemmStoreBf16 || EPI == kGemmGeluBf16 || EPI == kGemmGeluTanhBf16) {
@@ -278,6 +277,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               *reinterpret_cast<uint4*>(static_cast<bf16*>(Cv) + static_cast<int64_t>(grow) * ldc + gcol) = v;
           }
         } else {
+          // fp32 store; kGemmResidualOutF32 adds the residual R (read here,
+          // coalesced along rows) and writes R + acc to C, which may live on
+          // another GPU (the next stage's receive slot): the residual add and
+          // the stage-boundary send in one pass over the tile.
+          float4 res[8];
+          if (EPI == kGemmResidualOutF32) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int grow = row0 + 4 * i + (lane >> 3), gcol = col0 + (lane & 7) * 4;
+              res[i] = grow < M && gcol < N
+                           ? __ldg(reinterpret_cast<const float4*>(gate.resid + static_cast<int64_t>(grow) * gate.ldr + gcol))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
 #pragma unroll
           for (int u = 0; u < 8; ++u)
             tc::st_shared_v4(slab_addr(lane, u), r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]);
@@ -289,8 +302,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             float4 o = make_float4(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w));
             const int grow = row0 + rr, gcol = col0 + u * 4;
             if (grow < M && gcol < N) {
-              if (EPI == kGemmResidualF32) {
-                o.x = old[i].x + o.x; o.y = old[i].y + o.y; o.z = old[i].z + o.z; o.w = old[i].w + o.w;
+              if (EPI == kGemmResidualOutF32) {
+                o.x = res[i].x + o.x; o.y = res[i].y + o.y; o.z = res[i].z + o.z; o.w = res[i].w + o.w;
               }
               *reinterpret_cast<float4*>(static_cast<float*>(Cv) + static_cast<int64_t>(grow) * ldc + gcol) = o;
             }
@@ -303,9 +316,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc::fence_after_sync();
 #pragma unroll 1
       for (int c = 0; c < BN; c += 64) {
-        float4 old[8];
-        chunk(c, old);
-        chunk(c + 32, old);
+        chunk(c);
+        chunk(c + 32);
       }
       tc::fence_before_sync();
       __syncwarp();  // the leader's MMA reuses the accumulator once both CTAs drained it
@@ -437,6 +449,9 @@ void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int
   if (epi == kGemmResidualGatedF32 &&
       ((reinterpret_cast<uintptr_t>(gate.gate) & 15) || gate.grp_stride % 4 || gate.grp_rows < 1))
     fail(BP_ERR_INTERNAL, "gate table must be 16-byte aligned");
+  if (epi == kGemmResidualOutF32 &&
+      ((reinterpret_cast<uintptr_t>(gate.resid) | reinterpret_cast<uintptr_t>(C)) & 15 || gate.ldr % 4 || ldc % 4))
+    fail(BP_ERR_INTERNAL, "residual-out GEMM buffers must be 16-byte aligned");
   const CUtensorMap ma = cached_map(A, static_cast<uint64_t>(M), static_cast<uint64_t>(K), static_cast<uint64_t>(lda), BM, BK);
   // each CTA of the pair stages one 128-row half of the 256-row weight tile
   const CUtensorMap mbh =
@@ -452,6 +467,7 @@ void launch_gemm_tc(const bf16* A, int64_t lda, const bf16* W, int M, int N, int
     case kGemmResidualF32: launch_pair<kGemmResidualF32>(ma, mbh, M, N, K, C, ldc, mc, st, gate); break;
     case kGemmResidualGatedF32: launch_pair<kGemmResidualGatedF32>(ma, mbh, M, N, K, C, ldc, mc, st, gate); break;
     case kGemmGeluTanhBf16: launch_pair<kGemmGeluTanhBf16>(ma, mbh, M, N, K, C, ldc, mc, st, gate); break;
+    case kGemmResidualOutF32: launch_pair<kGemmResidualOutF32>(ma, mbh, M, N, K, C, ldc, mc, st, gate); break;
     default: launch_pair<kGemmStoreF32>(ma, mbh, M, N, K, C, ldc, mc, st, gate); break;
   }
   count_launch();

@@ -256,6 +256,8 @@ __global__ void __launch_bounds__(256) k_gemm_simt(const bf16* __restrict__ A, i
       else if (epi == kGemmResidualF32) static_cast<float*>(Cv)[o] += v;
       else if (epi == kGemmResidualGatedF32)
         static_cast<float*>(Cv)[o] += gate.gate[(gm / gate.grp_rows) * gate.grp_stride + gn] * v;
+      else if (epi == kGemmResidualOutF32)
+        static_cast<float*>(Cv)[o] = gate.resid[static_cast<int64_t>(gm) * gate.ldr + gn] + v;
       else if (epi == kGemmGeluTanhBf16)
         static_cast<bf16*>(Cv)[o] = __float2bfloat16_rn(0.5f * v * (1.f + tanhf(0.7978845608f * (v + 0.044715f * v * v * v))));
       else static_cast<float*>(Cv)[o] = v;
@@ -358,6 +360,8 @@ void launch_gemm_bf16(const bf16* A, int64_t lda, const bf16* W, int M, int N, i
   if (M <= 0 || N <= 0) return;
   if (epi == kGemmResidualGatedF32 && (!gate.gate || gate.grp_rows < 1))
     fail(BP_ERR_INTERNAL, "gated residual GEMM needs a gate table");
+  if (epi == kGemmResidualOutF32 && (!gate.resid || gate.ldr < N))
+    fail(BP_ERR_INTERNAL, "residual-out GEMM needs the residual input");
   if (g_gemm_impl >= 1) launch_gemm_tc(A, lda, W, M, N, K, C, ldc, epi, st, gate);
   else launch_gemm_simt(A, lda, W, M, N, K, C, ldc, epi, st, gate);
 }

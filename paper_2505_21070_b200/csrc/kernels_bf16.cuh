@@ -37,14 +37,19 @@ enum GemmEpi {
   kGemmResidualF32 = 2,  // C fp32 = C + acc (x += sublayer)  (forward_chunk, model.cpp:325-331)
   kGemmStoreF32 = 3,     // C fp32 = acc
   kGemmResidualGatedF32 = 4,  // C fp32 = C + gate[row group] * acc (Wan gated residual)
-  kGemmGeluTanhBf16 = 5       // C bf16 = gelu_tanh(acc)           (Wan FFN)
+  kGemmGeluTanhBf16 = 5,      // C bf16 = gelu_tanh(acc)           (Wan FFN)
+  kGemmResidualOutF32 = 6     // C fp32 = R + acc, R = gate.resid: the residual add written to
+                              // another buffer (the next rank's receive slot, fused send)
 };
 // Per-row-group gate of kGemmResidualGatedF32: row r scales by
 // gate + (r / grp_rows) * grp_stride (one fp32 vector of N per group).
+// kGemmResidualOutF32 reads the residual from resid (row stride ldr).
 struct GemmGate {
   const float* gate = nullptr;
   int grp_rows = 1;
   int64_t grp_stride = 0;
+  const float* resid = nullptr;
+  int64_t ldr = 0;
 };
 // C[M,N] = A[M,K] (bf16, row stride lda) x W[N,K]^T (bf16, K-major weights).
 void launch_gemm_bf16(const bf16* A, int64_t lda, const bf16* W, int M, int N, int K, void* C,

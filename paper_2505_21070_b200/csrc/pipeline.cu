@@ -159,6 +159,12 @@ __global__ void k_wait_geq(const uint32_t* addr, uint32_t v, int soft) {
   }
 }
 static const bool g_ipc_soft = std::getenv("BP_IPC_SOFT") != nullptr;
+// BP_IPC_FUSED_SEND=0: send hidden states with a peer copy after the forward
+// instead of from the last GEMM's epilogue (A/B and tests)
+static const bool g_ipc_fused = [] {
+  const char* e = std::getenv("BP_IPC_FUSED_SEND");
+  return !(e && e[0] == '0');
+}();
 void stream_wait_geq(cudaStream_t s, const uint32_t* addr, uint32_t v) {
   k_wait_geq<<<1, 32, 0, s>>>(addr, v, g_ipc_soft ? 1 : 0);
   BP_CUDA(cudaGetLastError());
@@ -647,6 +653,7 @@ void Pipeline::run_rank0_loopback(bp_emit_fn emit, void* user) {
   stats.boundary_bytes = boundary;
   stats.boundary_copies = copies() - copies_at_start;
   stats.registered_buffers = 0;
+  stats.fused_sends = 0;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (emit) {
@@ -720,19 +727,35 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
   BP_CUDA(cudaEventCreate(&e1));
   BP_CUDA(cudaEventRecord(e0, st_));
   const int64_t copies_at_start = s.input_copies();
-  int64_t boundary = 0;
+  int64_t boundary = 0, fused_sends = 0;
   const bool use_ipc = ipc();
   // the event after which pass i's ring slot may be overwritten: its send
   // (the slot holds the outgoing hidden state, or the last rank's eps), and
   // on the last rank also its forward (the x slot is not sent from there)
   auto slot_free = [&](int64_t i) { return ev_sent[i]; };
 
+  // Fused send (IPC, bf16): the last layer's FFN-down GEMM writes x + FFN(x)
+  // straight into the next rank's receive slot; the slot-free wait moves onto
+  // the compute stream right before that GEMM, and the send only publishes.
+  const bool fused_send = use_ipc && !last && s.fuses_send() && g_ipc_fused;
+  struct SlotWait { const uint32_t* addr; uint32_t v; };
   auto forward_pass = [&](const SchedPass& p, const void* payload) {
     StageInput in;
     before_stage(p, j, s, &in);
     in.payload = payload;
     in.slot = static_cast<int>(p.index % kRing);
     const int64_t i = p.index;
+    SlotWait sw{};
+    if (fused_send) {
+      sw.addr = ipc_cnt(ipc_block_.as<char>(), 2);
+      sw.v = i >= kRing ? ipc_epoch_ + static_cast<uint32_t>(i - kRing + 1) : ipc_epoch_;
+      in.out = ipc_slot(peer_next_, 0, i);
+      in.before_out = [](cudaStream_t st, void* u) {
+        const SlotWait* w = static_cast<const SlotWait*>(u);
+        stream_wait_geq(st, w->addr, w->v);
+      };
+      in.before_out_user = &sw;
+    }
     if (i >= kRing && (j == 0 || last)) BP_CUDA(cudaStreamWaitEvent(st_, slot_free(i - kRing), 0));
     char name[48];
     std::snprintf(name, sizeof name, "pass %lld stage %d", static_cast<long long>(i), j);
@@ -746,7 +769,10 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
   auto send_to = [&](ncclComm_t comm, cudaStream_t ss, const SchedPass& p, const void* buf, int peer,
                      size_t count, ncclDataType_t dt) {
     BP_CUDA(cudaStreamWaitEvent(ss, ev_fwd[p.index], 0));
-    if (use_ipc) {
+    if (use_ipc && fused_send && peer >= 0) {
+      stream_write(ss, ipc_cnt(peer_next_, 0), ipc_epoch_ + static_cast<uint32_t>(p.index + 1));
+      ++fused_sends;
+    } else if (use_ipc) {
       const bool eps_ch = peer < 0;
       ipc_send(eps_ch ? peer_eps_ : peer_next_, eps_ch ? 1 : 0, p.index, buf,
                count * (dt == ncclFloat64 ? 8 : 4), ss);
@@ -873,6 +899,7 @@ void Pipeline::run_nccl(bp_emit_fn emit, void* user) {
   stats.boundary_bytes = boundary;
   stats.boundary_copies = s.input_copies() - copies_at_start;
   stats.registered_buffers = registered_;
+  stats.fused_sends = fused_sends;
   for (int64_t i = 0; i < P; ++i) {
     cudaEventDestroy(ev_fwd[i]); cudaEventDestroy(ev_recv[i]);
     cudaEventDestroy(ev_sent[i]); cudaEventDestroy(ev_used[i]);

@@ -44,6 +44,18 @@ bp_status bp_selftest_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int3
     BP_CUDA(cudaMemcpy(da.p, A, static_cast<size_t>(M) * lda * 2, cudaMemcpyHostToDevice));
     BP_CUDA(cudaMemcpy(dw.p, W, static_cast<size_t>(N) * K * 2, cudaMemcpyHostToDevice));
     BP_CUDA(cudaMemcpy(dc.p, C, static_cast<size_t>(M) * ldc * cb, cudaMemcpyHostToDevice));
+    if (epi == bp::kGemmResidualOutF32) {  // C (in) is the residual, C (out) = C + acc from another buffer
+      bp::DevBuf dout;
+      dout.alloc(static_cast<size_t>(M) * ldc * 4);
+      BP_CUDA(cudaMemset(dout.p, 0xff, static_cast<size_t>(M) * ldc * 4));
+      bp::GemmGate g{};
+      g.resid = dc.as<float>();
+      g.ldr = ldc;
+      bp::launch_gemm_bf16(da.as<bp::bf16>(), lda, dw.as<bp::bf16>(), M, N, K, dout.p, ldc, epi, nullptr, g);
+      BP_CUDA(cudaDeviceSynchronize());
+      BP_CUDA(cudaMemcpy(C, dout.p, static_cast<size_t>(M) * ldc * 4, cudaMemcpyDeviceToHost));
+      return;
+    }
     bp::launch_gemm_bf16(da.as<bp::bf16>(), lda, dw.as<bp::bf16>(), M, N, K, dc.p, ldc, epi, nullptr);
     BP_CUDA(cudaDeviceSynchronize());
     BP_CUDA(cudaMemcpy(C, dc.p, static_cast<size_t>(M) * ldc * cb, cudaMemcpyDeviceToHost));
@@ -126,14 +138,22 @@ bp_status bp_bench_gemm(int32_t device, int32_t M, int32_t N, int32_t K, int32_t
     bp::k_fill_rand_bf16<<<1024, 256>>>(da.as<bp::bf16>(), static_cast<int64_t>(M) * K, 1, 1.0f);
     bp::k_fill_rand_bf16<<<1024, 256>>>(dw.as<bp::bf16>(), static_cast<int64_t>(N) * K, 2, 0.05f);
     BP_CUDA(cudaMemset(dc.p, 0, static_cast<size_t>(M) * N * cb));
+    bp::DevBuf dr;  // kGemmResidualOutF32: the residual input (the output goes to dc)
+    bp::GemmGate g{};
+    if (epi == bp::kGemmResidualOutF32) {
+      dr.alloc(static_cast<size_t>(M) * N * 4);
+      BP_CUDA(cudaMemset(dr.p, 0, static_cast<size_t>(M) * N * 4));
+      g.resid = dr.as<float>();
+      g.ldr = N;
+    }
     cudaStream_t st;
     BP_CUDA(cudaStreamCreate(&st));
-    for (int i = 0; i < 3; ++i) bp::launch_gemm_bf16(da.as<bp::bf16>(), K, dw.as<bp::bf16>(), M, N, K, dc.p, N, epi, st);
+    for (int i = 0; i < 3; ++i) bp::launch_gemm_bf16(da.as<bp::bf16>(), K, dw.as<bp::bf16>(), M, N, K, dc.p, N, epi, st, g);
     cudaEvent_t e0, e1;
     BP_CUDA(cudaEventCreate(&e0));
     BP_CUDA(cudaEventCreate(&e1));
     BP_CUDA(cudaEventRecord(e0, st));
-    for (int i = 0; i < iters; ++i) bp::launch_gemm_bf16(da.as<bp::bf16>(), K, dw.as<bp::bf16>(), M, N, K, dc.p, N, epi, st);
+    for (int i = 0; i < iters; ++i) bp::launch_gemm_bf16(da.as<bp::bf16>(), K, dw.as<bp::bf16>(), M, N, K, dc.p, N, epi, st, g);
     BP_CUDA(cudaEventRecord(e1, st));
     BP_CUDA(cudaEventSynchronize(e1));
     float t = 0;

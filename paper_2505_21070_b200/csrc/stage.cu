@@ -481,6 +481,7 @@ const void* Stage::forward(const StageInput& in) {
     if (f < 0 || f >= in.nframes) fail(BP_ERR_DIMENSION, "capture frame out of range");
   if (xs_.empty()) set_ring(1, in.tokens);
   if (in.slot < 0 || in.slot >= ring_depth()) fail(BP_ERR_INTERNAL, "residual ring slot out of range");
+  if (in.out && !fuses_send()) fail(BP_ERR_INTERNAL, "fused send requested on a stage that cannot fuse it");
   if (wan_) {
     if (in.use_prev == 2 || in.use_prev == 4 || in.mode == BP_CACHE_RECOMPUTE || in.record_inputs)
       fail(BP_ERR_CONFIG, "wan block supports the resident K/V cache and no cache, not the recompute route");
@@ -890,6 +891,7 @@ const void* Stage::forward_bf16(const StageInput& in) {
     }
   }
   const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(dh_)));
+  const bool fused = in.out != nullptr;
 
   Entry nc, nr;
   bf16* qkv = qkv_.as<bf16>();
@@ -980,8 +982,17 @@ const void* Stage::forward_bf16(const StageInput& in) {
     prof_mark(2, true);
     launch_gemm_bf16(ln, H, static_cast<const bf16*>(w.w1), static_cast<int>(S), F_, h_, hm, F_,
                      kGemmGeluBf16, st);
-    launch_gemm_bf16(hm, F_, static_cast<const bf16*>(w.w2), static_cast<int>(S), h_, F_, x, H,
-                     kGemmResidualF32, st);
+    if (fused && li == nl - 1) {  // x + FFN(x) written into the next rank's receive slot
+      if (in.before_out) in.before_out(st, in.before_out_user);
+      GemmGate g{};
+      g.resid = x;
+      g.ldr = H;
+      launch_gemm_bf16(hm, F_, static_cast<const bf16*>(w.w2), static_cast<int>(S), h_, F_, in.out, H,
+                       kGemmResidualOutF32, st, g);
+    } else {
+      launch_gemm_bf16(hm, F_, static_cast<const bf16*>(w.w2), static_cast<int>(S), h_, F_, x, H,
+                       kGemmResidualF32, st);
+    }
     prof_mark(2, false);
     nvtxRangePop();
   }
@@ -995,7 +1006,7 @@ const void* Stage::forward_bf16(const StageInput& in) {
     launch_gemm_f32_tile(x, H, static_cast<const float*>(w_out_), C_, static_cast<int>(S), C_, h_, eps, C_, false, st);
     return eps;
   }
-  return x;
+  return fused ? in.out : x;
 }
 
 void Stage::tag_entries(int64_t block_id, int level) {

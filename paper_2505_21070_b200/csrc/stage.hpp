@@ -26,6 +26,13 @@ struct StageInput {
   int mode = BP_CACHE_DISABLED;
   int use_prev = 0;                    // 0 none, 1 resident cache, 2 resident recording
   int slot = 0;                        // residual-stream ring slot (see Stage::set_ring)
+  // Fused send (bf16 reference block, not the last stage; see fuses_send()):
+  // the last layer's FFN-down GEMM writes x + FFN(x) straight into out (the
+  // next rank's receive slot, a peer mapping) instead of x, after
+  // before_out(stream, user) has enqueued the wait for that slot to be free.
+  void* out = nullptr;
+  void (*before_out)(cudaStream_t, void*) = nullptr;
+  void* before_out_user = nullptr;
 };
 
 class Stage {
@@ -40,6 +47,9 @@ class Stage {
 
   bool is_first() const { return begin_ == 0; }
   bool is_last() const { return end_ == m_.layers; }
+  // Whether forward() honours StageInput::out (the bf16 tensor-core path of
+  // the reference block on a stage that sends a hidden state).
+  bool fuses_send() const { return prec_ == BP_PREC_BF16 && !wan_ && !is_last() && end_ > begin_; }
   int precision() const { return prec_; }
   size_t act_bytes() const;  // bytes per hidden element (8 fp64, 4 fp32/bf16-path residual)
   size_t eps_bytes() const { return prec_ == BP_PREC_F64 ? 8 : 4; }

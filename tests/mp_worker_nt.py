@@ -40,7 +40,8 @@ def main():
         np.savez(prefix + ".npz", **out)
     with open(f"{prefix}.rank{rank}.json", "w") as f:
         json.dump({"boundary_copies": st["boundary_copies"], "registered_buffers": st["registered_buffers"],
-                   "boundary_bytes": st["boundary_bytes"], "torch_loaded": "torch" in sys.modules}, f)
+                   "boundary_bytes": st["boundary_bytes"], "fused_sends": st["fused_sends"],
+                   "passes": st["passes"], "torch_loaded": "torch" in sys.modules}, f)
 
 
 if __name__ == "__main__":

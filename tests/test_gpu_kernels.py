@@ -45,6 +45,25 @@ def test_gemm_tcgen05(lib, M, N, K, epi, impl):
     assert np.linalg.norm(g - c) / np.linalg.norm(c) < (5e-3 if epi in (0, 1) else 1e-5)
 
 
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 512, 128), (1000, 1536, 1536), (64, 96, 64),
+                                   (257, 1536, 8960)])
+@pytest.mark.parametrize("impl", [3, 0])
+def test_gemm_residual_out_equals_residual(lib, M, N, K, impl):
+    """The fused-send epilogue (kGemmResidualOutF32: out = R + acc into a
+    separate buffer, the next rank's receive slot) equals the in-place TMA
+    reduce-add epilogue (x += acc) bitwise, so a fused send cannot change
+    the latents."""
+    rng = np.random.default_rng(M + N + K)
+    A = to_bf16_bits(rng.standard_normal((M, K)))
+    W = to_bf16_bits(rng.standard_normal((N, K)) / np.sqrt(K))
+    C0 = rng.standard_normal((M, N)).astype(np.float32)
+    lib.bp_set_kernel_impl(impl, DEFAULT_ATTN_IMPL)
+    inplace = gemm(lib, A, W, C0, 2)
+    out = gemm(lib, A, W, C0, 6)
+    lib.bp_set_kernel_impl(DEFAULT_GEMM_IMPL, DEFAULT_ATTN_IMPL)
+    assert np.array_equal(inplace, out)
+
+
 @pytest.mark.parametrize("impl", [3])
 def test_gemm_row_position_invariance(lib, impl):
     """A row's result does not depend on its M position (cached == recompute),

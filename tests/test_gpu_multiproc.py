@@ -93,7 +93,8 @@ def run_ranks_nt(cfg, n, tmp_path, runs=2):
     return np.load(prefix + ".npz"), stats
 
 
-@pytest.mark.parametrize("transport,prec,n", [("ipc", "bf16", 2), ("ipc", "f64", 3), ("nccl", "bf16", 2)])
+@pytest.mark.parametrize("transport,prec,n", [("ipc", "bf16", 2), ("ipc", "bf16", 3), ("ipc", "f64", 3),
+                                              ("nccl", "bf16", 2)])
 def test_file_bootstrap_without_torch(bp, tmp_path, transport, prec, n):
     """No PyTorch anywhere in the ranks; stage boundaries received in place
     (zero device copies of hidden states); bitwise == the serial oracle."""
@@ -107,6 +108,30 @@ def test_file_bootstrap_without_torch(bp, tmp_path, transport, prec, n):
         assert np.array_equal(got[f"run{r}"], ref)
     assert all(not s["torch_loaded"] for s in stats)
     assert all(s["boundary_copies"] == 0 for s in stats), stats
+    # IPC + bf16: every hidden state is written into the next rank's slot by
+    # the last layer's residual GEMM epilogue (the fused send), no peer copy
+    fused = transport == "ipc" and prec == "bf16"
+    assert [s["fused_sends"] for s in stats] == [s["passes"] if fused and r < n - 1 else 0
+                                                 for r, s in enumerate(stats)], stats
+
+
+def test_ipc_fused_send_equals_copy_send(bp, tmp_path, monkeypatch):
+    """The fused send (epilogue stores into the peer slot) and the peer-copy
+    send (BP_IPC_FUSED_SEND=0) give the same latents, bitwise, over three
+    ranks with an uneven layer split (a middle rank both receives and fuses)."""
+    base = dict(G["mid"]["config"], precision="bf16", steps=3, blocks=2, layers=4)
+    want = bp.serial_oracle(base)
+    ref = np.concatenate([b["frames"].ravel() for b in want["blocks"]])
+    split = dict(base, devices=3, transport="ipc", layer_split=[1, 2, 1])
+    (tmp_path / "fused").mkdir()
+    (tmp_path / "copy").mkdir()
+    got, stats = run_ranks_nt(split, 3, tmp_path / "fused", runs=1)
+    assert np.array_equal(got["run0"], ref)
+    assert stats[0]["fused_sends"] > 0 and stats[1]["fused_sends"] > 0
+    monkeypatch.setenv("BP_IPC_FUSED_SEND", "0")
+    got2, stats2 = run_ranks_nt(split, 3, tmp_path / "copy", runs=1)
+    assert np.array_equal(got2["run0"], ref)
+    assert all(s["fused_sends"] == 0 for s in stats2)
 
 
 @pytest.mark.parametrize("prec", ["f64", "bf16"])

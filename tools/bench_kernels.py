@@ -33,7 +33,8 @@ if what in ("attn", "all"):
         print(f"attn impl={impl} {tag:12s} ms {ms.value:.4f} TF {tf:.1f}")
 if what in ("gemm", "all"):
     for m, n, k, epi, tag in ((18720, 4608, 1536, 0, "qkv bf16"), (18720, 1536, 1536, 2, "o resid"),
-                              (18720, 8960, 1536, 1, "ffn1 gelu"), (18720, 1536, 8960, 2, "ffn2 resid")):
+                              (18720, 8960, 1536, 1, "ffn1 gelu"), (18720, 1536, 8960, 2, "ffn2 resid"),
+                              (18720, 1536, 8960, 6, "ffn2 resid-out (fused send)")):
         if only not in tag:
             continue
         assert lib.bp_bench_gemm(0, m, n, k, epi, iters, ctypes.byref(ms)) == 0
