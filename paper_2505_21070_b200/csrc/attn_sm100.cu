@@ -413,7 +413,7 @@ constexpr uint32_t P2_Q = 0;
 constexpr uint32_t P2_K = P2_Q + 2 * TILE;
 constexpr uint32_t P2_V = P2_K + P2_KST * P2_KT;
 constexpr uint32_t P2_BAR = P2_V + P2_VST * P2_VT;
-constexpr uint32_t P2_SMEM_BYTES = P2_BAR + 256 + 1024;
+constexpr uint32_t P2_SMEM_BYTES = P2_BAR + 512 + 1024;  // 37 mbarriers + the TMEM slot, then alignment slack
 static_assert(P2_SMEM_BYTES <= 232448, "pair attention exceeds the 227 KB smem limit");
 
 struct AttnMapsP2 {
@@ -438,8 +438,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
   uint64_t* v_empty = v_full + P2_VST;      // [P2_VST] each CTA
   uint64_t* s_full = v_empty + P2_VST;      // [tile][buffer] each CTA
   uint64_t* p_full = s_full + 4;            // [tile][buffer] leader, 8 warp arrivals
-  uint64_t* pv_done = p_full + 4;           // [tile] each CTA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  uint64_t* pv_done = p_full + 4;           // [tile] each CTA, one phase per PV
+  uint64_t* o_done = pv_done + 2;           // [tile] each CTA, one phase: the last PV
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const uint32_t rank = tc::cluster_ctarank();
@@ -468,6 +469,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
     }
     tc::mbar_init(&pv_done[0], 1);
     tc::mbar_init(&pv_done[1], 1);
+    tc::mbar_init(&o_done[0], 1);
+    tc::mbar_init(&o_done[1], 1);
     tc::fence_mbarrier_init_cluster();
   }
   if (warp == 1) tc::tmem_alloc_cg2<512>(tmem_slot);
@@ -541,6 +544,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
           tc::mbar_wait_cluster(&p_full[x * 2 + (j & 1)], (j >> 1) & 1);
           tc::fence_after_sync();
           pv(x, j);
+          // tile x's epilogue barrier: completes with its last PV (and every
+          // MMA issued before it), not behind the other tile's last PV
+          if (j == T - 1) tc::mma_commit_cg2_multicast_elect(&o_done[x], kBoth);
         }
         tc::mma_commit_cg2_multicast_elect(&v_empty[j % P2_VST], kBoth);
         if (j + 2 < T) qk_pair(j + 2);  // S buffer j & 1 is free once PV(j) is issued (in-order)
@@ -602,11 +608,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
       l2 = __ffma2_rn(l2, make_float2(corr, corr), __fadd2_rn(ls_a, ls_b));
       m_used = m_new;
       // O must hold PV(j-1) before it is rescaled. pv_done completes one phase
-      // per step and is observed only here (rarely) and by the epilogue: the
-      // parity wait is exact because PV(j) cannot complete before this warp
-      // arrives P(j). Observing every phase (which compute-sanitizer's
-      // synccheck asks for; kObserveAll, BP_ATTN_OBSERVE_ALL=1, is the build
-      // tests/test_gpu_sanitizer.py runs) stalls the softmax behind the
+      // per step and is observed only here (rarely). A parity wait is exact
+      // only when at most one phase can be outstanding, and here it is: S(j)
+      // completing means PV(j-2) completed (QK(j) is issued after PV(j-2),
+      // and a commit tracks every earlier MMA), and PV(j) cannot complete
+      // before this warp arrives P(j). The epilogue has no S(T) to bound it
+      // (a parity wait on pv_done there could pass on PV(T-3)'s phase while
+      // PV(T-2) and PV(T-1) are still running; seen when another process
+      // time-slices the GPU), so it waits on o_done, which completes once.
+      // Observing every phase (which compute-sanitizer's synccheck asks for;
+      // kObserveAll, BP_ATTN_OBSERVE_ALL=1) stalls the softmax behind the
       // tensor pipe: 1450 vs 1497 TF/s, round 2.
       if (j >= 1 && __any_sync(0xffffffffu, need)) {
         tc::mbar_wait_cluster(&pv_done[x], (j - 1) & 1);
@@ -630,7 +641,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PP_THREADS, 1)
       if (lane == 0) tc::mbar_arrive_cluster(p_full_leader + static_cast<uint32_t>(b * 8));
     }
     if (T >= 1) {
-      tc::mbar_wait_cluster(&pv_done[x], (T - 1) & 1);
+      if (kObserveAll) tc::mbar_wait_cluster(&pv_done[x], (T - 1) & 1);
+      tc::mbar_wait_cluster(&o_done[x], 0);
       tc::fence_after_sync();
     }
     const int64_t row = static_cast<int64_t>(qpair) * 2 * BQ + x * BQ + r;

@@ -146,3 +146,18 @@ def test_ipc_pipeline_wan_block_equals_serial(bp, tmp_path, prec):
     ref = np.concatenate([b["frames"].ravel() for b in want["blocks"]])
     got = run_ranks(dict(base, devices=2, transport="ipc"), 2, tmp_path, runs=1)
     assert np.array_equal(got["run0"], ref), prec
+
+
+def test_ipc_fused_send_production_shape(bp, tmp_path):
+    """The fused send at the benchmarked token shape (Wan2.1-1.3B width, 480p
+    grid: S = 18720 rows of 1536 fp32 per hidden state, cached prefix 6240;
+    4 layers on 2 ranks, 2 blocks x 2 steps): the FFN-down epilogue writes
+    every tile into the peer slot; latents equal the single-process serial
+    run bitwise."""
+    base = dict(layers=4, hidden=1536, heads=12, ffn=8960, channels=64, height=30, width=52, context_len=512,
+                num_b=8, num_c=8, steps=2, blocks=2, precision="bf16", mode="single")
+    want = bp.serial_oracle(base)
+    ref = np.concatenate([b["frames"].ravel() for b in want["blocks"]])
+    got, stats = run_ranks_nt(dict(base, devices=2, transport="ipc"), 2, tmp_path, runs=1)
+    assert np.array_equal(got["run0"], ref)
+    assert stats[0]["fused_sends"] == stats[0]["passes"] > 0
