@@ -551,6 +551,8 @@ def main():
     h2d, d2h = est["h2d_bytes"], est["d2h_bytes"]
     if pool is not None:
         pipe.set_pool(None)
+    if dist is not None:  # no collectives after this point
+        dist.destroy_process_group()
 
     if rank != 0:
         return
